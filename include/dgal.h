@@ -1,0 +1,157 @@
+/*
+ * include/dgal.h — C ABI of libdgal.so: batched differentiable IoU of convex
+ * polygons on NVIDIA B200 (sm_100a).  From-scratch implementation of the data-
+ * parallel hot path of DGAL (arXiv 2011.11134).
+ *
+ * Citations: "P:n" = PAPER.md line n; "S:n" = SPEC.md line n; "R#" = reading in
+ * DESIGN.md §3 (the paper is silent or ambiguous there).
+ *
+ * Conventions common to every call
+ * --------------------------------
+ *  - Poly2<float,K> batches (P:39 `typedef Poly2<float, 4> Quad2`; "stored in a
+ *    fixed size point array ... in counter-clockwise order"): structure of arrays.
+ *    Vertex k of polygon n is (x[n*K + k], y[n*K + k]).  Exactly K vertices per
+ *    polygon, convex, counter-clockwise.  K is 4 or 8.
+ *  - ALL pointers are DEVICE pointers owned by the caller; the library never
+ *    allocates, never frees, keeps no global state and never synchronises the
+ *    host ("fix-size allocated memory").  Work is enqueued on `stream`
+ *    (a cudaStream_t; NULL = legacy default stream).
+ *  - Inputs are trusted: no CCW/convexity check on the device.
+ *    Invalid polygons give unspecified but finite results.
+ *  - Alignment: every x/y plane and gradient plane must be 16-byte aligned
+ *    (float4 loads/stores); xflags must be 2K-byte aligned (8 B for K=4, 16 B
+ *    for K=8); uint64 masks 8-byte aligned.  Violations -> DGAL_ERR_MISALIGNED.
+ *  - n == 0 (or m == 0) is a no-op returning DGAL_OK.
+ *  - Errors are detected on the host before launch (nothing is enqueued); a
+ *    launch failure (cudaGetLastError) returns DGAL_ERR_CUDA.  Asynchronous
+ *    device faults surface at the caller's next synchronisation.
+ *  - Results are bitwise deterministic: a pair's outputs depend only on that
+ *    pair, whatever the batch size, launch shape or GPU count.
+ *
+ * Flag bytes xflags (R2, following S:102-103): FromP1(i) = 0x40|i, FromP2(j) =
+ * 0x80|j, Cross(i,j) = 0xC0|i<<3|j (p1 edge i x p2 edge j), padding 0x00.  The
+ * nx valid bytes list the intersection's vertices counter-clockwise, rotated to
+ * start at the smallest byte (R3).  nx == 0 <=> empty intersection (IoU 0).
+ */
+#ifndef DGAL_H_
+#define DGAL_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DGAL_OK = 0,
+    DGAL_ERR_INVALID_ARG = 1,    /* negative size, NULL required pointer, bad cap */
+    DGAL_ERR_UNSUPPORTED_K = 2,  /* K not in {4, 8} */
+    DGAL_ERR_MISALIGNED = 3,     /* alignment rule above violated */
+    DGAL_ERR_CUDA = 4            /* kernel launch failed */
+} dgal_status;
+
+/* Same type as cudaStream_t / CUstream. */
+typedef struct CUstream_st *dgal_stream;
+
+/*
+ * Forward IoU of n independent pairs (the listing's `iou`):
+ *   intersection = intersect(p1, p2, xflags); nx = intersection.nvertices;
+ *   iou = area(intersection) / (area(p1) + area(p2) - area(intersection)).
+ * p1 is the subject, p2 the clipper (R4).
+ *   iou    [n]       float, overwritten
+ *   nx     [n]       uint8, overwritten (0 or 3..2K)
+ *   xflags [n * 2K]  uint8, overwritten (see flag bytes above)
+ */
+dgal_status dgal_iou_paired_fwd(int K, int64_t n,
+                                const float *x1, const float *y1,
+                                const float *x2, const float *y2,
+                                float *iou, uint8_t *nx, uint8_t *xflags,
+                                dgal_stream stream);
+
+/*
+ * Backward (the listing's `iou_backward` -> `iou_grad(p1, p2, grad, nx,
+ * xflags, grad1, grad2)`): propagates grad_iou[k] = dL/dIoU_k to every vertex of
+ * both polygons through the recorded nx/xflags of dgal_iou_paired_fwd on the
+ * same inputs.  Outputs are OVERWRITTEN (not accumulated; P:52 declares fresh
+ * grad1, grad2) in the input SoA layout (the polygon type holds the
+ * gradient).  nx == 0 -> zero gradient (S:303 subgradient).
+ *   grad_iou [n]; gx1, gy1, gx2, gy2 [n * K] float.
+ */
+dgal_status dgal_iou_paired_bwd(int K, int64_t n,
+                                const float *x1, const float *y1,
+                                const float *x2, const float *y2,
+                                const float *grad_iou,
+                                const uint8_t *nx, const uint8_t *xflags,
+                                float *gx1, float *gy1, float *gx2, float *gy2,
+                                dgal_stream stream);
+
+/*
+ * Pairwise IoU of a row block against all columns ("cartesian";
+ * north_star "full N x M pairwise matrices (detection/NMS)"), forward only.
+ * Rows play p1, columns p2 (R4).  Row r has global index row_offset + r; column c
+ * has global index c (for NMS pass the same score-sorted boxes as columns and
+ * the caller's row block as rows).
+ *   iou   [n_rows * m] float, row-major (ld = m), nullable.
+ *   mask  [n_rows * mask_words] uint64, nullable, mask_words >= ceil(m/64):
+ *         bit c of row r  <=>  c != row_offset + r  and  IoU(r, c) > nms_thresh
+ *         (strict, R14).  Bits c > row_offset + r form the classic NMS
+ *         suppression row; bits c < row_offset + r are the boxes that can
+ *         suppress box row_offset + r.
+ *   nbr_count [n_rows], nbr_idx [n_rows * nbr_cap] int32, nullable (both or
+ *         neither; requires mask):  the list of columns c < row_offset + r with
+ *         IoU > nms_thresh, in no particular order; nbr_count[r] is the true
+ *         count (it may exceed nbr_cap, then only nbr_cap entries are stored).
+ *         The library zeroes nbr_count itself (cudaMemsetAsync on `stream`).
+ */
+dgal_status dgal_iou_pairwise(int K, int64_t n_rows,
+                              const float *row_x, const float *row_y,
+                              int64_t m,
+                              const float *col_x, const float *col_y,
+                              int64_t row_offset,
+                              float *iou,
+                              float nms_thresh,
+                              uint64_t *mask, int64_t mask_words,
+                              int32_t *nbr_count, int32_t *nbr_idx, int32_t nbr_cap,
+                              dgal_stream stream);
+
+/*
+ * Greedy rotated NMS keep decision (north_star "rotated-NMS keep mask"; textbook
+ * greedy order, R14): boxes sorted by descending score; box i is kept iff no KEPT
+ * box k < i has IoU(i, k) > thr.  Computed as the unique fixed point of that
+ * recursion by parallel rounds: a box whose suppressors are all
+ * removed is kept, a box with a kept suppressor is removed.
+ *
+ * dgal_nms_round: ONE round over the rows [row_offset, row_offset + n_rows) of an
+ *   n_total-box problem (one rank's row block).  Reads the global status vector
+ *   `status` [n_total] (0 undecided, 1 kept, 2 removed), updates the entries of
+ *   its own rows in place, and atomically adds the number of its rows still
+ *   undecided to *undecided (device int32; the caller zeroes it).  Uses nbr lists
+ *   when nbr_count[r] <= nbr_cap, else scans the lower part of mask row r.
+ * dgal_nms_keep: all rounds for a single-GPU problem (rows = all n boxes,
+ *   row_offset = 0), in one persistent single-CTA kernel (no host round trips);
+ *   writes keep[i] in {0,1}.  status [n] is caller-provided scratch.
+ * mask / nbr_* are exactly the outputs of dgal_iou_pairwise with the same thr.
+ */
+dgal_status dgal_nms_round(int64_t n_total, int64_t n_rows, int64_t row_offset,
+                           const uint64_t *mask, int64_t mask_words,
+                           const int32_t *nbr_count, const int32_t *nbr_idx, int32_t nbr_cap,
+                           uint8_t *status, int32_t *undecided,
+                           dgal_stream stream);
+
+dgal_status dgal_nms_keep(int64_t n,
+                          const uint64_t *mask, int64_t mask_words,
+                          const int32_t *nbr_count, const int32_t *nbr_idx, int32_t nbr_cap,
+                          uint8_t *status, uint8_t *keep,
+                          dgal_stream stream);
+
+/* Human-readable name of a status code (static storage). */
+const char *dgal_status_string(dgal_status s);
+
+/* Build description: "libdgal <version> sm_100a nvcc <ver>" (static storage). */
+const char *dgal_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DGAL_H_ */

@@ -1,0 +1,155 @@
+"""paper_2011_11134_b200 — batched differentiable IoU of convex polygons on B200.
+
+Thin Python binding of libdgal.so (include/dgal.h), argument marshalling only:
+every step of the method runs in the CUDA kernels behind the C ABI.  PyTorch
+supplies device memory and the current CUDA stream.  There is no CPU path.
+
+Polygon batches are two float32 CUDA tensors (x, y) of shape [n, K] (or flat
+[n*K]), K in {4, 8}, vertices counter-clockwise.
+
+    iou, nx, xflags = iou_paired_fwd(x1, y1, x2, y2)
+    gx1, gy1, gx2, gy2 = iou_paired_bwd(x1, y1, x2, y2, g, nx, xflags)
+    iou, mask, cnt, idx = iou_pairwise(rx, ry, cx, cy, ...)    # N x M + NMS mask
+    keep = nms_keep(mask, cnt, idx)                           # greedy rotated NMS
+    loss-side autograd: PolyIoU.apply(x1, y1, x2, y2)
+"""
+from __future__ import annotations
+
+import torch
+
+from ._lib import DgalError, call, lib  # noqa: F401
+
+__all__ = ["iou_paired_fwd", "iou_paired_bwd", "iou_pairwise", "nms_round", "nms_keep",
+           "nms", "PolyIoU", "DgalError", "build_info"]
+
+
+def build_info() -> str:
+    return lib().dgal_build_info().decode()
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _plane(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name}: expected a CUDA tensor (there is no CPU path)")
+    if t.dtype != torch.float32:
+        raise TypeError(f"{name}: expected float32, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    return t
+
+
+def _K_n(x: torch.Tensor, K: int | None):
+    if K is None:
+        if x.dim() != 2:
+            raise ValueError("pass K= for flat coordinate planes")
+        K = x.shape[-1]
+    n = x.numel() // K
+    if n * K != x.numel():
+        raise ValueError("plane size is not a multiple of K")
+    return K, n
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def iou_paired_fwd(x1, y1, x2, y2, K: int | None = None, out=None):
+    """Forward IoU of n pairs (dgal_iou_paired_fwd).  Returns (iou f32[n], nx u8[n],
+    xflags u8[n, 2K]); `out` may supply those three tensors."""
+    for t, nm in ((x1, "x1"), (y1, "y1"), (x2, "x2"), (y2, "y2")):
+        _plane(t, nm)
+    K, n = _K_n(x1, K)
+    dev = x1.device
+    if out is None:
+        iou = torch.empty(n, dtype=torch.float32, device=dev)
+        nx = torch.empty(n, dtype=torch.uint8, device=dev)
+        xf = torch.empty((n, 2 * K), dtype=torch.uint8, device=dev)
+    else:
+        iou, nx, xf = out
+    call("dgal_iou_paired_fwd", K, n, _ptr(x1), _ptr(y1), _ptr(x2), _ptr(y2), _ptr(iou), _ptr(nx),
+         _ptr(xf), _stream(dev))
+    return iou, nx, xf
+
+
+def iou_paired_bwd(x1, y1, x2, y2, grad_iou, nx, xflags, K: int | None = None, out=None):
+    """iou_grad (dgal_iou_paired_bwd): returns (gx1, gy1, gx2, gy2), each shaped like x1."""
+    for t, nm in ((x1, "x1"), (y1, "y1"), (x2, "x2"), (y2, "y2"), (grad_iou, "grad_iou")):
+        _plane(t, nm)
+    K, n = _K_n(x1, K)
+    if out is None:
+        out = tuple(torch.empty_like(x1) for _ in range(4))
+    gx1, gy1, gx2, gy2 = out
+    call("dgal_iou_paired_bwd", K, n, _ptr(x1), _ptr(y1), _ptr(x2), _ptr(y2), _ptr(grad_iou), _ptr(nx),
+         _ptr(xflags), _ptr(gx1), _ptr(gy1), _ptr(gx2), _ptr(gy2), _stream(x1.device))
+    return gx1, gy1, gx2, gy2
+
+
+def iou_pairwise(rx, ry, cx, cy, K: int | None = None, row_offset: int = 0, thr: float = 0.7,
+                 want_iou: bool = True, want_mask: bool = True, nbr_cap: int = 0, out=None):
+    """Pairwise IoU of rows x columns (dgal_iou_pairwise).  Returns
+    (iou f32[nr, m] | None, mask u64[nr, ceil(m/64)] | None, nbr_count i32[nr] | None,
+     nbr_idx i32[nr, nbr_cap] | None).  mask/nbr semantics: include/dgal.h."""
+    for t, nm in ((rx, "rx"), (ry, "ry"), (cx, "cx"), (cy, "cy")):
+        _plane(t, nm)
+    K, nr = _K_n(rx, K)
+    _, m = _K_n(cx, K)
+    dev = rx.device
+    words = (m + 63) // 64
+    if out is not None:
+        iou, mask, cnt, idx = out
+    else:
+        iou = torch.empty((nr, m), dtype=torch.float32, device=dev) if want_iou else None
+        mask = torch.empty((nr, words), dtype=torch.int64, device=dev) if want_mask else None
+        cnt = torch.empty(nr, dtype=torch.int32, device=dev) if nbr_cap > 0 else None
+        idx = torch.empty((nr, nbr_cap), dtype=torch.int32, device=dev) if nbr_cap > 0 else None
+    call("dgal_iou_pairwise", K, nr, _ptr(rx), _ptr(ry), m, _ptr(cx), _ptr(cy), int(row_offset), _ptr(iou),
+         float(thr), _ptr(mask), words if mask is not None else 0, _ptr(cnt), _ptr(idx),
+         int(nbr_cap if cnt is not None else 0), _stream(dev))
+    return iou, mask, cnt, idx
+
+
+def nms_round(n_total: int, row_offset: int, mask, nbr_count, nbr_idx, status, undecided):
+    """One parallel NMS round over this rank's rows (dgal_nms_round)."""
+    n_rows = mask.shape[0]
+    cap = nbr_idx.shape[1] if nbr_idx is not None else 0
+    call("dgal_nms_round", int(n_total), n_rows, int(row_offset), _ptr(mask), mask.shape[1], _ptr(nbr_count),
+         _ptr(nbr_idx), cap, _ptr(status), _ptr(undecided), _stream(mask.device))
+
+
+def nms_keep(mask, nbr_count=None, nbr_idx=None, status=None, keep=None):
+    """Greedy NMS keep vector u8[n] from a single-GPU pairwise mask (dgal_nms_keep)."""
+    n = mask.shape[0]
+    dev = mask.device
+    cap = nbr_idx.shape[1] if nbr_idx is not None else 0
+    status = torch.empty(n, dtype=torch.uint8, device=dev) if status is None else status
+    keep = torch.empty(n, dtype=torch.uint8, device=dev) if keep is None else keep
+    call("dgal_nms_keep", n, _ptr(mask), mask.shape[1], _ptr(nbr_count), _ptr(nbr_idx), cap, _ptr(status),
+         _ptr(keep), _stream(dev))
+    return keep
+
+
+def nms(x, y, thr: float = 0.7, K: int | None = None, nbr_cap: int = 64):
+    """Rotated NMS of score-sorted polygons: pairwise mask + keep (single GPU)."""
+    _, mask, cnt, idx = iou_pairwise(x, y, x, y, K=K, thr=thr, want_iou=False, want_mask=True,
+                                     nbr_cap=nbr_cap)
+    return nms_keep(mask, cnt, idx)
+
+
+class PolyIoU(torch.autograd.Function):
+    """Differentiable paired IoU: forward = dgal_iou_paired_fwd, backward =
+    dgal_iou_paired_bwd through the saved nx / xflags (the paper's listing)."""
+
+    @staticmethod
+    def forward(ctx, x1, y1, x2, y2):
+        x1, y1, x2, y2 = (t.contiguous() for t in (x1, y1, x2, y2))
+        iou, nx, xf = iou_paired_fwd(x1, y1, x2, y2)
+        ctx.save_for_backward(x1, y1, x2, y2, nx, xf)
+        return iou
+
+    @staticmethod
+    def backward(ctx, g):
+        x1, y1, x2, y2, nx, xf = ctx.saved_tensors
+        return iou_paired_bwd(x1, y1, x2, y2, g.contiguous().float(), nx, xf)

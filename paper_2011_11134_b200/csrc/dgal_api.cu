@@ -1,0 +1,130 @@
+// dgal_api.cu — the extern "C" boundary of libdgal.so (include/dgal.h): host-side
+// argument validation, K dispatch, launch on the caller's stream.  No
+// allocation, no global state, no host synchronisation.
+#include <cstdint>
+
+#include "../../include/dgal.h"
+#include "dgal_internal.h"
+
+#ifndef DGAL_VERSION
+#define DGAL_VERSION "0.1.0"
+#endif
+
+namespace {
+
+inline bool aligned(const void *p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+inline dgal_status from_cuda(cudaError_t e) { return e == cudaSuccess ? DGAL_OK : DGAL_ERR_CUDA; }
+
+inline cudaStream_t as_cuda(dgal_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+dgal_status dgal_iou_paired_fwd(int K, int64_t n, const float *x1, const float *y1, const float *x2,
+                                const float *y2, float *iou, uint8_t *nx, uint8_t *xflags,
+                                dgal_stream stream)
+{
+    if (K != 4 && K != 8) return DGAL_ERR_UNSUPPORTED_K;
+    if (n < 0) return DGAL_ERR_INVALID_ARG;
+    if (n == 0) return DGAL_OK;
+    if (!x1 || !y1 || !x2 || !y2 || !iou || !nx || !xflags) return DGAL_ERR_INVALID_ARG;
+    if (!aligned(x1, 16) || !aligned(y1, 16) || !aligned(x2, 16) || !aligned(y2, 16) ||
+        !aligned(xflags, (uintptr_t)(2 * K)))
+        return DGAL_ERR_MISALIGNED;
+    return from_cuda(dgal::launch_paired_fwd(K, n, x1, y1, x2, y2, iou, nx, xflags, as_cuda(stream)));
+}
+
+dgal_status dgal_iou_paired_bwd(int K, int64_t n, const float *x1, const float *y1, const float *x2,
+                                const float *y2, const float *grad_iou, const uint8_t *nx,
+                                const uint8_t *xflags, float *gx1, float *gy1, float *gx2, float *gy2,
+                                dgal_stream stream)
+{
+    if (K != 4 && K != 8) return DGAL_ERR_UNSUPPORTED_K;
+    if (n < 0) return DGAL_ERR_INVALID_ARG;
+    if (n == 0) return DGAL_OK;
+    if (!x1 || !y1 || !x2 || !y2 || !grad_iou || !nx || !xflags || !gx1 || !gy1 || !gx2 || !gy2)
+        return DGAL_ERR_INVALID_ARG;
+    if (!aligned(x1, 16) || !aligned(y1, 16) || !aligned(x2, 16) || !aligned(y2, 16) ||
+        !aligned(gx1, 16) || !aligned(gy1, 16) || !aligned(gx2, 16) || !aligned(gy2, 16) ||
+        !aligned(xflags, (uintptr_t)(2 * K)))
+        return DGAL_ERR_MISALIGNED;
+    return from_cuda(dgal::launch_paired_bwd(K, n, x1, y1, x2, y2, grad_iou, nx, xflags, gx1, gy1, gx2,
+                                             gy2, as_cuda(stream)));
+}
+
+dgal_status dgal_iou_pairwise(int K, int64_t n_rows, const float *row_x, const float *row_y, int64_t m,
+                              const float *col_x, const float *col_y, int64_t row_offset, float *iou,
+                              float nms_thresh, uint64_t *mask, int64_t mask_words, int32_t *nbr_count,
+                              int32_t *nbr_idx, int32_t nbr_cap, dgal_stream stream)
+{
+    if (K != 4 && K != 8) return DGAL_ERR_UNSUPPORTED_K;
+    if (n_rows < 0 || m < 0 || row_offset < 0) return DGAL_ERR_INVALID_ARG;
+    if (n_rows == 0 || m == 0) return DGAL_OK;
+    if (!row_x || !row_y || !col_x || !col_y) return DGAL_ERR_INVALID_ARG;
+    if (!iou && !mask) return DGAL_ERR_INVALID_ARG;                 // nothing to compute
+    if (m > (int64_t)65535 * dgal::kPwTileCols) return DGAL_ERR_INVALID_ARG;
+    if (mask) {
+        if (!(nms_thresh >= 0.f)) return DGAL_ERR_INVALID_ARG;    // also rejects NaN
+        if (mask_words < (m + 63) / 64) return DGAL_ERR_INVALID_ARG;
+        if (!aligned(mask, 8)) return DGAL_ERR_MISALIGNED;
+    }
+    if ((nbr_count == nullptr) != (nbr_idx == nullptr)) return DGAL_ERR_INVALID_ARG;
+    if (nbr_count && (!mask || nbr_cap < 0)) return DGAL_ERR_INVALID_ARG;
+    if (!aligned(row_x, 16) || !aligned(row_y, 16) || !aligned(col_x, 16) || !aligned(col_y, 16) ||
+        (iou && !aligned(iou, 4)))
+        return DGAL_ERR_MISALIGNED;
+    return from_cuda(dgal::launch_pairwise(K, n_rows, row_x, row_y, m, col_x, col_y, row_offset, iou,
+                                           nms_thresh, mask, mask_words, nbr_count, nbr_idx, nbr_cap,
+                                           as_cuda(stream)));
+}
+
+dgal_status dgal_nms_round(int64_t n_total, int64_t n_rows, int64_t row_offset, const uint64_t *mask,
+                           int64_t mask_words, const int32_t *nbr_count, const int32_t *nbr_idx,
+                           int32_t nbr_cap, uint8_t *status, int32_t *undecided, dgal_stream stream)
+{
+    if (n_total < 0 || n_rows < 0 || row_offset < 0 || row_offset + n_rows > n_total)
+        return DGAL_ERR_INVALID_ARG;
+    if (n_rows == 0) return DGAL_OK;
+    if (!mask || !status || !undecided || mask_words < (n_total + 63) / 64) return DGAL_ERR_INVALID_ARG;
+    if ((nbr_count == nullptr) != (nbr_idx == nullptr) || nbr_cap < 0) return DGAL_ERR_INVALID_ARG;
+    if (!aligned(mask, 8) || !aligned(undecided, 4)) return DGAL_ERR_MISALIGNED;
+    return from_cuda(dgal::launch_nms_round(n_total, n_rows, row_offset, mask, mask_words, nbr_count,
+                                            nbr_idx, nbr_cap, status, undecided, as_cuda(stream)));
+}
+
+dgal_status dgal_nms_keep(int64_t n, const uint64_t *mask, int64_t mask_words, const int32_t *nbr_count,
+                          const int32_t *nbr_idx, int32_t nbr_cap, uint8_t *status, uint8_t *keep,
+                          dgal_stream stream)
+{
+    if (n < 0) return DGAL_ERR_INVALID_ARG;
+    if (n == 0) return DGAL_OK;
+    if (!mask || !status || !keep || mask_words < (n + 63) / 64) return DGAL_ERR_INVALID_ARG;
+    if ((nbr_count == nullptr) != (nbr_idx == nullptr) || nbr_cap < 0) return DGAL_ERR_INVALID_ARG;
+    if (!aligned(mask, 8)) return DGAL_ERR_MISALIGNED;
+    return from_cuda(dgal::launch_nms_keep(n, mask, mask_words, nbr_count, nbr_idx, nbr_cap, status, keep,
+                                           as_cuda(stream)));
+}
+
+const char *dgal_status_string(dgal_status s)
+{
+    switch (s) {
+    case DGAL_OK: return "DGAL_OK";
+    case DGAL_ERR_INVALID_ARG: return "DGAL_ERR_INVALID_ARG";
+    case DGAL_ERR_UNSUPPORTED_K: return "DGAL_ERR_UNSUPPORTED_K";
+    case DGAL_ERR_MISALIGNED: return "DGAL_ERR_MISALIGNED";
+    case DGAL_ERR_CUDA: return "DGAL_ERR_CUDA";
+    }
+    return "DGAL_ERR_UNKNOWN";
+}
+
+const char *dgal_build_info(void)
+{
+#define DGAL_STR2(x) #x
+#define DGAL_STR(x) DGAL_STR2(x)
+    return "libdgal " DGAL_VERSION " sm_100a nvcc " DGAL_STR(__CUDACC_VER_MAJOR__) "." DGAL_STR(
+        __CUDACC_VER_MINOR__) "." DGAL_STR(__CUDACC_VER_BUILD__);
+}
+
+}  // extern "C"

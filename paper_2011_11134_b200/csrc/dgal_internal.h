@@ -1,0 +1,41 @@
+// dgal_internal.h — launch configuration and launcher prototypes shared by the
+// .cu translation units of libdgal.so (not part of the public ABI).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dgal {
+
+constexpr int kPairedThreads = 256;     // paired kernels: one pair per thread
+
+// pairwise kernel geometry
+constexpr int kPwThreads = 256;         // 8 warps
+constexpr int kPwWarps = kPwThreads / 32;
+constexpr int kPwTileCols = 1024;       // column tile staged in shared memory
+constexpr int kPwRowsPerCta = 64;       // row block per CTA (8 rows per warp)
+constexpr int kPwQueueCap = 32 + 128;   // per-warp candidate queue (<=31 left + 128 pushed)
+
+constexpr int kNmsKeepThreads = 1024;   // single-CTA keep kernel
+constexpr int kNmsRoundThreads = 256;
+
+cudaError_t launch_paired_fwd(int K, int64_t n, const float *x1, const float *y1, const float *x2,
+                              const float *y2, float *iou, uint8_t *nx, uint8_t *xflags,
+                              cudaStream_t st);
+cudaError_t launch_paired_bwd(int K, int64_t n, const float *x1, const float *y1, const float *x2,
+                              const float *y2, const float *grad, const uint8_t *nx,
+                              const uint8_t *xflags, float *gx1, float *gy1, float *gx2, float *gy2,
+                              cudaStream_t st);
+cudaError_t launch_pairwise(int K, int64_t n_rows, const float *rx, const float *ry, int64_t m,
+                            const float *cx, const float *cy, int64_t row_offset, float *iou,
+                            float thr, uint64_t *mask, int64_t mask_words, int32_t *nbr_count,
+                            int32_t *nbr_idx, int32_t cap, cudaStream_t st);
+cudaError_t launch_nms_round(int64_t n_total, int64_t n_rows, int64_t row_offset,
+                             const uint64_t *mask, int64_t mask_words, const int32_t *nbr_count,
+                             const int32_t *nbr_idx, int32_t cap, uint8_t *status, int32_t *undecided,
+                             cudaStream_t st);
+cudaError_t launch_nms_keep(int64_t n, const uint64_t *mask, int64_t mask_words,
+                            const int32_t *nbr_count, const int32_t *nbr_idx, int32_t cap,
+                            uint8_t *status, uint8_t *keep, cudaStream_t st);
+
+}  // namespace dgal

@@ -1,0 +1,159 @@
+"""GPU parity of the paired forward/backward (dgal_iou_paired_fwd/bwd)
+against the CPU oracle, through the C ABI.  Tolerances are the north_star's:
+nx/xflags bit-exact on margin inputs, IoU <= 1e-5 abs, vertex gradients <=
+1e-4 abs or <= 1e-3 rel."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2011_11134_b200 as dgal
+import synth
+from gpu_util import (assert_flags_exact, assert_grad_close, assert_iou_close,
+                      check_paired_against_oracle, dev, gpu_paired, to_dev)
+from helpers import box, margin_batch, regular
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("cfg,n", [(1, 1024), (3, 40_000), (4, 20_000)])
+def test_paired_margin_inputs_full_compare(cfg, n):
+    """Every output element of a margin-filtered batch of the config."""
+    check_paired_against_oracle(margin_batch(cfg, n))
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 255, 257, 1000, 4097])
+def test_ragged_sizes(n):
+    check_paired_against_oracle(margin_batch(1, n))
+
+
+def _pairs(P_list, Q_list, K):
+    P = np.stack(P_list).astype(np.float32)
+    Q = np.stack(Q_list).astype(np.float32)
+    mk = lambda A: synth.Polys(np.ascontiguousarray(A[..., 0].reshape(-1)),  # noqa: E731
+                               np.ascontiguousarray(A[..., 1].reshape(-1)), K)
+    g = np.linspace(-1, 1, len(P_list)).astype(np.float32)
+    return synth.PairBatch(mk(P), mk(Q), g)
+
+
+def test_degenerate_zoo():
+    """identical (IoU exactly 1), disjoint, touching edge / corner (empty),
+    strict subset / superset, offset squares."""
+    sq = np.array([[0, 0], [1, 0], [1, 1], [0, 1]], float)
+    cases = [(sq, sq), (sq, sq + 5), (sq, sq + [1.0, 0]), (sq, sq + [1.0, 1.0]),
+             (sq * 0.5 + 0.25, sq), (sq, sq * 0.5 + 0.25), (sq, sq + 0.5)]
+    rng = np.random.default_rng(0)
+    for _ in range(200):   # random identical pairs at scene coordinates
+        b = box(*rng.uniform(-300, 300, 2), *rng.uniform(0.3, 12, 2), rng.uniform(-4, 4))
+        cases.append((b, b.copy()))
+    b = _pairs([c[0] for c in cases], [c[1] for c in cases], 4)
+    iou, nx, xf, gr = gpu_paired(b)
+    assert np.all(iou[7:] == 1.0) and iou[0] == 1.0
+    assert list(xf[0][:4]) == [0x40, 0x41, 0x42, 0x43] and nx[0] == 4
+    assert iou[1] == 0 and iou[2] == 0 and iou[3] == 0 and np.all(nx[1:4] == 0)
+    assert np.all(xf[1:4] == 0)
+    for k in (1, 2, 3):
+        assert all(np.all(g.reshape(-1, 4)[k] == 0) for g in gr)
+    assert list(xf[4][:4]) == [0x40, 0x41, 0x42, 0x43]
+    assert list(xf[5][:4]) == [0x80, 0x81, 0x82, 0x83]
+    assert list(xf[6][:4]) == [0x42, 0xD3, 0x80, 0xC8]
+    assert abs(iou[6] - 1 / 7) < 1e-6
+    ref = oracle.iou_paired_fwd(b.p1, b.p2)
+    assert_iou_close(iou, ref["iou"])
+
+
+@pytest.mark.parametrize("K", [4, 8])
+def test_regular_ngons_max_vertices(K):
+    """Regular K-gons with equal apothem rotated by pi/K: IoU = cos(pi/K), nx = 2K
+    (the capacity bound; 16 vertices for K=8), all Cross."""
+    rng = np.random.default_rng(K)
+    P_list, Q_list = [], []
+    for _ in range(256):
+        a = rng.uniform(0.5, 3)
+        R = a / math.cos(math.pi / K)
+        ph = rng.uniform(0, 6.3)
+        c = rng.uniform(-50, 50, 2)
+        P_list.append(regular(K, R, ph, c))
+        Q_list.append(regular(K, R, ph + math.pi / K, c))
+    b = _pairs(P_list, Q_list, K)
+    ok = oracle.margin_ok(b.p1, b.p2)
+    iou, nx, xf, gr = gpu_paired(b)
+    assert np.all(np.abs(iou - math.cos(math.pi / K)) < 2e-5)
+    assert np.all(nx[ok] == 2 * K)
+    ref = oracle.iou_paired_fwd(b.p1, b.p2)
+    assert_flags_exact(nx[ok], xf[ok], {"nx": ref["nx"][ok], "xflags": ref["xflags"][ok]})
+    rg = oracle.iou_paired_bwd(b.p1, b.p2, b.grad)
+    for got, want in zip(gr, rg):
+        assert_grad_close(got.reshape(want.shape)[ok], want[ok])
+
+
+def test_bitwise_linearity_and_determinism():
+    b = margin_batch(3, 20_000)
+    x1, y1 = to_dev(b.p1)
+    x2, y2 = to_dev(b.p2)
+    g = torch.from_numpy(b.grad).to(dev())
+    iou, nx, xf = dgal.iou_paired_fwd(x1, y1, x2, y2)
+    iou2, nx2, xf2 = dgal.iou_paired_fwd(x1, y1, x2, y2)
+    assert torch.equal(iou, iou2) and torch.equal(nx, nx2) and torch.equal(xf, xf2)
+    r1 = dgal.iou_paired_bwd(x1, y1, x2, y2, g, nx, xf)
+    r2 = dgal.iou_paired_bwd(x1, y1, x2, y2, 2 * g, nx, xf)
+    r3 = dgal.iou_paired_bwd(x1, y1, x2, y2, -g, nx, xf)
+    for a, bb, c in zip(r1, r2, r3):
+        assert torch.equal(bb, 2 * a) and torch.equal(c, -a)
+    # a prefix of the batch gives bitwise the same per-pair results
+    m = 777
+    i3, n3, f3 = dgal.iou_paired_fwd(x1[:m].contiguous(), y1[:m].contiguous(), x2[:m].contiguous(),
+                                     y2[:m].contiguous())
+    assert torch.equal(i3, iou[:m]) and torch.equal(f3, xf[:m])
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_full_size_sampled(cfg):
+    """BASELINE size, the launch configuration bench.py times (raw inputs, one
+    launch over all pairs); sampled outputs checked one by one against the oracle.
+    IoU is checked on every sampled pair, nx/xflags/gradients on the sampled
+    pairs that are a margin away from degeneracy."""
+    b = synth.gen_config(cfg)
+    iou, nx, xf, gr = gpu_paired(b)
+    rng = np.random.default_rng(cfg)
+    idx = np.sort(rng.choice(b.n, size=100_000, replace=False))
+    s = b.take(idx)
+    ref = oracle.iou_paired_fwd(s.p1, s.p2)
+    assert_iou_close(iou[idx], ref["iou"])
+    ok = oracle.margin_ok(s.p1, s.p2)
+    assert ok.mean() > 0.85
+    assert_flags_exact(nx[idx][ok], xf[idx][ok], {"nx": ref["nx"][ok], "xflags": ref["xflags"][ok]})
+    K = b.p1.K
+    rg = oracle.iou_paired_bwd(s.p1, s.p2, s.grad)
+    for got, want in zip(gr, rg):
+        assert_grad_close(got.reshape(-1, K)[idx][ok], want[ok])
+    # invariants that hold for every pair
+    assert np.all((iou >= 0) & (iou <= 1))
+    assert np.all((nx == 0) | ((nx >= 3) & (nx <= 2 * K)))
+    assert np.all(iou[nx == 0] == 0)
+
+
+def test_autograd_function_matches_bwd():
+    b = margin_batch(1, 512)
+    x1, y1 = to_dev(b.p1)
+    x2, y2 = to_dev(b.p2)
+    for t in (x1, y1, x2, y2):
+        t.requires_grad_(True)
+    iou = dgal.PolyIoU.apply(x1, y1, x2, y2)
+    g = torch.from_numpy(b.grad).to(dev())
+    (iou * g).sum().backward()
+    _, nx, xf = dgal.iou_paired_fwd(x1.detach(), y1.detach(), x2.detach(), y2.detach())
+    r = dgal.iou_paired_bwd(x1.detach(), y1.detach(), x2.detach(), y2.detach(), g, nx, xf)
+    for t, want in zip((x1, y1, x2, y2), r):
+        assert torch.equal(t.grad, want)
+
+
+def test_empty_batch_is_noop():
+    z = torch.empty((0, 4), dtype=torch.float32, device=dev())
+    iou, nx, xf = dgal.iou_paired_fwd(z, z, z, z)
+    assert iou.numel() == 0
+    with pytest.raises(dgal.DgalError):
+        bad = torch.zeros((8, 5), dtype=torch.float32, device=dev())
+        dgal.iou_paired_fwd(bad, bad, bad, bad)
