@@ -3,26 +3,33 @@
 // fully unrolled over the compile-time vertex count K ("templated
 // with options for precision and size ... fix-size allocated memory"), so no
 // array is ever dynamically indexed and nothing spills to local memory
-// (checked by tests/test_build_artifacts.py on the SASS).
+// (checked on the SASS by tests/test_build_artifacts.py).
 //
 // Method.  The paper's `intersect(p1, p2, xflags)` is
 // realised as an edge-interval clip: every edge of p1 is clipped against the
 // closed half-planes of p2 and every edge of p2 against the open half-planes of
 // p1 (Cyrus-Beck intervals [t0, t1] on each edge).  In exact arithmetic these
 // intervals are exactly the boundary pieces of p1 ∩ p2, so
-//   * area:  2 A_i = sum_i (t1-t0)_i cross(v_i, v_i+1) + sum_j (s1-s0)_j cross(w_j, w_j+1)
-//     (Green's theorem on each boundary piece, no vertex list needed),
-//   * nx / xflags: walking p1's edges in order emits FromP1(i) or the
-//     entering Cross(i, j_in), then the exiting Cross(i, j_out) followed by the
-//     run of p2 vertices strictly inside p1 — the CCW vertex sequence of p1 ∩ p2,
-//     rotated to start at its smallest byte (R3),
-//   * iou_grad: d A_i / d v moves only the boundary pieces lying on the
-//     edges incident to v (shape derivative), so with n_i = perp(v_i+1 - v_i):
+//   * area:  2 A_i = sum_i (t1-t0)_i v_i x v_i+1 + sum_j (s1-s0)_j w_j x w_j+1
+//     (Green's theorem on each boundary piece, no vertex list needed);
+//   * nx / xflags: walking p1's edges in order emits FromP1(i) or
+//     the entering Cross(i, j_in), then the exiting Cross(i, j_out) followed by
+//     the run of p2 vertices strictly inside p1 — the CCW vertex sequence of
+//     p1 ∩ p2 — rotated to start at its smallest byte (R3);
+//   * iou_grad: dA_i/dv moves only the boundary pieces lying on the edges
+//     incident to v (shape derivative); with n = perp(edge vector),
 //       dA_i/dv_i += n_i ∫_{t0}^{t1} (1-t) dt,   dA_i/dv_i+1 += n_i ∫_{t0}^{t1} t dt,
-//     where the interval end points are read from the recorded xflags.
-// Decision predicates (inside/outside) are evaluated contraction-free
-// (__fmul_rn/__fsub_rn) so a point exactly on a line gives exactly 0: identical
-// polygons give IoU == 1 exactly (the pairwise diagonal).
+//     where the interval end points come from the crossings recorded in xflags.
+//
+// Performance notes (sm_100a, ncu-guided): the kernels are
+// instruction-bound with the ALU pipe (compare/select/min/max/logic, half rate)
+// the binding unit, so the Cyrus-Beck update is written branch-free with the
+// class of each line taken from sign(a - b) alone: an FMA-pipe saturating
+// multiply turns it into a 0/1 mask, leaving two min/max per (edge, line) on the
+// ALU pipe.  The line index that defines t0 / t1 (needed for the flags) rides in
+// the three low mantissa bits of t (<= 7 ulp, below the IoU tolerance).
+// Decision predicates are contraction-free (__fmul_rn/__fsub_rn) so a point on
+// a line gives exactly 0: identical polygons give IoU == 1 exactly.
 #pragma once
 
 #include <cstdint>
@@ -39,6 +46,9 @@ struct Poly {
 // ---------------------------------------------------------------------------
 // small helpers
 // ---------------------------------------------------------------------------
+constexpr float kTiny = 1e-30f;   // below any non-degenerate decision value
+constexpr float kBig = 1e30f;
+
 __device__ __forceinline__ float cross_rn(float ax, float ay, float bx, float by)
 {
     // a x b with both products rounded separately: exact 0 for parallel
@@ -50,6 +60,27 @@ __device__ __forceinline__ float rcp_approx(float x)
 {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// carry a line index 0..7 in the 3 low mantissa bits of a finite-or-NaN value
+__device__ __forceinline__ float enc_idx(float v, int j)
+{
+    return __int_as_float((__float_as_int(v) & ~7) | j);
+}
+__device__ __forceinline__ int dec_idx(float v) { return __float_as_int(v) & 7; }
+
+// 64-bit shifts with PTX semantics (amounts >= 64 give 0), no C++ UB
+__device__ __forceinline__ uint64_t shl64(uint64_t x, uint32_t s)
+{
+    uint64_t r;
+    asm("shl.b64 %0, %1, %2;" : "=l"(r) : "l"(x), "r"(s));
+    return r;
+}
+__device__ __forceinline__ uint64_t shr64(uint64_t x, uint32_t s)
+{
+    uint64_t r;
+    asm("shr.b64 %0, %1, %2;" : "=l"(r) : "l"(x), "r"(s));
     return r;
 }
 
@@ -95,53 +126,54 @@ struct Seq {
     uint64_t w[NW];
 };
 
-// OR the (<= 8 byte) value r into the byte string at byte offset pos.
+// OR the (<= 8 byte) value r into the byte string at byte offset pos (0..2K-1).
 template <int K>
 __device__ __forceinline__ void seq_or(Seq<K> &s, uint64_t r, int pos)
 {
-#pragma unroll
-    for (int k = 0; k < Seq<K>::NW; ++k) {
-        const int sh = 8 * pos - 64 * k;  // bit offset of r inside word k
-        uint64_t part = 0;
-        if (sh >= 0 && sh < 64) part = r << sh;
-        else if (sh < 0 && sh > -64) part = r >> (-sh);
-        s.w[k] |= part;
+    if (K == 4) {
+        s.w[0] |= shl64(r, 8u * (uint32_t)pos);
+    } else {
+        const uint32_t sh = 8u * (uint32_t)pos;
+        s.w[0] |= shl64(r, sh);
+        s.w[Seq<K>::NW - 1] |= (sh >= 64u) ? shl64(r, sh - 64u) : shr64(r, 64u - sh);
     }
 }
 
 template <int K>
-__device__ __forceinline__ uint32_t seq_byte(const Seq<K> &s, int p)
+__device__ __forceinline__ uint32_t seq_byte(const Seq<K> &s, int p)  // p static
 {
-    // select the word without a dynamic array index (keeps s in registers)
-    uint64_t w = s.w[0];
-#pragma unroll
-    for (int k = 1; k < Seq<K>::NW; ++k) w = ((p >> 3) == k) ? s.w[k] : w;
+    const uint64_t w = s.w[p >> 3];
     return (uint32_t)(w >> (8 * (p & 7))) & 0xFFu;
 }
 
-// Rotate the first n bytes of s left by r bytes (byte r becomes byte 0).
+// Canonical form (R3): rotate the n valid bytes so the smallest byte comes first.
+// The minimum and its position come from one min over keys (byte << 4 | pos).
 template <int K>
-__device__ __forceinline__ Seq<K> seq_rotate(const Seq<K> &s, int n, int r)
+__device__ __forceinline__ Seq<K> seq_canonical(const Seq<K> &s, int n)
 {
-    Seq<K> o;
+    uint32_t best = 0xFFFFFFFFu;
 #pragma unroll
-    for (int k = 0; k < Seq<K>::NW; ++k) o.w[k] = 0;
+    for (int p = 0; p < 2 * K; ++p) {
+        const uint32_t key = (seq_byte<K>(s, p) << 4) | (uint32_t)p;
+        best = (p < n) ? min(best, key) : best;
+    }
+    const uint32_t r = best & 15u;
+    Seq<K> o;
     if (K == 4) {
-        // one word: bytes [r, n) then [0, r)
         const uint64_t x = s.w[0];
-        const uint64_t lo = (r > 0) ? (x >> (8 * r)) : x;
-        const uint64_t hi = (r > 0) ? (x << (8 * (n - r))) : 0;
-        uint64_t m = (n >= 8) ? ~0ull : ((1ull << (8 * n)) - 1ull);
-        o.w[0] = (lo | hi) & m;
+        const uint64_t m = shl64(~0ull, 8u * (uint32_t)n);  // bytes >= n
+        o.w[0] = (shr64(x, 8u * r) | shl64(x, 8u * ((uint32_t)n - r))) & ~m;
     } else {
+        o.w[0] = 0;
+        o.w[Seq<K>::NW - 1] = 0;
 #pragma unroll
         for (int p = 0; p < 2 * K; ++p) {
-            if (p < n) {
-                int q = p + r;
-                q = (q >= n) ? q - n : q;
-                const uint64_t b = seq_byte<K>(s, q);
-                o.w[p >> 3] |= b << (8 * (p & 7));
-            }
+            int q = p + (int)r;
+            q = (q >= n) ? q - n : q;
+            // byte q of s, q dynamic: select the word, then shift
+            const uint64_t w = (q >= 8) ? s.w[Seq<K>::NW - 1] : s.w[0];
+            const uint64_t b = (p < n) ? ((w >> (8 * (q & 7))) & 0xFFull) : 0ull;
+            o.w[p >> 3] |= b << (8 * (p & 7));
         }
     }
     return o;
@@ -163,186 +195,163 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
 {
     constexpr uint32_t KMASK = (1u << K) - 1u;
 
-    // edge vectors g_i = v_i+1 - v_i (p1), f_j = w_j+1 - w_j (p2)
-    float gx[K], gy[K], fx[K], fy[K];
+    // edge vectors g_i = v_i+1 - v_i (p1), f_j = w_j+1 - w_j (p2); shoelace terms
+    float gx[K], gy[K], fx[K], fy[K], C1[K], C2[K];
+    float A1x2 = 0.f, A2x2 = 0.f;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         const int i1 = (i + 1) % K;
         gx[i] = P.x[i1] - P.x[i]; gy[i] = P.y[i1] - P.y[i];
         fx[i] = Q.x[i1] - Q.x[i]; fy[i] = Q.y[i1] - Q.y[i];
-    }
-    // shoelace terms: C1_i = v_i x v_i+1, C2_j = w_j x w_j+1
-    float C1[K], C2[K];
-    float A1x2 = 0.f, A2x2 = 0.f;
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-        const int i1 = (i + 1) % K;
-        C1[i] = P.x[i] * P.y[i1] - P.x[i1] * P.y[i];
+        C1[i] = P.x[i] * P.y[i1] - P.x[i1] * P.y[i];   // S:173
         C2[i] = Q.x[i] * Q.y[i1] - Q.x[i1] * Q.y[i];
         // same order as the A_i sum below: identical polygons give A_i == A_1 bitwise
         A1x2 = __fadd_rn(A1x2, C1[i]);
         A2x2 = __fadd_rn(A2x2, C2[i]);
     }
 
-    // ---- p1 edges against the CLOSED half-planes of p2 (inside: d >= 0) ----
-    // d[i][j] = f_j x (v_i - w_j), computed one vertex row at a time.
-    float drow0[K], dprev[K];
-    float satP2[K];  // max_i d[i][j]: <= 0 means p1 lies outside line j (separating)
+    // decision values, shifted by +-tiny (below any non-degenerate value) so that
+    // "inside" is "> 0" on both sides and no value is exactly 0:
+    //   d[i][j] = f_j x (v_i - w_j) + tiny   p1 vertex i vs p2 line j, CLOSED test (d >= 0)
+    //   e[j][i] = g_i x (w_j - v_i) - tiny   p2 vertex j vs p1 line i, OPEN test (e > 0)
+    float d[K][K], e[K][K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-        drow0[j] = cross_rn(fx[j], fy[j], __fsub_rn(P.x[0], Q.x[j]), __fsub_rn(P.y[0], Q.y[j]));
-        dprev[j] = drow0[j];
-        satP2[j] = drow0[j];
-    }
-    float Aix2 = 0.f;
-    uint32_t valid1 = 0;
-    int jin[K], jout[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-        float dnext[K];
+    for (int i = 0; i < K; ++i)
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-            if (i + 1 < K) {
-                dnext[j] = cross_rn(fx[j], fy[j], __fsub_rn(P.x[i + 1], Q.x[j]),
-                                    __fsub_rn(P.y[i + 1], Q.y[j]));
-                satP2[j] = fmaxf(satP2[j], dnext[j]);
-            } else {
-                dnext[j] = drow0[j];
-            }
+            const float Dx = __fsub_rn(P.x[i], Q.x[j]), Dy = __fsub_rn(P.y[i], Q.y[j]);
+            d[i][j] = __fadd_rn(cross_rn(fx[j], fy[j], Dx, Dy), kTiny);
+            e[j][i] = __fsub_rn(cross_rn(Dx, Dy, gx[i], gy[i]), kTiny);
         }
-        float t0 = 0.f, t1 = 1.f;
-        bool dead = false;
-        int ji = -1, jo = -1;
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const float a = dprev[j], b = dnext[j];
-            const bool oa = a < 0.f, ob = b < 0.f;
-            dead |= oa & ob;
-            const float t = a * rcp_approx(a - b);
-            if (oa & !ob & (t > t0)) { t0 = t; if (FLAGS) ji = j; }
-            if (ob & !oa & (t < t1)) { t1 = t; if (FLAGS) jo = j; }
-        }
-        const bool v = !dead && (t0 < t1);
-        valid1 |= (uint32_t)v << i;
-        Aix2 = fmaf(v ? (t1 - t0) : 0.f, C1[i], Aix2);
-        jin[i] = ji;
-        jout[i] = jo;
-#pragma unroll
-        for (int j = 0; j < K; ++j) dprev[j] = dnext[j];
-    }
 
-    // ---- p2 edges against the OPEN half-planes of p1 (inside: e > 0) ----
-    // e[j][i] = g_i x (w_j - v_i) = (v_i - w_j) x g_i
-    float erow0[K], eprev[K];
-    float satP1[K];  // max_j e[j][i] <= 0: p2 lies outside line i
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-        erow0[i] = cross_rn(__fsub_rn(P.x[i], Q.x[0]), __fsub_rn(P.y[i], Q.y[0]), gx[i], gy[i]);
-        eprev[i] = erow0[i];
-        satP1[i] = erow0[i];
-    }
-    uint32_t in2 = 0;  // bit j: w_j strictly inside p1
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-        float enext[K];
-        bool allin = true;
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            allin &= eprev[i] > 0.f;
-            if (j + 1 < K) {
-                enext[i] = cross_rn(__fsub_rn(P.x[i], Q.x[j + 1]), __fsub_rn(P.y[i], Q.y[j + 1]),
-                                    gx[i], gy[i]);
-                satP1[i] = fmaxf(satP1[i], enext[i]);
-            } else {
-                enext[i] = erow0[i];
-            }
-        }
-        in2 |= (uint32_t)allin << j;
-        float s0 = 0.f, s1 = 1.f;
-        bool dead = false;
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            const float a = eprev[i], b = enext[i];
-            const bool oa = a <= 0.f, ob = b <= 0.f;
-            dead |= oa & ob;
-            const float t = a * rcp_approx(a - b);
-            if (oa & !ob) s0 = fmaxf(s0, t);
-            if (ob & !oa) s1 = fminf(s1, t);
-        }
-        const bool v = !dead && (s0 < s1);
-        Aix2 = fmaf(v ? (s1 - s0) : 0.f, C2[j], Aix2);
-#pragma unroll
-        for (int i = 0; i < K; ++i) eprev[i] = enext[i];
-    }
-
-    // Separating axis (closed): some edge line of either polygon has the other
+    // Separating axis (closed): an edge line of either polygon with the other
     // polygon entirely on or outside it -> the intersection has zero area.  This
-    // is what makes collinear, opposite-facing edges (touching boxes) empty.
+    // makes collinear, opposite-facing edges (touching boxes) exactly empty.
     bool separated = false;
 #pragma unroll
-    for (int k = 0; k < K; ++k) separated |= (satP2[k] <= 0.f) | (satP1[k] <= 0.f);
+    for (int j = 0; j < K; ++j) {
+        float m1 = d[0][j], m2 = e[0][j];
+#pragma unroll
+        for (int i = 1; i < K; ++i) { m1 = fmaxf(m1, d[i][j]); m2 = fmaxf(m2, e[i][j]); }
+        separated |= (m1 <= kTiny) | (m2 <= 0.f);
+    }
+
+    // Cyrus-Beck intervals.  For the edge a -> b against one line (a, b = the
+    // shifted decision values of its end points, never 0): the inside set is
+    // {t : a + t (b - a) > 0}; b > a bounds it below by t* = a / (a - b), b < a
+    // above, b == a keeps all (a > 0: t* = +inf) or nothing (a < 0: t* = -inf).
+    // Both-outside end points give t* > 1 (below) or t* < 0 (above): the interval
+    // empties itself.  (m t* is NaN when m = 0 and t* = inf: max/min ignore it.)
+    float t0[K], t1[K], s0[K], s1[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        const int i1 = (i + 1) % K;
+        float lo = 0.f, hi = 1.f, lo2 = 0.f, hi2 = 1.f;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            // t* = a/(a-b) near 0 (lower bounds) and as 1 + b/(a-b) near 1 (upper
+            // bounds): an end point lying on the line (|a| or |b| = tiny) then gives
+            // t* = 0 or 1 exactly, so identical polygons keep [0, 1] intervals.
+            {   // p1 edge i vs p2 line j
+                const float a = d[i][j], b = d[i1][j];
+                const float den = a - b;
+                const float r = rcp_approx(den);
+                const float m = __saturatef(-den * kBig);      // 1: bounds below
+                float tE = m * (a * r);                       // finite or NaN
+                float tX = fmaf(m, kBig, fmaf(b, r, 1.f));    // +-inf when a == b
+                if (FLAGS) { tE = enc_idx(tE, j); tX = enc_idx(fmaxf(tX, -1.f), j); }
+                lo = fmaxf(lo, tE);
+                hi = fminf(hi, tX);
+            }
+            {   // p2 edge i vs p1 line j
+                const float a = e[i][j], b = e[i1][j];
+                const float den = a - b;
+                const float r = rcp_approx(den);
+                const float m = __saturatef(-den * kBig);
+                lo2 = fmaxf(lo2, m * (a * r));
+                hi2 = fminf(hi2, fmaf(m, kBig, fmaf(b, r, 1.f)));
+            }
+        }
+        t0[i] = lo; t1[i] = hi; s0[i] = lo2; s1[i] = hi2;
+    }
+
+    // area of p1 ∩ p2 (Green), interleaved so identical polygons reproduce A1x2 bitwise
+    float Aix2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        Aix2 = fmaf(fmaxf(t1[k] - t0[k], 0.f), C1[k], Aix2);
+        Aix2 = fmaf(fmaxf(s1[k] - s0[k], 0.f), C2[k], Aix2);
+    }
+    Aix2 = fminf(Aix2, fminf(A1x2, A2x2));
+    bool nonempty = !separated && (Aix2 > 0.f);
 
     FwdOut<K, FLAGS> out;
 #pragma unroll
     for (int k = 0; k < Seq<K>::NW; ++k) out.seq.w[k] = 0;
     out.nx = 0;
     out.iou = 0.f;
-    Aix2 = fminf(Aix2, fminf(A1x2, A2x2));
-    bool nonempty = !separated && (Aix2 > 0.f);
 
     if (FLAGS) {
-        // Emit the CCW vertex sequence by walking p1's edges in order.
+        // p2 vertex j strictly inside p1 <=> its edge interval starts at 0 unclipped
+        uint32_t in2 = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) in2 |= (uint32_t)((s0[j] <= 0.f) & (s0[j] < s1[j])) << j;
+        const uint32_t in2dup = in2 | (in2 << K);
+
+        // Walk p1's edges in order: [FromP1(i) | Cross(i, j_in)] [Cross(i, j_out) run of FromP2]
         Seq<K> s;
 #pragma unroll
         for (int k = 0; k < Seq<K>::NW; ++k) s.w[k] = 0;
-        int cnt = 0;
-        uint32_t minb = 0x100u;
-        int minpos = 0;
+        int pos = 0;
 #pragma unroll
         for (int i = 0; i < K; ++i) {
-            if ((valid1 >> i) & 1u) {
-                const uint32_t b0 = (jin[i] < 0) ? (0x40u | i) : (0xC0u | (i << 3) | (uint32_t)jin[i]);
-                if (cnt < 2 * K) seq_or<K>(s, b0, cnt);
-                if (b0 < minb) { minb = b0; minpos = cnt; }
-                ++cnt;
-                if (jout[i] >= 0) {
-                    const uint32_t b1 = 0xC0u | (i << 3) | (uint32_t)jout[i];
-                    if (cnt < 2 * K) seq_or<K>(s, b1, cnt);
-                    if (b1 < minb) { minb = b1; minpos = cnt; }
-                    ++cnt;
-                    // run of p2 vertices strictly inside p1 following p2 edge jout
-                    const int p0 = (jout[i] + 1) % K;
-                    const uint32_t rot = ((in2 >> p0) | (in2 << (K - p0))) & KMASK;
-                    const int L = __ffs(~rot) - 1;  // trailing ones, <= K
-                    if (L > 0) {
-                        uint64_t run;
-                        if (K == 4) {
-                            const uint32_t pat = __funnelshift_r(0x83828180u, 0x83828180u, 8 * p0);
-                            run = (uint64_t)(L >= 4 ? pat : (pat & ((1u << (8 * L)) - 1u)));
-                        } else {
-                            const uint64_t pat = 0x8786858483828180ull;
-                            const uint64_t r8 = p0 ? ((pat >> (8 * p0)) | (pat << (64 - 8 * p0))) : pat;
-                            run = (L >= 8) ? r8 : (r8 & ((1ull << (8 * L)) - 1ull));
-                        }
-                        if (cnt < 2 * K) seq_or<K>(s, run, cnt);
-                        const bool wraps = p0 + L > K;
-                        const uint32_t rb = wraps ? 0x80u : (0x80u | p0);
-                        if (rb < minb) { minb = rb; minpos = cnt + (wraps ? K - p0 : 0); }
-                        cnt += L;
+            const bool valid = t0[i] < t1[i];
+            const bool has_in = t0[i] > kTiny;
+            const bool has_out = t1[i] < 1.f;
+            const uint32_t b0 = has_in ? (0xC0u | (i << 3) | (uint32_t)dec_idx(t0[i])) : (0x40u | i);
+            const uint32_t jo = (uint32_t)dec_idx(t1[i]);
+            const uint32_t b1 = 0xC0u | (i << 3) | jo;
+            // run of p2 vertices inside p1 after p2 edge j_out: trailing ones of in2 rotated
+            const uint32_t p0 = (jo + 1u) & (K - 1u);
+            const uint32_t rot = (in2dup >> p0) & KMASK;
+            const uint32_t L = __ffs(~rot) - 1;               // <= K
+            uint64_t run;
+            if (K == 4) {
+                const uint32_t pat = __funnelshift_r(0x83828180u, 0x83828180u, 8u * p0);
+                run = (uint64_t)(pat & (uint32_t)(shl64(1ull, 8u * L) - 1ull));
+            } else {
+                const uint64_t pat = 0x8786858483828180ull;
+                const uint64_t r8 = shr64(pat, 8u * p0) | shl64(pat, 64u - 8u * p0);
+                run = r8 & (shl64(1ull, 8u * L) - 1ull);
+            }
+            if (K == 4) {
+                uint64_t seg = b0;
+                seg |= has_out ? (((uint64_t)b1 << 8) | (run << 16)) : 0ull;
+                const int c = valid ? (has_out ? 2 + (int)L : 1) : 0;
+                s.w[0] |= valid ? shl64(seg, 8u * (uint32_t)pos) : 0ull;
+                pos += c;
+            } else {
+                if (valid) {
+                    if (pos < 2 * K) seq_or<K>(s, b0, pos);
+                    ++pos;
+                    if (has_out) {
+                        if (pos < 2 * K) seq_or<K>(s, b1, pos);
+                        ++pos;
+                        if (pos < 2 * K) seq_or<K>(s, run, pos);
+                        pos += (int)L;
                     }
                 }
             }
         }
-        if (cnt == 0 && in2 == KMASK) {  // p2 inside p1: all FromP2 (p1's edges never on the boundary)
+        if (pos == 0 && in2 == KMASK) {  // p2 inside p1: all FromP2, in order
             if (K == 4) s.w[0] = 0x83828180ull;
-            else { s.w[0] = 0x8786858483828180ull; s.w[1] = 0; }
-            cnt = K;
-            minpos = 0;
+            else { s.w[0] = 0x8786858483828180ull; s.w[Seq<K>::NW - 1] = 0; }
+            pos = K;
         }
-        nonempty = nonempty && cnt >= 3 && cnt <= 2 * K;
+        nonempty = nonempty && pos >= 3 && pos <= 2 * K;
         if (nonempty) {
-            out.seq = seq_rotate<K>(s, cnt, minpos);
-            out.nx = cnt;
+            out.seq = seq_canonical<K>(s, pos);
+            out.nx = pos;
         }
     }
     if (nonempty) {
@@ -355,11 +364,29 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
 // ---------------------------------------------------------------------------
 // backward: iou_grad through the recorded nx / xflags
 // ---------------------------------------------------------------------------
+// Flag-byte -> provenance bits, staged in shared memory by the kernel:
+//   v[b]: FromP1(i) -> bit i, FromP2(j) -> bit 8 + j
+//   x[b]: Cross(i,j) -> bit 8 i + j
+// (every other byte, including the 0x00 padding, maps to 0).
+struct FlagLut {
+    uint64_t x[256];
+    uint32_t v[256];
+};
+
+__device__ __forceinline__ void fill_flag_lut(FlagLut &L, int tid, int nthreads)
+{
+    for (int b = tid; b < 256; b += nthreads) {
+        const int tag = b >> 6, i = (b >> 3) & 7, j = b & 7;
+        L.v[b] = (tag == 1) ? (1u << j) : (tag == 2) ? (1u << (8 + j)) : 0u;
+        L.x[b] = (tag == 3) ? (1ull << (8 * i + j)) : 0ull;
+    }
+}
+
 // Returns dL/dv for p1 and p2 (recentred coordinates; the gradient is the same
 // in the original frame because IoU is translation invariant, R11).
 template <int K>
 __device__ __forceinline__ void iou_bwd(const Poly<K> &P, const Poly<K> &Q, float g, int nx,
-                                        const Seq<K> &seq, Poly<K> &G1, Poly<K> &G2)
+                                        const Seq<K> &seq, const FlagLut &L, Poly<K> &G1, Poly<K> &G2)
 {
 #pragma unroll
     for (int k = 0; k < K; ++k) { G1.x[k] = 0.f; G1.y[k] = 0.f; G2.x[k] = 0.f; G2.y[k] = 0.f; }
@@ -378,76 +405,53 @@ __device__ __forceinline__ void iou_bwd(const Poly<K> &P, const Poly<K> &Q, floa
         A2x2 += C2[i];
     }
 
-    // Which original vertices are vertices of p1 ∩ p2 (SWAR exact zero-byte test
-    // on the 2K flag bytes).
-    uint32_t m1 = 0, m2 = 0;
+    // provenance of the recorded vertices (the 0x00 padding maps to nothing)
+    uint32_t V = 0;
+    uint64_t X = 0;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        bool h1 = false, h2 = false;
-#pragma unroll
-        for (int w = 0; w < Seq<K>::NW; ++w) {
-            const uint64_t x1 = seq.w[w] ^ (0x4040404040404040ull | (0x0101010101010101ull * k));
-            const uint64_t x2 = seq.w[w] ^ (0x8080808080808080ull | (0x0101010101010101ull * k));
-            h1 |= (((x1 - 0x0101010101010101ull) & ~x1 & 0x8080808080808080ull) != 0);
-            h2 |= (((x2 - 0x0101010101010101ull) & ~x2 & 0x8080808080808080ull) != 0);
-        }
-        m1 |= (uint32_t)h1 << k;
-        m2 |= (uint32_t)h2 << k;
+    for (int p = 0; p < 2 * K; ++p) {
+        const uint32_t b = seq_byte<K>(seq, p);
+        V |= L.v[b];
+        X |= L.x[b];
     }
 
-    // Crossing vertices Cross(i, j): bytes whose two tag bits are both set.
-    // X = v_i + t g_i = w_j + s f_j.  P1 edge i ENTERS p2 there iff g_i x f_j < 0;
-    // then the boundary piece on edge i starts at t and the piece on p2 edge j
-    // ends at s, otherwise the other way round.
+    // Each recorded Cross(i, j) is X = v_i + t g_i = w_j + s f_j.  If p1 edge i
+    // enters p2 there (g_i x f_j < 0) the boundary piece on p1 edge i starts at t
+    // and the piece on p2 edge j ends at s; otherwise the other way round.
     float t0[K], t1[K], s0[K], s1[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) { t0[k] = 0.f; t1[k] = 1.f; s0[k] = 0.f; s1[k] = 1.f; }
-    uint32_t hc1 = 0, hc2 = 0;
 #pragma unroll
-    for (int w = 0; w < Seq<K>::NW; ++w) {
-        const uint64_t word = seq.w[w];
-        uint64_t c3 = word & (word << 1) & 0x8080808080808080ull;
-        while (c3) {
-            const int pos = __ffsll((long long)c3) - 1;  // bit 7 of the byte
-            c3 &= c3 - 1;
-            const uint32_t b = (uint32_t)(word >> (pos - 7)) & 0xFFu;
-            const int i = (b >> 3) & 7, j = b & 7;
-            const float vx = pick<K>(P.x, i), vy = pick<K>(P.y, i);
-            const float ex = pick<K>(gx, i), ey = pick<K>(gy, i);
-            const float wx = pick<K>(Q.x, j), wy = pick<K>(Q.y, j);
-            const float hx = pick<K>(fx, j), hy = pick<K>(fy, j);
-            const float Dx = wx - vx, Dy = wy - vy;
-            const float den = ex * hy - ey * hx;         // g_i x f_j
-            const float r = 1.f / den;
-            const float t = (Dx * hy - Dy * hx) * r;     // along p1 edge i
-            const float s = (Dx * ey - Dy * ex) * r;     // along p2 edge j
-            const bool enter = den < 0.f;                // f_j x g_i > 0: d rises along g_i
+    for (int i = 0; i < K; ++i)
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                if (k == i) { if (enter) t0[k] = t; else t1[k] = t; }
-                if (k == j) { if (enter) s1[k] = s; else s0[k] = s; }
-            }
-            hc1 |= 1u << i;
-            hc2 |= 1u << j;
+        for (int j = 0; j < K; ++j) {
+            const bool present = (X >> (8 * i + j)) & 1ull;
+            const float Dx = Q.x[j] - P.x[i], Dy = Q.y[j] - P.y[i];
+            const float den = gx[i] * fy[j] - gy[i] * fx[j];
+            const float r = rcp_approx(den);
+            const float t = __saturatef((Dx * fy[j] - Dy * fx[j]) * r);   // along p1 edge i
+            const float s = __saturatef((Dx * gy[i] - Dy * gx[i]) * r);   // along p2 edge j
+            const bool enter = den < 0.f;
+            t0[i] = (present & enter) ? t : t0[i];
+            t1[i] = (present & !enter) ? t : t1[i];
+            s1[j] = (present & enter) ? s : s1[j];
+            s0[j] = (present & !enter) ? s : s0[j];
         }
-    }
 
-    // Boundary intervals -> A_i and the per-edge weights
-    //   alpha = ∫ (1-t) dt = (t1-t0)(1 - (t0+t1)/2),  beta = ∫ t dt = (t1-t0)(t0+t1)/2.
+    // boundary pieces -> A_i and the edge weights
+    //   alpha = ∫ (1-t) dt = l (1 - h),  beta = ∫ t dt = l h,  l = t1 - t0, h = (t0 + t1)/2
     float al1[K], be1[K], al2[K], be2[K];
     float Aix2 = 0.f;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         const int i1 = (i + 1) % K;
-        const bool on1 = ((m1 >> i) & 1u) | ((m1 >> i1) & 1u) | ((hc1 >> i) & 1u);
-        const bool on2 = ((m2 >> i) & 1u) | ((m2 >> i1) & 1u) | ((hc2 >> i) & 1u);
-        const float a0 = fminf(fmaxf(t0[i], 0.f), 1.f), a1 = fminf(fmaxf(t1[i], 0.f), 1.f);
-        const float b0 = fminf(fmaxf(s0[i], 0.f), 1.f), b1 = fminf(fmaxf(s1[i], 0.f), 1.f);
-        const float l1 = on1 ? fmaxf(a1 - a0, 0.f) : 0.f;
-        const float l2 = on2 ? fmaxf(b1 - b0, 0.f) : 0.f;
-        const float h1 = 0.5f * (a0 + a1), h2 = 0.5f * (b0 + b1);
-        al1[i] = l1 * (1.f - h1); be1[i] = l1 * h1;
-        al2[i] = l2 * (1.f - h2); be2[i] = l2 * h2;
+        const bool on1 = (((V >> i) | (V >> i1)) & 1u) || ((X >> (8 * i)) & 0xFFull);
+        const bool on2 = (((V >> (8 + i)) | (V >> (8 + i1))) & 1u) || (X & (0x0101010101010101ull << i));
+        const float l1 = on1 ? fmaxf(t1[i] - t0[i], 0.f) : 0.f;
+        const float l2 = on2 ? fmaxf(s1[i] - s0[i], 0.f) : 0.f;
+        const float h1 = 0.5f * (t0[i] + t1[i]), h2 = 0.5f * (s0[i] + s1[i]);
+        al1[i] = l1 - l1 * h1; be1[i] = l1 * h1;
+        al2[i] = l2 - l2 * h2; be2[i] = l2 * h2;
         Aix2 = fmaf(l1, C1[i], Aix2);
         Aix2 = fmaf(l2, C2[i], Aix2);
     }

@@ -52,6 +52,9 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
                   float *__restrict__ gx1, float *__restrict__ gy1,
                   float *__restrict__ gx2, float *__restrict__ gy2)
 {
+    __shared__ FlagLut lut;
+    fill_flag_lut(lut, threadIdx.x, blockDim.x);
+    __syncthreads();
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     Poly<K> P, Q, G1, G2;
@@ -68,7 +71,7 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
         s.w[Seq<K>::NW - 1] = v.y;
     }
     recentre<K>(P, Q);
-    iou_bwd<K>(P, Q, g, m, s, G1, G2);
+    iou_bwd<K>(P, Q, g, m, s, lut, G1, G2);
     store_plane<K>(gx1, k, G1.x);
     store_plane<K>(gy1, k, G1.y);
     store_plane<K>(gx2, k, G2.x);

@@ -1,0 +1,174 @@
+"""GPU parity of the pairwise IoU matrix, the NMS overlap mask / suppressor lists
+and the greedy keep decision (dgal_iou_pairwise, dgal_nms_round, dgal_nms_keep)
+against the CPU oracle.  R14: mask bits of pairs with |IoU_oracle - thr| <= 1e-5
+are "don't care"; keep parity is oracle_scan(gpu_mask) == gpu_keep, and equals
+the oracle's own greedy NMS when no pair lies in that band."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2011_11134_b200 as dgal
+import synth
+from gpu_util import IOU_ATOL, dev, to_dev
+
+pytestmark = pytest.mark.gpu
+BAND = 1e-5
+
+
+def _bits(mask_i64, m):
+    """uint64 words [n, w] -> bool [n, m]"""
+    w = mask_i64.view(np.uint64)
+    b = np.unpackbits(w.view(np.uint8).reshape(w.shape[0], -1), axis=1, bitorder="little")
+    return b[:, :m].astype(bool)
+
+
+def _check_mask(gpu_bits, ref_iou, thr, row_offset=0):
+    n, m = ref_iou.shape
+    want = ref_iou > thr
+    rows = np.arange(n)[:, None] + row_offset
+    want &= np.arange(m)[None, :] != rows
+    care = np.abs(ref_iou - thr) > BAND
+    bad = (gpu_bits != want) & care
+    assert not bad.any(), f"{int(bad.sum())} mask bits differ (first {np.argwhere(bad)[:5]})"
+
+
+def _check_lists(gpu_bits, cnt, idx, row_offset=0):
+    n = gpu_bits.shape[0]
+    cap = idx.shape[1]
+    for r in range(n):
+        g = row_offset + r
+        want = set(np.nonzero(gpu_bits[r, :g])[0].tolist())
+        assert cnt[r] == len(want)
+        if cnt[r] <= cap:
+            assert set(idx[r, :cnt[r]].tolist()) == want
+
+
+@pytest.mark.parametrize("thr", [0.7, 0.3])
+def test_cfg2_full(thr):
+    sc = synth.gen_cfg2_scene()
+    p = sc.polys
+    x, y = to_dev(p)
+    iou, mask, cnt, idx = dgal.iou_pairwise(x, y, x, y, thr=thr, nbr_cap=64)
+    keep = dgal.nms_keep(mask, cnt, idx)
+    torch.cuda.synchronize()
+    ref = oracle.iou_pairwise(p, p)
+    got = iou.cpu().numpy()
+    err = np.abs(got - ref)
+    assert err.max() <= IOU_ATOL, err.max()
+    assert np.all(np.diag(got) == 1.0)
+    bits = _bits(mask.cpu().numpy(), p.n)
+    _check_mask(bits, ref, thr)
+    _check_lists(bits, cnt.cpu().numpy(), idx.cpu().numpy())
+    k = keep.cpu().numpy()
+    assert np.array_equal(k, oracle.nms_scan_mask(mask.cpu().numpy().view(np.uint64)))
+    if not np.any(np.abs(ref - thr) <= BAND):
+        assert np.array_equal(k, oracle.nms_greedy(ref, thr))
+
+
+def test_pairwise_equals_paired_forward():
+    """Row r x column c of the matrix is the paired forward of (r, c): the same
+    clip; the paired kernel carries line indices in the 3 low mantissa bits of
+    the interval parameters, so the two agree to a few ulp."""
+    sc = synth.gen_cfg2_scene(n_objects=10, per_object=30, seed=5)
+    p = sc.polys
+    x, y = to_dev(p)
+    iou, _, _, _ = dgal.iou_pairwise(x, y, x, y, want_mask=False)
+    n = p.n
+    rng = np.random.default_rng(0)
+    ri = rng.integers(0, n, 20000)
+    ci = rng.integers(0, n, 20000)
+    a, b = p.take(ri), p.take(ci)
+    x1, y1 = to_dev(a)
+    x2, y2 = to_dev(b)
+    pi, _, _ = dgal.iou_paired_fwd(x1, y1, x2, y2)
+    torch.cuda.synchronize()
+    d = np.abs(iou.cpu().numpy()[ri, ci] - pi.cpu().numpy())
+    assert d.max() <= 2e-6, d.max()
+
+
+@pytest.mark.parametrize("nr,m", [(1, 1), (37, 1500), (65, 1031), (200, 2049)])
+def test_ragged_shapes_and_row_blocks(nr, m):
+    sc = synth.gen_cfg5_scene(n_objects=max(1, (m + 49) // 50), per_object=50, seed=m)
+    cols = sc.polys.take(np.arange(m))
+    off = min(3, m - 1)
+    rows = cols.take(np.arange(off, min(m, off + nr)))
+    nr = rows.n
+    rx, ry = to_dev(rows)
+    cx, cy = to_dev(cols)
+    iou, mask, cnt, idx = dgal.iou_pairwise(rx, ry, cx, cy, row_offset=off, thr=0.1, nbr_cap=8)
+    torch.cuda.synchronize()
+    ref = oracle.iou_pairwise(rows, cols)
+    assert np.abs(iou.cpu().numpy() - ref).max() <= IOU_ATOL
+    bits = _bits(mask.cpu().numpy(), m)
+    _check_mask(bits, ref, 0.1, row_offset=off)
+    _check_lists(bits, cnt.cpu().numpy(), idx.cpu().numpy(), row_offset=off)
+
+
+def test_mask_only_and_k8():
+    b = synth.gen_cfg4_pairs(600, seed=3)
+    p = b.p1
+    x, y = to_dev(p)
+    iou, mask, _, _ = dgal.iou_pairwise(x, y, x, y, thr=0.2)
+    _, mask2, _, _ = dgal.iou_pairwise(x, y, x, y, thr=0.2, want_iou=False)
+    torch.cuda.synchronize()
+    ref = oracle.iou_pairwise(p, p)
+    assert np.abs(iou.cpu().numpy() - ref).max() <= IOU_ATOL
+    assert torch.equal(mask, mask2)
+    _check_mask(_bits(mask.cpu().numpy(), p.n), ref, 0.2)
+
+
+def test_nms_rounds_equal_keep_and_overflow_fallback():
+    sc = synth.gen_cfg5_scene(n_objects=200, per_object=50, seed=9)
+    x, y = to_dev(sc.polys)
+    n = sc.polys.n
+    _, mask, cnt, idx = dgal.iou_pairwise(x, y, x, y, thr=sc.thr, want_iou=False, nbr_cap=64)
+    keep = dgal.nms_keep(mask, cnt, idx)
+    # overflowing lists (cap 1) exercise the mask-scan path
+    _, mask1, cnt1, idx1 = dgal.iou_pairwise(x, y, x, y, thr=sc.thr, want_iou=False, nbr_cap=1)
+    keep1 = dgal.nms_keep(mask1, cnt1, idx1)
+    keep0 = dgal.nms_keep(mask)           # no lists at all
+    # host-driven rounds over two "row blocks" of one problem
+    status = torch.zeros(n, dtype=torch.uint8, device=dev())
+    und = torch.zeros(1, dtype=torch.int32, device=dev())
+    h = n // 2
+    for _ in range(10_000):
+        und.zero_()
+        dgal.nms_round(n, 0, mask[:h], cnt[:h], idx[:h], status, und)
+        dgal.nms_round(n, h, mask[h:], cnt[h:], idx[h:], status, und)
+        if int(und.item()) == 0:
+            break
+    torch.cuda.synchronize()
+    k = keep.cpu().numpy()
+    assert np.array_equal(k, oracle.nms_scan_mask(mask.cpu().numpy().view(np.uint64)))
+    assert np.array_equal(keep1.cpu().numpy(), k) and np.array_equal(keep0.cpu().numpy(), k)
+    assert np.array_equal((status == 1).to(torch.uint8).cpu().numpy(), k)
+    assert 0 < k.sum() < n
+
+
+def test_cfg5_full_size_sampled():
+    """100k x 100k at the bench's launch configuration: the full IoU matrix and
+    mask on the device; 128 sampled rows checked element by element; the keep
+    vector checked against the oracle's greedy scan of the GPU mask."""
+    sc = synth.gen_cfg5_scene()
+    p = sc.polys
+    n = p.n
+    x, y = to_dev(p)
+    iou, mask, cnt, idx = dgal.iou_pairwise(x, y, x, y, thr=sc.thr, nbr_cap=64)
+    keep = dgal.nms_keep(mask, cnt, idx)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(5)
+    rows = np.sort(rng.choice(n, 128, replace=False))
+    got = iou[torch.from_numpy(rows).to(dev())].cpu().numpy()
+    ref = oracle.iou_pairwise(p.take(rows), p)
+    assert np.abs(got - ref).max() <= IOU_ATOL
+    bits = _bits(mask[torch.from_numpy(rows).to(dev())].cpu().numpy(), n)
+    want = (ref > sc.thr) & (np.arange(n)[None, :] != rows[:, None])
+    care = np.abs(ref - sc.thr) > BAND
+    assert not ((bits != want) & care).any()
+    diag = iou.diagonal().cpu().numpy()
+    assert np.all(diag == 1.0)
+    del iou
+    k = keep.cpu().numpy()
+    assert np.array_equal(k, oracle.nms_scan_mask(mask.cpu().numpy().view(np.uint64)))
+    assert 0.05 < k.mean() < 0.9
