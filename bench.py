@@ -2,16 +2,20 @@
 """Benchmark of the DGAL hot path on B200 (driver contract: one JSON line).
 
 Headline workload = BASELINE cfg3: paired IoU loss forward + backward over 2^24
-KITTI-like rotated-box pairs Poly2<float,4> per GPU (one "step" = one
-dgal_iou_paired_fwd + one dgal_iou_paired_bwd over the whole batch, i.e. every
-§8(a) row of the paired path a0-a12).  Multi-GPU (torchrun, one process per
+KITTI-like rotated-box pairs Poly2<float,4> per GPU.  One "step" = one
+dgal_iou_paired_fwd + one dgal_iou_paired_bwd over the whole batch (every
+§8(a) row of the paired path, a0-a12).  Multi-GPU (torchrun, one process per
 GPU): weak scaling, each rank owns its own 2^24-pair shard, no collective on the
 data path; elapsed = max over ranks of the CUDA-event time.
+
+Secondary lines in the same JSON object ("secondary"): cfg4 (paired K=8
+octagons, 2^22 pairs per GPU, weak) and cfg5 (pairwise 100k x 100k IoU matrix +
+NMS mask + greedy keep, rows sharded over the GPUs: strong scaling).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
 --impl reference times the CPU oracle (oracle/, double precision, all host
-cores) on a bounded sample of the same workload (the tier's reference arm).
+cores) on a bounded sample of the same workload (this tier's reference arm).
 """
 from __future__ import annotations
 
@@ -29,12 +33,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "IoU pairs/sec fwd+bwd (1/2/4/8 B200), % of FP32/HBM roofline vs CPU oracle"
 UNIT = "pairs/s"
-N_PAIRS = 1 << 24        # cfg3 per GPU
-K = 4
-# algorithmic bytes per pair: fwd reads 4 planes x 16 B, writes
-# iou 4 + nx 1 + xflags 8; bwd reads 64 + g 4 + nx 1 + xflags 8, writes 64.
-FWD_BYTES = 64 + 4 + 1 + 8
-BWD_BYTES = 64 + 4 + 1 + 8 + 64
+
+
+def algorithmic_bytes(K):
+    """Per pair: fwd reads 2 polygons (16 K B) and writes iou 4 +
+    nx 1 + xflags 2K; bwd reads the polygons, g 4, nx 1, xflags 2K and writes the
+    two gradient polygons (16 K B)."""
+    poly = 16 * K
+    fwd = poly + 4 + 1 + 2 * K
+    bwd = poly + 4 + 1 + 2 * K + poly
+    return fwd, bwd
 
 
 def _env_int(name, default):
@@ -49,8 +57,8 @@ def measured_peaks():
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
-    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: 1 GiB bf16 copy, read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
 def ncu_traffic():
@@ -63,7 +71,7 @@ def ncu_traffic():
 
 
 class ClockSampler:
-    """NVML sampling of SM clock + throttle reasons while running (10 ms period)."""
+    """NVML sampling of SM clock + clock-event reasons (10 ms period)."""
 
     REASONS = {
         0x0000000000000002: "applications_clocks_setting",
@@ -87,7 +95,6 @@ class ClockSampler:
         except Exception as e:  # pragma: no cover
             self.err = str(e)
         self._stop = threading.Event()
-        self.window = None
 
     def _run(self):
         nv = self.nv
@@ -127,56 +134,240 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(win)}
 
 
-def cpu_oracle_rate(batch, seconds=10.0, threads=0):
-    """Time the oracle (fwd + bwd, as it stands) on a bounded prefix of the workload."""
+# ---------------------------------------------------------------------------
+# CPU oracle (reference arm and cpu_baseline)
+# ---------------------------------------------------------------------------
+def oracle_fwdbwd(s, nt):
     import oracle
-    nt = threads or oracle.max_threads()
-    probe = batch.take(np.arange(min(20000, batch.n)))
-    t = time.perf_counter()
-    oracle.iou_paired_fwd(probe.p1, probe.p2, nthreads=nt)
-    oracle.iou_paired_bwd(probe.p1, probe.p2, probe.grad, nthreads=nt)
-    rate = probe.n / (time.perf_counter() - t)
-    n = int(min(batch.n, max(probe.n, rate * seconds)))
-    s = batch.take(np.arange(n))
-    t = time.perf_counter()
     oracle.iou_paired_fwd(s.p1, s.p2, nthreads=nt)
     oracle.iou_paired_bwd(s.p1, s.p2, s.grad, nthreads=nt)
+
+
+def cpu_oracle_rate(sample, seconds=10.0):
+    """The oracle (as it stands: fwd + bwd in float64, OpenMP over all host
+    cores) timed on a bounded sample, repeated to ~`seconds` of CPU work."""
+    import oracle
+    nt = oracle.max_threads()
+    t = time.perf_counter()
+    oracle_fwdbwd(sample, nt)
     dt = time.perf_counter() - t
-    return n / dt, nt, n, dt
+    reps = max(1, int(seconds / max(dt, 1e-3)))
+    t = time.perf_counter()
+    for _ in range(reps):
+        oracle_fwdbwd(sample, nt)
+    dt = time.perf_counter() - t
+    return sample.n * reps / dt, nt, reps, dt
 
 
 def run_reference(args, rank):
-    import synth
     if rank != 0:
         return 0
-    batch = synth.gen_cfg3_pairs(1 << 20)
     import oracle
+    import synth
+    batch = synth.gen_cfg3_pairs(1 << 18)
     nt = oracle.max_threads()
-    # each step = fwd+bwd over a bounded sample (sized from a probe to ~2 s/step)
-    rate, nt, _, _ = cpu_oracle_rate(batch, seconds=1.0)
-    n = int(min(batch.n, max(20000, rate * 2.0)))
+    # each step = fwd+bwd over a bounded sample sized from a probe to ~1 s/step
+    probe = batch.take(np.arange(20000))
+    t = time.perf_counter()
+    oracle_fwdbwd(probe, nt)
+    rate = probe.n / (time.perf_counter() - t)
+    n = int(min(batch.n, max(20000, rate * 1.0)))
     s = batch.take(np.arange(n))
     for _ in range(args.warmup):
-        oracle.iou_paired_fwd(s.p1, s.p2, nthreads=nt)
-        oracle.iou_paired_bwd(s.p1, s.p2, s.grad, nthreads=nt)
+        oracle_fwdbwd(s, nt)
     t = time.perf_counter()
     for _ in range(args.steps):
-        oracle.iou_paired_fwd(s.p1, s.p2, nthreads=nt)
-        oracle.iou_paired_bwd(s.p1, s.p2, s.grad, nthreads=nt)
+        oracle_fwdbwd(s, nt)
     dt = time.perf_counter() - t
     v = n * args.steps / dt
-    sample = f"first {n} pairs of the cfg3 workload per step (of {N_PAIRS} per GPU), fwd+bwd, float64"
+    sample = (f"first {n} pairs of the cfg3 workload (of 2^24 per GPU) per step, fwd+bwd in float64, "
+              f"{nt} OpenMP threads")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "cfg3 paired IoU fwd+bwd, KITTI-like rotated boxes, K=4 (CPU oracle sample)",
-                   "pairs_per_step": n},
+        "config": {"workload": "cfg3: paired IoU loss fwd+bwd, KITTI-like rotated-box pairs, Poly2<float,4> "
+                               "(CPU oracle, bounded sample per step)", "pairs_per_step": n},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": nt, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
     return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+class Ctx:
+    def __init__(self, world, rank, local):
+        import torch
+        self.torch = torch
+        self.world, self.rank, self.local = world, rank, local
+        torch.cuda.set_device(local)
+        self.dev = torch.device("cuda", local)
+        self.dist = None
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("nccl", device_id=self.dev)
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max_over_ranks(self, v):
+        if not self.dist:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+
+def paired_inputs(ctx, cfg, n):
+    import synth
+    torch = ctx.torch
+    b = synth.gen_config(cfg, n, seed=synth.seed_for(cfg, ctx.rank))
+    K = b.p1.K
+    T = lambda a: torch.from_numpy(a.reshape(n, K)).to(ctx.dev)  # noqa: E731
+    x1, y1, x2, y2 = T(b.p1.x), T(b.p1.y), T(b.p2.x), T(b.p2.y)
+    g = torch.full((n,), -1.0 / n, dtype=torch.float32, device=ctx.dev)   # d mean(1 - IoU) / dIoU
+    return K, (x1, y1, x2, y2), g, b
+
+
+def time_paired(ctx, K, planes, g, steps, warmup, sampler=None):
+    """CUDA-event timing of `steps` fwd+bwd steps on the current stream; per-kernel
+    averages from events around each launch.  Returns (ms_total, fwd_ms, bwd_ms, t0, t1)."""
+    import paper_2011_11134_b200 as dgal
+    torch = ctx.torch
+    n = g.numel()
+    iou = torch.empty(n, dtype=torch.float32, device=ctx.dev)
+    nx = torch.empty(n, dtype=torch.uint8, device=ctx.dev)
+    xf = torch.empty((n, 2 * K), dtype=torch.uint8, device=ctx.dev)
+    grads = tuple(torch.empty((n, K), dtype=torch.float32, device=ctx.dev) for _ in range(4))
+    for _ in range(warmup):
+        dgal.iou_paired_fwd(*planes, out=(iou, nx, xf))
+        dgal.iou_paired_bwd(*planes, g, nx, xf, out=grads)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(ctx.dev)
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    start.record(stream)
+    for s in range(steps):
+        e0, e1, e2 = ev[s]
+        e0.record(stream)
+        dgal.iou_paired_fwd(*planes, out=(iou, nx, xf))
+        e1.record(stream)
+        dgal.iou_paired_bwd(*planes, g, nx, xf, out=grads)
+        e2.record(stream)
+    end.record(stream)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    ctx.barrier()
+    ms = start.elapsed_time(end)
+    fwd_ms = sum(a.elapsed_time(b) for a, b, _ in ev) / steps
+    bwd_ms = sum(b.elapsed_time(c) for _, b, c in ev) / steps
+    return ctx.max_over_ranks(ms), fwd_ms, bwd_ms, t0, t1, (iou, grads)
+
+
+def bench_e2e(ctx, K, planes, g, iou_dev, steps):
+    from paper_2011_11134_b200.hostpipe import HostPipeline
+    torch = ctx.torch
+    n = g.numel()
+    pipe = HostPipeline(K, device=ctx.dev)
+    x4h = torch.stack(planes).cpu().pin_memory()
+    gh = g.cpu().pin_memory()
+    iouh = torch.empty(n, dtype=torch.float32).pin_memory()
+    g4h = torch.empty((4, n, K), dtype=torch.float32).pin_memory()
+    pipe.run(x4h, gh, iouh, g4h)
+    torch.cuda.synchronize()
+    assert torch.equal(iouh, iou_dev.cpu()), "e2e IoU differs from the device-resident run"
+    ctx.barrier()
+    stream = torch.cuda.current_stream(ctx.dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        pipe.run(x4h, gh, iouh, g4h)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ems = ctx.max_over_ranks(a.elapsed_time(b))
+    return {"value": n * steps * ctx.world / (ems * 1e-3), "unit": UNIT,
+            "h2d_bytes_per_step": int(x4h.numel() * 4 + gh.numel() * 4),
+            "d2h_bytes_per_step": int(iouh.numel() * 4 + g4h.numel() * 4),
+            "ms_per_step": ems / steps, "steps": steps,
+            "path": "pinned host buffers -> 3-stream chunked pipeline (H2D, fwd, bwd, D2H) per GPU"}
+
+
+def bench_cfg5(ctx, steps, warmup, peak):
+    """Pairwise 100k x 100k IoU matrix + NMS mask/lists + greedy keep; rows sharded."""
+    import paper_2011_11134_b200 as dgal
+    import synth
+    from paper_2011_11134_b200.dist import nms_rounds, shard_range
+    torch = ctx.torch
+    sc = synth.gen_cfg5_scene()
+    n = sc.polys.n
+    x = torch.from_numpy(sc.polys.x.reshape(n, 4)).to(ctx.dev)
+    y = torch.from_numpy(sc.polys.y.reshape(n, 4)).to(ctx.dev)
+    B = -(-n // ctx.world)
+    lo, hi = shard_range(n, ctx.world, ctx.rank, B)
+    rx, ry = x[lo:hi].contiguous(), y[lo:hi].contiguous()
+    nr, words, cap = hi - lo, (n + 63) // 64, 64
+    out = (torch.empty((nr, n), dtype=torch.float32, device=ctx.dev),
+           torch.empty((nr, words), dtype=torch.int64, device=ctx.dev),
+           torch.empty(nr, dtype=torch.int32, device=ctx.dev),
+           torch.empty((nr, cap), dtype=torch.int32, device=ctx.dev))
+    status = torch.zeros(ctx.world * B, dtype=torch.uint8, device=ctx.dev)
+    keep = torch.empty(n, dtype=torch.uint8, device=ctx.dev)
+    und = torch.zeros(1, dtype=torch.int32, device=ctx.dev)
+
+    def step():
+        dgal.iou_pairwise(rx, ry, x, y, row_offset=lo, thr=sc.thr, nbr_cap=cap, out=out)
+        if ctx.world == 1:
+            dgal.nms_keep(out[1], out[2], out[3], status=status, keep=keep)
+            return 1
+        status.zero_()
+        r = nms_rounds(n, lo, hi, lambda st: dgal.nms_round(n, lo, out[1], out[2], out[3], st, und),
+                       status)
+        return r
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(ctx.dev)
+    ctx.barrier()
+    mat_ms, tot_ms, rounds = 0.0, 0.0, 0
+    for _ in range(steps):
+        a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record(stream)
+        dgal.iou_pairwise(rx, ry, x, y, row_offset=lo, thr=sc.thr, nbr_cap=cap, out=out)
+        b.record(stream)
+        if ctx.world == 1:
+            dgal.nms_keep(out[1], out[2], out[3], status=status, keep=keep)
+        else:
+            status.zero_()
+            rounds = nms_rounds(n, lo, hi,
+                                lambda st: dgal.nms_round(n, lo, out[1], out[2], out[3], st, und), status)
+        c.record(stream)
+        torch.cuda.synchronize()
+        mat_ms += a.elapsed_time(b)
+        tot_ms += a.elapsed_time(c)
+    mat_ms, tot_ms = mat_ms / steps, tot_ms / steps
+    mat_max = ctx.max_over_ranks(mat_ms)
+    tot_max = ctx.max_over_ranks(tot_ms)
+    kept = int((keep if ctx.world == 1 else (status[:n] == 1)).sum().item())
+    bytes_local = nr * n * 4 + nr * words * 8
+    del out
+    torch.cuda.empty_cache()
+    return {"workload": "cfg5: pairwise IoU 100k x 100k nuScenes-like boxes + NMS mask + greedy keep (thr 0.7)",
+            "scaling": "strong (rows sharded)", "n_gpus": ctx.world,
+            "pairs_per_s_matrix": n * n / (mat_max * 1e-3),
+            "ms_matrix": mat_max, "ms_matrix_plus_nms": tot_max, "nms_rounds": rounds, "kept": kept,
+            "roofline": {"bound": "hbm (output write)", "kernel": "pairwise_kernel<4>",
+                         "achieved": bytes_local / (mat_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": bytes_local / (mat_ms * 1e-3) / 1e9 / peak,
+                         "algorithmic_bytes_per_pair": 4.125}}
 
 
 def main(argv=None):
@@ -185,9 +376,10 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="dgal", choices=["dgal", "reference"])
-    ap.add_argument("--pairs", type=int, default=N_PAIRS, help="pairs per GPU (default: cfg3's 2^24)")
+    ap.add_argument("--pairs", type=int, default=1 << 24, help="cfg3 pairs per GPU (default 2^24)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
@@ -195,130 +387,64 @@ def main(argv=None):
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
-
     if args.impl == "reference":
         return run_reference(args, rank)
 
-    import torch
-    import paper_2011_11134_b200 as dgal
-    import synth
-    from paper_2011_11134_b200.hostpipe import HostPipeline
+    ctx = Ctx(world, rank, local)
+    torch = ctx.torch
+    peak, peak_src = measured_peaks()
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-
-    # ---- inputs: this rank's shard, resident in HBM ----
+    # ---- headline: cfg3 paired fwd+bwd, weak scaling ----
     n = args.pairs
-    batch = synth.gen_cfg3_pairs(n, seed=synth.seed_for(3, rank))
-    T = lambda a: torch.from_numpy(a).to(dev)  # noqa: E731
-    x1, y1 = T(batch.p1.x.reshape(n, K)), T(batch.p1.y.reshape(n, K))
-    x2, y2 = T(batch.p2.x.reshape(n, K)), T(batch.p2.y.reshape(n, K))
-    g = torch.full((n,), -1.0 / n, dtype=torch.float32, device=dev)   # d(mean(1-IoU))/dIoU
-    iou = torch.empty(n, dtype=torch.float32, device=dev)
-    nx = torch.empty(n, dtype=torch.uint8, device=dev)
-    xf = torch.empty((n, 2 * K), dtype=torch.uint8, device=dev)
-    grads = tuple(torch.empty((n, K), dtype=torch.float32, device=dev) for _ in range(4))
-
-    def step():
-        dgal.iou_paired_fwd(x1, y1, x2, y2, out=(iou, nx, xf))
-        dgal.iou_paired_bwd(x1, y1, x2, y2, g, nx, xf, out=grads)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-
+    K, planes, g, batch = paired_inputs(ctx, 3, n)
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.05)
-    stream = torch.cuda.current_stream(dev)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t_wall0 = time.perf_counter()
-    start = torch.cuda.Event(enable_timing=True)
-    end = torch.cuda.Event(enable_timing=True)
-    start.record(stream)
-    for s in range(args.steps):
-        e0, e1, e2 = ev[s]
-        e0.record(stream)
-        dgal.iou_paired_fwd(x1, y1, x2, y2, out=(iou, nx, xf))
-        e1.record(stream)
-        dgal.iou_paired_bwd(x1, y1, x2, y2, g, nx, xf, out=grads)
-        e2.record(stream)
-    end.record(stream)
-    torch.cuda.synchronize()
-    t_wall1 = time.perf_counter()
-    if dist:
-        dist.barrier()
+    ms, fwd_ms, bwd_ms, t0, t1, (iou_dev, _) = time_paired(ctx, K, planes, g, args.steps, args.warmup)
     time.sleep(0.02)
     sampler.stop()
+    value = n * args.steps * world / (ms * 1e-3)
+    fb, bb = algorithmic_bytes(K)
+    fwd_gbs = n * fb / (fwd_ms * 1e-3) / 1e9
+    bwd_gbs = n * bb / (bwd_ms * 1e-3) / 1e9
 
-    ms = start.elapsed_time(end)
-    fwd_ms = sum(a.elapsed_time(b) for a, b, _ in ev) / args.steps
-    bwd_ms = sum(b.elapsed_time(c) for _, b, c in ev) / args.steps
-    if dist:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    total_pairs = n * args.steps * world
-    value = total_pairs / (ms * 1e-3)
+    e2e = None if args.no_e2e else bench_e2e(ctx, K, planes, g, iou_dev, args.e2e_steps)
+    del planes, g, iou_dev
+    torch.cuda.empty_cache()
 
-    # ---- e2e: host buffers, H2D + fwd + bwd + D2H inside the timed region ----
-    e2e = None
-    if not args.no_e2e:
-        pipe = HostPipeline(K, device=dev)
-        x4h = torch.stack([x1, y1, x2, y2]).cpu().pin_memory()
-        gh = g.cpu().pin_memory()
-        iouh = torch.empty(n, dtype=torch.float32).pin_memory()
-        g4h = torch.empty((4, n, K), dtype=torch.float32).pin_memory()
-        pipe.run(x4h, gh, iouh, g4h)
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(args.e2e_steps):
-            pipe.run(x4h, gh, iouh, g4h)
-        b.record(stream)
-        torch.cuda.synchronize()
-        ems = a.elapsed_time(b)
-        if dist:
-            t = torch.tensor([ems], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
-        e2e = {"value": n * args.e2e_steps * world / (ems * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": int(x4h.numel() * 4 + gh.numel() * 4),
-               "d2h_bytes_per_step": int(iouh.numel() * 4 + g4h.numel() * 4),
-               "ms_per_step": ems / args.e2e_steps,
-               "path": "pinned host -> chunked 3-stream pipeline (H2D, fwd, bwd, D2H)"}
-        # sanity: the e2e result equals the device result
-        assert torch.equal(iouh, iou.cpu()), "e2e IoU differs from device IoU"
+    secondary = {}
+    if not args.no_secondary:
+        n4 = 1 << 22
+        K4, planes4, g4, _ = paired_inputs(ctx, 4, n4)
+        ms4, f4, b4, _, _, _ = time_paired(ctx, K4, planes4, g4, max(10, args.steps // 4), args.warmup)
+        fb4, bb4 = algorithmic_bytes(K4)
+        secondary["cfg4"] = {
+            "workload": "cfg4: paired IoU fwd+bwd, 2^22 convex octagon pairs Poly2<float,8> per GPU",
+            "scaling": "weak", "pairs_per_s": n4 * max(10, args.steps // 4) * world / (ms4 * 1e-3),
+            "ms_per_step": ms4 / max(10, args.steps // 4),
+            "paired_fwd": {"ms": f4, "GB/s": n4 * fb4 / (f4 * 1e-3) / 1e9,
+                           "frac": n4 * fb4 / (f4 * 1e-3) / 1e9 / peak},
+            "paired_bwd": {"ms": b4, "GB/s": n4 * bb4 / (b4 * 1e-3) / 1e9,
+                           "frac": n4 * bb4 / (b4 * 1e-3) / 1e9 / peak}}
+        del planes4, g4
+        torch.cuda.empty_cache()
+        secondary["cfg5"] = bench_cfg5(ctx, steps=5, warmup=2, peak=peak)
 
-    if dist:
-        dist.destroy_process_group()
+    if ctx.dist:
+        ctx.dist.destroy_process_group()
     if rank != 0:
         return 0
 
-    peak, peak_src = measured_peaks()
-    fwd_gbs = n * FWD_BYTES / (fwd_ms * 1e-3) / 1e9
-    bwd_gbs = n * BWD_BYTES / (bwd_ms * 1e-3) / 1e9
     dom = "paired_fwd" if fwd_ms >= bwd_ms else "paired_bwd"
     dom_gbs = fwd_gbs if dom == "paired_fwd" else bwd_gbs
     traffic = ncu_traffic().get(f"{dom}_k4_bytes_per_launch")
-    clocks = sampler.summary(t_wall0, t_wall1)
-
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        sample = synth.gen_cfg3_pairs(1 << 20, seed=synth.seed_for(3, rank))
-        rate, nt, ns, dt = cpu_oracle_rate(sample, seconds=10.0)
+        sample = batch.take(np.arange(1 << 18))
+        rate, nt, reps, dt = cpu_oracle_rate(sample, seconds=10.0)
         cpu = {"value": rate, "unit": UNIT, "cores": nt, "kind": "oracle",
-               "sample": f"first {ns} pairs of this cfg3 workload, fwd+bwd in float64 ({dt:.1f} s)"}
+               "sample": f"first {sample.n} pairs of this cfg3 batch, fwd+bwd in float64, repeated {reps}x "
+                         f"({dt:.1f} s, {nt} OpenMP threads)"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -327,17 +453,19 @@ def main(argv=None):
         "config": {"workload": "cfg3: paired IoU loss fwd+bwd, KITTI-like rotated-box pairs, Poly2<float,4>",
                    "pairs_per_gpu": n, "global_pairs": n * world, "K": K,
                    "parallelism": f"dp{world} (contiguous pair shards, no collective)",
-                   "l2": "inputs 1.07 GB/GPU > 126 MB L2 (no flush needed)"},
+                   "l2": "inputs 1.07 GB/GPU > 126 MB L2, no flush needed"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": peak, "unit": "GB/s",
                      "frac": dom_gbs / peak, "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_pair": {"paired_fwd": FWD_BYTES, "paired_bwd": BWD_BYTES},
+                     "algorithmic_bytes_per_pair": {"paired_fwd": fb, "paired_bwd": bb},
                      "paired_fwd": {"ms": fwd_ms, "GB/s": fwd_gbs, "frac": fwd_gbs / peak},
                      "paired_bwd": {"ms": bwd_ms, "GB/s": bwd_gbs, "frac": bwd_gbs / peak},
-                     "step_frac": (n * (FWD_BYTES + BWD_BYTES) / (ms / args.steps * 1e-3) / 1e9) / peak},
-        "clocks": clocks,
+                     "step_GB/s": n * (fb + bb) / (ms / args.steps * 1e-3) / 1e9,
+                     "step_frac": n * (fb + bb) / (ms / args.steps * 1e-3) / 1e9 / peak},
+        "clocks": sampler.summary(t0, t1),
         "gpu_launches": 2 * args.steps,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "secondary": secondary,
     }
     print(json.dumps(line))
     return 0

@@ -43,8 +43,10 @@ paired_fwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
     }
 }
 
+// K=4: cap registers at 80 so 3 CTAs (24 warps) fit per SM — the backward moves
+// 141 B/pair and was latency-bound (long_scoreboard) at 2 CTAs/SM.
 template <int K>
-__global__ void __launch_bounds__(kPairedThreads)
+__global__ void __launch_bounds__(kPairedThreads, (K == 4) ? 3 : 1)
 paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
                   const float *__restrict__ x2, const float *__restrict__ y2,
                   const float *__restrict__ grad, const uint8_t *__restrict__ nx,

@@ -39,16 +39,18 @@ class HostPipeline:
             s = self.streams[c % self.ns]
             b = self.buf[c % self.ns]
             with torch.cuda.stream(s):
-                xin = b["xin"][:, :m]
-                xin.copy_(x4_host[:, off:off + m], non_blocking=True)
+                # one contiguous copy per plane (a strided [4, m, K] copy is slow)
+                planes = [b["xin"][i, :m] for i in range(4)]
+                for i in range(4):
+                    planes[i].copy_(x4_host[i, off:off + m], non_blocking=True)
                 g = b["g"][:m]
                 g.copy_(g_host[off:off + m], non_blocking=True)
-                x1, y1, x2, y2 = (xin[i] for i in range(4))
-                iou, nx, xf = iou_paired_fwd(x1, y1, x2, y2, out=(b["iou"][:m], b["nx"][:m], b["xf"][:m]))
-                go = b["gout"][:, :m]
-                iou_paired_bwd(x1, y1, x2, y2, g, nx, xf, out=tuple(go[i] for i in range(4)))
+                iou, nx, xf = iou_paired_fwd(*planes, out=(b["iou"][:m], b["nx"][:m], b["xf"][:m]))
+                go = [b["gout"][i, :m] for i in range(4)]
+                iou_paired_bwd(*planes, g, nx, xf, out=tuple(go))
                 iou_host[off:off + m].copy_(iou, non_blocking=True)
-                grad4_host[:, off:off + m].copy_(go, non_blocking=True)
+                for i in range(4):
+                    grad4_host[i, off:off + m].copy_(go[i], non_blocking=True)
             c += 1
         for s in self.streams:
             cur.wait_stream(s)

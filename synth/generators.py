@@ -19,6 +19,7 @@ This module holds no arithmetic of the method (no clipping, area or IoU).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -116,11 +117,19 @@ def boxes_to_polys(cx, cy, length, width, theta) -> Polys:
 
 
 def _chunked(n, seed, draw_chunk):
-    """Call draw_chunk(rng, CHUNK) for ceil(n/CHUNK) chunks, concat, truncate."""
+    """Call draw_chunk(rng, CHUNK) for ceil(n/CHUNK) chunks (each with its own
+    SeedSequence child, drawn in a thread pool — the result does not depend on
+    the scheduling), concat, truncate."""
     nch = max(1, -(-n // CHUNK))
     ss = np.random.SeedSequence(seed)
-    parts = [draw_chunk(np.random.Generator(np.random.PCG64(child)), CHUNK)
-             for child in ss.spawn(nch)]
+    children = ss.spawn(nch)
+    job = lambda c: draw_chunk(np.random.Generator(np.random.PCG64(c)), CHUNK)  # noqa: E731
+    if nch >= 8:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 4)) as ex:
+            parts = list(ex.map(job, children))
+    else:
+        parts = [job(c) for c in children]
     return [np.concatenate(fields)[:n] for fields in zip(*parts)]
 
 
