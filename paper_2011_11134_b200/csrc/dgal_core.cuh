@@ -63,10 +63,13 @@ __device__ __forceinline__ float rcp_approx(float x)
     return r;
 }
 
-// carry a line index 0..7 in the 3 low mantissa bits of a finite-or-NaN value
+// carry a line index 0..7 in the 3 low mantissa bits of a finite value:
+// one LOP3 (v & ~7) | j with j in a register
 __device__ __forceinline__ float enc_idx(float v, int j)
 {
-    return __int_as_float((__float_as_int(v) & ~7) | j);
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(__float_as_uint(v)), "n"(0xFFFFFFF8), "r"(j));
+    return __uint_as_float(r);
 }
 __device__ __forceinline__ int dec_idx(float v) { return __float_as_int(v) & 7; }
 
@@ -254,14 +257,21 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
             // t* = 0 or 1 exactly, so identical polygons keep [0, 1] intervals.
             {   // p1 edge i vs p2 line j
                 const float a = d[i][j], b = d[i1][j];
-                const float den = a - b;
-                const float r = rcp_approx(den);
-                const float m = __saturatef(-den * kBig);      // 1: bounds below
-                float tE = m * (a * r);                       // finite or NaN
-                float tX = fmaf(m, kBig, fmaf(b, r, 1.f));    // +-inf when a == b
-                if (FLAGS) { tE = enc_idx(tE, j); tX = enc_idx(fmaxf(tX, -1.f), j); }
-                lo = fmaxf(lo, tE);
-                hi = fminf(hi, tX);
+                if (FLAGS) {
+                    // den + tiny keeps r finite (a == b: r = 1e30, t* = +-huge): the
+                    // candidates stay finite, so the index bits survive
+                    const float den = (a - b) + kTiny;
+                    const float r = rcp_approx(den);
+                    const float m = __saturatef(-den * kBig);  // 1: bounds below
+                    lo = fmaxf(lo, enc_idx(m * (a * r), j));
+                    hi = fminf(hi, enc_idx(fmaf(m, kBig, fmaf(b, r, 1.f)), j));
+                } else {
+                    const float den = a - b;
+                    const float r = rcp_approx(den);
+                    const float m = __saturatef(-den * kBig);  // 1: bounds below
+                    lo = fmaxf(lo, m * (a * r));               // finite or NaN (ignored)
+                    hi = fminf(hi, fmaf(m, kBig, fmaf(b, r, 1.f)));  // +-inf when a == b
+                }
             }
             {   // p2 edge i vs p1 line j
                 const float a = e[i][j], b = e[i1][j];
