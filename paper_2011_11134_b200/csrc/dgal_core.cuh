@@ -376,10 +376,8 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
 // ---------------------------------------------------------------------------
 // Flag-byte -> provenance bits, staged in shared memory by the kernel:
 //   v[b]: FromP1(i) -> bit i, FromP2(j) -> bit 8 + j
-//   x[b]: Cross(i,j) -> bit 8 i + j
 // (every other byte, including the 0x00 padding, maps to 0).
 struct FlagLut {
-    uint64_t x[256];
     uint32_t v[256];
 };
 
@@ -387,21 +385,42 @@ __device__ __forceinline__ void fill_flag_lut(FlagLut &L, int tid, int nthreads)
 {
     for (int b = tid; b < 256; b += nthreads) {
         const int tag = b >> 6, i = (b >> 3) & 7, j = b & 7;
+        (void)i;
         L.v[b] = (tag == 1) ? (1u << j) : (tag == 2) ? (1u << (8 + j)) : 0u;
-        L.x[b] = (tag == 3) ? (1ull << (8 * i + j)) : 0ull;
     }
 }
 
-// Returns dL/dv for p1 and p2 (recentred coordinates; the gradient is the same
-// in the original frame because IoU is translation invariant, R11).
-template <int K>
-__device__ __forceinline__ void iou_bwd(const Poly<K> &P, const Poly<K> &Q, float g, int nx,
-                                        const Seq<K> &seq, const FlagLut &L, Poly<K> &G1, Poly<K> &G2)
+// Backward of one pair whose raw inputs sit in shared memory (this thread's K
+// vertices at sPx[0..K-1] etc.), writing dL/dv of p1 and p2 (the same in the
+// recentred and the original frame: IoU is translation invariant, R11).
+//
+// The crossing loop visits only the Cross bytes actually recorded in xflags
+// (2.7 per pair on cfg3 instead of K^2 candidate pairs), reading the four
+// vertices it needs by dynamic index from shared memory and writing the two
+// interval end points it defines into `scr`, a per-thread scratch transposed as
+// [slot][kTile] so that dynamic slots never conflict on banks:
+//   slot i = t0 of p1 edge i, K + i = t1, 2K + j = s0 of p2 edge j, 3K + j = s1.
+// Coordinates are used raw there: vertex differences of one scene are exact
+// (Sterbenz) and the crossing parameters only need differences.
+template <int K, int TILE>
+__device__ __forceinline__ void iou_bwd_smem(const float *sPx, const float *sPy, const float *sQx,
+                                             const float *sQy, float g, int nx, const Seq<K> &seq,
+                                             const FlagLut &L, float *scr, Poly<K> &G1, Poly<K> &G2)
 {
 #pragma unroll
     for (int k = 0; k < K; ++k) { G1.x[k] = 0.f; G1.y[k] = 0.f; G2.x[k] = 0.f; G2.y[k] = 0.f; }
     if (nx == 0) return;
 
+    // recentred register copies (origin p1.v0) for the edge normals and shoelace terms
+    Poly<K> P, Q;
+    {
+        const float ox = sPx[0], oy = sPy[0];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            P.x[k] = sPx[k] - ox; P.y[k] = sPy[k] - oy;
+            Q.x[k] = sQx[k] - ox; Q.y[k] = sQy[k] - oy;
+        }
+    }
     float gx[K], gy[K], fx[K], fy[K], C1[K], C2[K];
     float A1x2 = 0.f, A2x2 = 0.f;
 #pragma unroll
@@ -417,36 +436,48 @@ __device__ __forceinline__ void iou_bwd(const Poly<K> &P, const Poly<K> &Q, floa
 
     // provenance of the recorded vertices (the 0x00 padding maps to nothing)
     uint32_t V = 0;
-    uint64_t X = 0;
 #pragma unroll
-    for (int p = 0; p < 2 * K; ++p) {
-        const uint32_t b = seq_byte<K>(seq, p);
-        V |= L.v[b];
-        X |= L.x[b];
+    for (int p = 0; p < 2 * K; ++p) V |= L.v[seq_byte<K>(seq, p)];
+
+    // default interval end points: pieces run vertex to vertex
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        scr[k * TILE] = 0.f;
+        scr[(K + k) * TILE] = 1.f;
+        scr[(2 * K + k) * TILE] = 0.f;
+        scr[(3 * K + k) * TILE] = 1.f;
     }
 
     // Each recorded Cross(i, j) is X = v_i + t g_i = w_j + s f_j.  If p1 edge i
     // enters p2 there (g_i x f_j < 0) the boundary piece on p1 edge i starts at t
     // and the piece on p2 edge j ends at s; otherwise the other way round.
-    float t0[K], t1[K], s0[K], s1[K];
+    uint32_t hc1 = 0, hc2 = 0;
 #pragma unroll
-    for (int k = 0; k < K; ++k) { t0[k] = 0.f; t1[k] = 1.f; s0[k] = 0.f; s1[k] = 1.f; }
-#pragma unroll
-    for (int i = 0; i < K; ++i)
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const bool present = (X >> (8 * i + j)) & 1ull;
-            const float Dx = Q.x[j] - P.x[i], Dy = Q.y[j] - P.y[i];
-            const float den = gx[i] * fy[j] - gy[i] * fx[j];
+    for (int w = 0; w < Seq<K>::NW; ++w) {
+        const uint64_t word = seq.w[w];
+        uint64_t c3 = word & (word << 1) & 0x8080808080808080ull;
+        while (c3) {
+            const int pos = __ffsll((long long)c3) - 1;  // bit 7 of the byte
+            c3 &= c3 - 1;
+            const uint32_t b = (uint32_t)(word >> (pos - 7));
+            const int i = (b >> 3) & (K - 1), j = b & (K - 1);
+            const int i1 = (i + 1) & (K - 1), j1 = (j + 1) & (K - 1);
+            const float vx = sPx[i], vy = sPy[i];
+            const float ex = sPx[i1] - vx, ey = sPy[i1] - vy;
+            const float wx = sQx[j], wy = sQy[j];
+            const float hx = sQx[j1] - wx, hy = sQy[j1] - wy;
+            const float Dx = wx - vx, Dy = wy - vy;
+            const float den = ex * hy - ey * hx;              // g_i x f_j
             const float r = rcp_approx(den);
-            const float t = __saturatef((Dx * fy[j] - Dy * fx[j]) * r);   // along p1 edge i
-            const float s = __saturatef((Dx * gy[i] - Dy * gx[i]) * r);   // along p2 edge j
+            const float t = __saturatef((Dx * hy - Dy * hx) * r);   // along p1 edge i
+            const float s = __saturatef((Dx * ey - Dy * ex) * r);   // along p2 edge j
             const bool enter = den < 0.f;
-            t0[i] = (present & enter) ? t : t0[i];
-            t1[i] = (present & !enter) ? t : t1[i];
-            s1[j] = (present & enter) ? s : s1[j];
-            s0[j] = (present & !enter) ? s : s0[j];
+            scr[(enter ? i : K + i) * TILE] = t;
+            scr[(enter ? 3 * K + j : 2 * K + j) * TILE] = s;
+            hc1 |= 1u << i;
+            hc2 |= 1u << j;
         }
+    }
 
     // boundary pieces -> A_i and the edge weights
     //   alpha = ∫ (1-t) dt = l (1 - h),  beta = ∫ t dt = l h,  l = t1 - t0, h = (t0 + t1)/2
@@ -455,11 +486,13 @@ __device__ __forceinline__ void iou_bwd(const Poly<K> &P, const Poly<K> &Q, floa
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         const int i1 = (i + 1) % K;
-        const bool on1 = (((V >> i) | (V >> i1)) & 1u) || ((X >> (8 * i)) & 0xFFull);
-        const bool on2 = (((V >> (8 + i)) | (V >> (8 + i1))) & 1u) || (X & (0x0101010101010101ull << i));
-        const float l1 = on1 ? fmaxf(t1[i] - t0[i], 0.f) : 0.f;
-        const float l2 = on2 ? fmaxf(s1[i] - s0[i], 0.f) : 0.f;
-        const float h1 = 0.5f * (t0[i] + t1[i]), h2 = 0.5f * (s0[i] + s1[i]);
+        const bool on1 = (((V >> i) | (V >> i1) | (hc1 >> i)) & 1u) != 0;
+        const bool on2 = (((V >> (8 + i)) | (V >> (8 + i1)) | (hc2 >> i)) & 1u) != 0;
+        const float a0 = scr[i * TILE], a1 = scr[(K + i) * TILE];
+        const float b0 = scr[(2 * K + i) * TILE], b1 = scr[(3 * K + i) * TILE];
+        const float l1 = on1 ? fmaxf(a1 - a0, 0.f) : 0.f;
+        const float l2 = on2 ? fmaxf(b1 - b0, 0.f) : 0.f;
+        const float h1 = 0.5f * (a0 + a1), h2 = 0.5f * (b0 + b1);
         al1[i] = l1 - l1 * h1; be1[i] = l1 * h1;
         al2[i] = l2 - l2 * h2; be2[i] = l2 * h2;
         Aix2 = fmaf(l1, C1[i], Aix2);

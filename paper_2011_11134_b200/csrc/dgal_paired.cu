@@ -2,6 +2,7 @@
 // pair, polygons and clip state in registers, float4 SoA streaming loads.
 #include "dgal_core.cuh"
 #include "dgal_internal.h"
+#include "dgal_pipe.cuh"
 
 namespace dgal {
 
@@ -43,41 +44,103 @@ paired_fwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
     }
 }
 
-// K=4: cap registers at 80 so 3 CTAs (24 warps) fit per SM — the backward moves
-// 141 B/pair and was latency-bound (long_scoreboard) at 2 CTAs/SM.
+// ---------------------------------------------------------------------------
+// Backward: persistent CTAs, bulk-copy (TMA engine) pipeline of input tiles
+// ---------------------------------------------------------------------------
+// One tile = kTile consecutive pairs = one contiguous byte range per input
+// (x1, y1, x2, y2, grad, xflags, nx).  Thread 0 prefetches tile it+1 into the
+// other stage of a 2-deep shared-memory ring while every thread computes tile
+// it from shared memory, so the 141 B/pair of HBM traffic overlaps the math at
+// any occupancy.  The tail tile (or misaligned inputs) is loaded directly.
+constexpr int kTile = 256;
+
 template <int K>
-__global__ void __launch_bounds__(kPairedThreads, (K == 4) ? 3 : 1)
+struct BwdSmem {
+    struct Stage {
+        float x1[kTile * K], y1[kTile * K], x2[kTile * K], y2[kTile * K];
+        float g[kTile];
+        uint64_t xf[kTile * (K / 4)];  // 2K flag bytes per pair
+        uint8_t nx[kTile];
+    };
+    Stage st[2];
+    float scr[4 * K * kTile];  // crossing end points, [slot][thread]
+    FlagLut lut;
+    uint64_t bar[2];
+};
+
+template <int K>
+__global__ void __launch_bounds__(kTile, (K == 4) ? 3 : 1)
 paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
                   const float *__restrict__ x2, const float *__restrict__ y2,
                   const float *__restrict__ grad, const uint8_t *__restrict__ nx,
                   const uint8_t *__restrict__ xflags,
                   float *__restrict__ gx1, float *__restrict__ gy1,
-                  float *__restrict__ gx2, float *__restrict__ gy2)
+                  float *__restrict__ gx2, float *__restrict__ gy2, int use_bulk)
 {
-    __shared__ FlagLut lut;
-    fill_flag_lut(lut, threadIdx.x, blockDim.x);
-    __syncthreads();
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    Poly<K> P, Q, G1, G2;
-    load_poly<K>(x1, y1, k, P);
-    load_poly<K>(x2, y2, k, Q);
-    const float g = __ldcs(grad + k);
-    const int m = nx[k];
-    Seq<K> s;
-    if (K == 4) {
-        s.w[0] = __ldcs(reinterpret_cast<const unsigned long long *>(xflags) + k);
-    } else {
-        const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2 *>(xflags) + k);
-        s.w[0] = v.x;
-        s.w[Seq<K>::NW - 1] = v.y;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    BwdSmem<K> &S = *reinterpret_cast<BwdSmem<K> *>(smem_raw);
+    const int tid = threadIdx.x;
+    const int64_t ntiles = (n + kTile - 1) / kTile;
+    const int64_t nfull = use_bulk ? n / kTile : 0;  // tiles fed by bulk copies
+    constexpr uint32_t kStageBytes = 4u * kTile * K * 4u + kTile * 4u + kTile * 2u * K + kTile;
+
+    fill_flag_lut(S.lut, tid, kTile);
+    if (tid == 0) {
+        mbar_init(&S.bar[0], 1);
+        mbar_init(&S.bar[1], 1);
+        fence_mbar_init();
     }
-    recentre<K>(P, Q);
-    iou_bwd<K>(P, Q, g, m, s, lut, G1, G2);
-    store_plane<K>(gx1, k, G1.x);
-    store_plane<K>(gy1, k, G1.y);
-    store_plane<K>(gx2, k, G2.x);
-    store_plane<K>(gy2, k, G2.y);
+    __syncthreads();
+
+    auto issue = [&](int64_t tile, int s) {
+        const int64_t b = tile * kTile;
+        typename BwdSmem<K>::Stage &T = S.st[s];
+        mbar_arrive_expect_tx(&S.bar[s], kStageBytes);
+        bulk_g2s(T.x1, x1 + b * K, kTile * K * 4, &S.bar[s]);
+        bulk_g2s(T.y1, y1 + b * K, kTile * K * 4, &S.bar[s]);
+        bulk_g2s(T.x2, x2 + b * K, kTile * K * 4, &S.bar[s]);
+        bulk_g2s(T.y2, y2 + b * K, kTile * K * 4, &S.bar[s]);
+        bulk_g2s(T.g, grad + b, kTile * 4, &S.bar[s]);
+        bulk_g2s(T.xf, xflags + b * 2 * K, kTile * 2 * K, &S.bar[s]);
+        bulk_g2s(T.nx, nx + b, kTile, &S.bar[s]);
+    };
+
+    int64_t tile = blockIdx.x;
+    if (tid == 0 && tile < nfull) issue(tile, 0);
+    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+        const int s = it & 1;
+        const int64_t next = tile + gridDim.x;
+        if (tid == 0 && next < nfull) issue(next, s ^ 1);
+        typename BwdSmem<K>::Stage &T = S.st[s];
+        const int64_t k = tile * kTile + tid;
+        if (tile < nfull) {
+            mbar_wait(&S.bar[s], (uint32_t)(it >> 1) & 1u);
+        } else if (k < n) {  // direct path: this thread stages its own pair
+#pragma unroll
+            for (int q = 0; q < K; ++q) {
+                T.x1[tid * K + q] = x1[k * K + q]; T.y1[tid * K + q] = y1[k * K + q];
+                T.x2[tid * K + q] = x2[k * K + q]; T.y2[tid * K + q] = y2[k * K + q];
+            }
+            T.g[tid] = grad[k];
+            T.nx[tid] = nx[k];
+#pragma unroll
+            for (int q = 0; q < K / 4; ++q)
+                T.xf[tid * (K / 4) + q] = reinterpret_cast<const uint64_t *>(xflags)[k * (K / 4) + q];
+        }
+        if (k < n) {
+            Seq<K> sq;
+#pragma unroll
+            for (int q = 0; q < K / 4; ++q) sq.w[q] = T.xf[tid * (K / 4) + q];
+            Poly<K> G1, G2;
+            iou_bwd_smem<K, kTile>(T.x1 + tid * K, T.y1 + tid * K, T.x2 + tid * K, T.y2 + tid * K, T.g[tid],
+                                   T.nx[tid], sq, S.lut, S.scr + tid, G1, G2);
+            store_plane<K>(gx1, k, G1.x);
+            store_plane<K>(gy1, k, G1.y);
+            store_plane<K>(gx2, k, G2.x);
+            store_plane<K>(gy2, k, G2.y);
+        }
+        __syncthreads();  // stage s fully consumed before it is refilled
+    }
 }
 
 static inline unsigned grid_for(int64_t n) { return (unsigned)((n + kPairedThreads - 1) / kPairedThreads); }
@@ -93,18 +156,43 @@ cudaError_t launch_paired_fwd(int K, int64_t n, const float *x1, const float *y1
     return cudaGetLastError();
 }
 
+namespace {
+template <int K>
+cudaError_t launch_bwd_k(int64_t n, const float *x1, const float *y1, const float *x2, const float *y2,
+                         const float *grad, const uint8_t *nx, const uint8_t *xflags, float *gx1, float *gy1,
+                         float *gx2, float *gy2, cudaStream_t st)
+{
+    static int dev_cached = -1, limit = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t smem = sizeof(BwdSmem<K>);
+    if (dev != dev_cached) {
+        cudaError_t e = cudaFuncSetAttribute(paired_bwd_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        int sms = 0, per = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, paired_bwd_kernel<K>, kTile, smem);
+        limit = sms * (per > 0 ? per : 1);
+        dev_cached = dev;
+    }
+    const int64_t ntiles = (n + kTile - 1) / kTile;
+    const unsigned grid = (unsigned)(ntiles < limit ? ntiles : limit);
+    auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+    const int use_bulk = al16(grad) && al16(nx) && al16(xflags);   // planes are 16 B aligned (ABI)
+    paired_bwd_kernel<K><<<grid, kTile, smem, st>>>(n, x1, y1, x2, y2, grad, nx, xflags, gx1, gy1, gx2, gy2,
+                                                     use_bulk);
+    return cudaGetLastError();
+}
+}  // namespace
+
 cudaError_t launch_paired_bwd(int K, int64_t n, const float *x1, const float *y1, const float *x2,
                               const float *y2, const float *grad, const uint8_t *nx,
                               const uint8_t *xflags, float *gx1, float *gy1, float *gx2, float *gy2,
                               cudaStream_t st)
 {
-    if (K == 4)
-        paired_bwd_kernel<4><<<grid_for(n), kPairedThreads, 0, st>>>(n, x1, y1, x2, y2, grad, nx, xflags,
-                                                                     gx1, gy1, gx2, gy2);
-    else
-        paired_bwd_kernel<8><<<grid_for(n), kPairedThreads, 0, st>>>(n, x1, y1, x2, y2, grad, nx, xflags,
-                                                                     gx1, gy1, gx2, gy2);
-    return cudaGetLastError();
+    if (K == 4) return launch_bwd_k<4>(n, x1, y1, x2, y2, grad, nx, xflags, gx1, gy1, gx2, gy2, st);
+    return launch_bwd_k<8>(n, x1, y1, x2, y2, grad, nx, xflags, gx1, gy1, gx2, gy2, st);
 }
 
 }  // namespace dgal

@@ -157,3 +157,21 @@ def test_empty_batch_is_noop():
     with pytest.raises(dgal.DgalError):
         bad = torch.zeros((8, 5), dtype=torch.float32, device=dev())
         dgal.iou_paired_fwd(bad, bad, bad, bad)
+
+
+def test_backward_unaligned_side_inputs():
+    """grad / nx / xflags not 16-byte aligned: the kernel loads tiles directly
+    instead of by bulk copy; results are bitwise those of the aligned call."""
+    b = margin_batch(3, 5000)
+    x1, y1 = to_dev(b.p1)
+    x2, y2 = to_dev(b.p2)
+    g = torch.from_numpy(b.grad).to(dev())
+    iou, nx, xf = dgal.iou_paired_fwd(x1, y1, x2, y2)
+    ref = dgal.iou_paired_bwd(x1, y1, x2, y2, g, nx, xf)
+    gb = torch.empty(g.numel() + 1, device=dev())[1:]
+    gb.copy_(g)
+    nb = torch.empty(nx.numel() + 3, dtype=torch.uint8, device=dev())[3:]
+    nb.copy_(nx)
+    got = dgal.iou_paired_bwd(x1, y1, x2, y2, gb, nb, xf)
+    for a, c in zip(ref, got):
+        assert torch.equal(a, c)
