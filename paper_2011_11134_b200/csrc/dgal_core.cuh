@@ -375,7 +375,8 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
 // backward: iou_grad through the recorded nx / xflags
 // ---------------------------------------------------------------------------
 // Flag-byte -> provenance bits, staged in shared memory by the kernel:
-//   v[b]: FromP1(i) -> bit i, FromP2(j) -> bit 8 + j
+//   FromP1(i) -> bit i, FromP2(j) -> bit 8 + j,
+//   Cross(i,j) -> bit 16 + i (p1 edge i has a crossing) | bit 24 + j (p2 edge j has one)
 // (every other byte, including the 0x00 padding, maps to 0).
 struct FlagLut {
     uint32_t v[256];
@@ -385,33 +386,65 @@ __device__ __forceinline__ void fill_flag_lut(FlagLut &L, int tid, int nthreads)
 {
     for (int b = tid; b < 256; b += nthreads) {
         const int tag = b >> 6, i = (b >> 3) & 7, j = b & 7;
-        (void)i;
-        L.v[b] = (tag == 1) ? (1u << j) : (tag == 2) ? (1u << (8 + j)) : 0u;
+        L.v[b] = (tag == 1) ? (1u << j) : (tag == 2) ? (1u << (8 + j))
+               : (tag == 3) ? ((1u << (16 + i)) | (1u << (24 + j))) : 0u;
     }
 }
 
-// Backward of one pair whose raw inputs sit in shared memory (this thread's K
-// vertices at sPx[0..K-1] etc.), writing dL/dv of p1 and p2 (the same in the
-// recentred and the original frame: IoU is translation invariant, R11).
-//
-// The crossing loop visits only the Cross bytes actually recorded in xflags
-// (2.7 per pair on cfg3 instead of K^2 candidate pairs), reading the four
-// vertices it needs by dynamic index from shared memory and writing the two
-// interval end points it defines into `scr`, a per-thread scratch transposed as
-// [slot][kTile] so that dynamic slots never conflict on banks:
-//   slot i = t0 of p1 edge i, K + i = t1, 2K + j = s0 of p2 edge j, 3K + j = s1.
-// Coordinates are used raw there: vertex differences of one scene are exact
-// (Sterbenz) and the crossing parameters only need differences.
+// Backward, split in three phases so a warp can share the crossing work:
+//   bwd_prologue   (per pair)     default interval end points into the scratch;
+//   bwd_crossing   (per Cross)    one recorded Cross(i, j): its two end points;
+//   bwd_epilogue   (per pair)     pieces -> A_i -> dL/dv of p1 and p2.
+// The scratch is per pair, transposed as [slot][TILE] so dynamic slots never
+// conflict on banks: slot i = t0 of p1 edge i, K + i = t1, 2K + j = s0 of p2
+// edge j, 3K + j = s1.  Inputs are read raw from shared memory (vertex
+// differences of one scene are exact by Sterbenz; the crossing parameters only
+// need differences); the epilogue recentres on p1.v0 for the shoelace terms.
 template <int K, int TILE>
-__device__ __forceinline__ void iou_bwd_smem(const float *sPx, const float *sPy, const float *sQx,
-                                             const float *sQy, float g, int nx, const Seq<K> &seq,
-                                             const FlagLut &L, float *scr, Poly<K> &G1, Poly<K> &G2)
+__device__ __forceinline__ void bwd_prologue(float *scr)
+{
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        scr[k * TILE] = 0.f;
+        scr[(K + k) * TILE] = 1.f;
+        scr[(2 * K + k) * TILE] = 0.f;
+        scr[(3 * K + k) * TILE] = 1.f;
+    }
+}
+
+// Cross(i, j) is X = v_i + t g_i = w_j + s f_j.  If p1 edge i enters p2 there
+// (g_i x f_j < 0) the boundary piece on p1 edge i starts at t and the piece on
+// p2 edge j ends at s; otherwise the other way round.
+template <int K, int TILE>
+__device__ __forceinline__ void bwd_crossing(const float *sPx, const float *sPy, const float *sQx,
+                                             const float *sQy, uint32_t b, float *scr)
+{
+    const int i = (b >> 3) & (K - 1), j = b & (K - 1);
+    const int i1 = (i + 1) & (K - 1), j1 = (j + 1) & (K - 1);
+    const float vx = sPx[i], vy = sPy[i];
+    const float ex = sPx[i1] - vx, ey = sPy[i1] - vy;
+    const float wx = sQx[j], wy = sQy[j];
+    const float hx = sQx[j1] - wx, hy = sQy[j1] - wy;
+    const float Dx = wx - vx, Dy = wy - vy;
+    const float den = ex * hy - ey * hx;                       // g_i x f_j
+    const float r = rcp_approx(den);
+    const float t = __saturatef((Dx * hy - Dy * hx) * r);      // along p1 edge i
+    const float s = __saturatef((Dx * ey - Dy * ex) * r);      // along p2 edge j
+    const bool enter = den < 0.f;
+    scr[(enter ? i : K + i) * TILE] = t;
+    scr[(enter ? 3 * K + j : 2 * K + j) * TILE] = s;
+}
+
+// V = OR of the flag table over the recorded bytes (vertex / crossing provenance).
+template <int K, int TILE>
+__device__ __forceinline__ void bwd_epilogue(const float *sPx, const float *sPy, const float *sQx,
+                                             const float *sQy, float g, uint32_t V, const float *scr,
+                                             Poly<K> &G1, Poly<K> &G2)
 {
 #pragma unroll
     for (int k = 0; k < K; ++k) { G1.x[k] = 0.f; G1.y[k] = 0.f; G2.x[k] = 0.f; G2.y[k] = 0.f; }
-    if (nx == 0) return;
+    if (V == 0) return;  // nx == 0: zero subgradient
 
-    // recentred register copies (origin p1.v0) for the edge normals and shoelace terms
     Poly<K> P, Q;
     {
         const float ox = sPx[0], oy = sPy[0];
@@ -434,60 +467,16 @@ __device__ __forceinline__ void iou_bwd_smem(const float *sPx, const float *sPy,
         A2x2 += C2[i];
     }
 
-    // provenance of the recorded vertices (the 0x00 padding maps to nothing)
-    uint32_t V = 0;
-#pragma unroll
-    for (int p = 0; p < 2 * K; ++p) V |= L.v[seq_byte<K>(seq, p)];
-
-    // default interval end points: pieces run vertex to vertex
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        scr[k * TILE] = 0.f;
-        scr[(K + k) * TILE] = 1.f;
-        scr[(2 * K + k) * TILE] = 0.f;
-        scr[(3 * K + k) * TILE] = 1.f;
-    }
-
-    // Each recorded Cross(i, j) is X = v_i + t g_i = w_j + s f_j.  If p1 edge i
-    // enters p2 there (g_i x f_j < 0) the boundary piece on p1 edge i starts at t
-    // and the piece on p2 edge j ends at s; otherwise the other way round.
-    uint32_t hc1 = 0, hc2 = 0;
-#pragma unroll
-    for (int w = 0; w < Seq<K>::NW; ++w) {
-        const uint64_t word = seq.w[w];
-        uint64_t c3 = word & (word << 1) & 0x8080808080808080ull;
-        while (c3) {
-            const int pos = __ffsll((long long)c3) - 1;  // bit 7 of the byte
-            c3 &= c3 - 1;
-            const uint32_t b = (uint32_t)(word >> (pos - 7));
-            const int i = (b >> 3) & (K - 1), j = b & (K - 1);
-            const int i1 = (i + 1) & (K - 1), j1 = (j + 1) & (K - 1);
-            const float vx = sPx[i], vy = sPy[i];
-            const float ex = sPx[i1] - vx, ey = sPy[i1] - vy;
-            const float wx = sQx[j], wy = sQy[j];
-            const float hx = sQx[j1] - wx, hy = sQy[j1] - wy;
-            const float Dx = wx - vx, Dy = wy - vy;
-            const float den = ex * hy - ey * hx;              // g_i x f_j
-            const float r = rcp_approx(den);
-            const float t = __saturatef((Dx * hy - Dy * hx) * r);   // along p1 edge i
-            const float s = __saturatef((Dx * ey - Dy * ex) * r);   // along p2 edge j
-            const bool enter = den < 0.f;
-            scr[(enter ? i : K + i) * TILE] = t;
-            scr[(enter ? 3 * K + j : 2 * K + j) * TILE] = s;
-            hc1 |= 1u << i;
-            hc2 |= 1u << j;
-        }
-    }
-
     // boundary pieces -> A_i and the edge weights
     //   alpha = ∫ (1-t) dt = l (1 - h),  beta = ∫ t dt = l h,  l = t1 - t0, h = (t0 + t1)/2
+    // p1 edge i is on the boundary iff v_i or v_i+1 is a vertex of p1 ∩ p2 or it is crossed
     float al1[K], be1[K], al2[K], be2[K];
     float Aix2 = 0.f;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         const int i1 = (i + 1) % K;
-        const bool on1 = (((V >> i) | (V >> i1) | (hc1 >> i)) & 1u) != 0;
-        const bool on2 = (((V >> (8 + i)) | (V >> (8 + i1)) | (hc2 >> i)) & 1u) != 0;
+        const bool on1 = (((V >> i) | (V >> i1) | (V >> (16 + i))) & 1u) != 0;
+        const bool on2 = (((V >> (8 + i)) | (V >> (8 + i1)) | (V >> (24 + i))) & 1u) != 0;
         const float a0 = scr[i * TILE], a1 = scr[(K + i) * TILE];
         const float b0 = scr[(2 * K + i) * TILE], b1 = scr[(3 * K + i) * TILE];
         const float l1 = on1 ? fmaxf(a1 - a0, 0.f) : 0.f;

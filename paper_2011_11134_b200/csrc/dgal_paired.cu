@@ -63,7 +63,8 @@ struct BwdSmem {
         uint8_t nx[kTile];
     };
     Stage st[2];
-    float scr[4 * K * kTile];  // crossing end points, [slot][thread]
+    float scr[4 * K * kTile];                       // interval end points, [slot][pair]
+    uint16_t queue[kTile / 32][32 * 2 * K];         // per-warp crossing queue: lane << 8 | byte
     FlagLut lut;
     uint64_t bar[2];
 };
@@ -127,13 +128,52 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
             for (int q = 0; q < K / 4; ++q)
                 T.xf[tid * (K / 4) + q] = reinterpret_cast<const uint64_t *>(xflags)[k * (K / 4) + q];
         }
-        if (k < n) {
-            Seq<K> sq;
+        // ---- per pair: provenance bits, crossing bytes -> the warp's queue ----
+        const int warp = tid >> 5, lane = tid & 31;
+        const bool live = k < n;
+        Seq<K> sq;
 #pragma unroll
-            for (int q = 0; q < K / 4; ++q) sq.w[q] = T.xf[tid * (K / 4) + q];
+        for (int q = 0; q < K / 4; ++q) sq.w[q] = live ? T.xf[tid * (K / 4) + q] : 0ull;
+        const int m = live ? T.nx[tid] : 0;
+        uint32_t V = 0;
+        int cnt = 0;
+#pragma unroll
+        for (int p = 0; p < 2 * K; ++p) {
+            const uint32_t b = (p < m) ? seq_byte<K>(sq, p) : 0u;
+            V |= S.lut.v[b];
+            cnt += (b >= 0xC0u);
+        }
+        int incl = cnt;                                  // warp prefix sum of the counts
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+            if (lane >= d) incl += v;
+        }
+        const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        int at = incl - cnt;
+        uint16_t *queue = S.queue[warp];
+#pragma unroll
+        for (int p = 0; p < 2 * K; ++p) {
+            const uint32_t b = (p < m) ? seq_byte<K>(sq, p) : 0u;
+            if (b >= 0xC0u) queue[at++] = (uint16_t)((lane << 8) | b);
+        }
+        bwd_prologue<K, kTile>(S.scr + tid);
+        __syncwarp();
+        // ---- the warp's crossings, 32 at a time (full SIMT efficiency) ----
+        for (int base = 0; base < total; base += 32) {   // warp-uniform trip count
+            const int e = base + lane;
+            if (e < total) {
+                const uint32_t ent = queue[e];
+                const int pt = warp * 32 + (int)(ent >> 8);
+                bwd_crossing<K, kTile>(T.x1 + pt * K, T.y1 + pt * K, T.x2 + pt * K, T.y2 + pt * K,
+                                       ent & 0xFFu, S.scr + pt);
+            }
+        }
+        __syncwarp();
+        if (live) {
             Poly<K> G1, G2;
-            iou_bwd_smem<K, kTile>(T.x1 + tid * K, T.y1 + tid * K, T.x2 + tid * K, T.y2 + tid * K, T.g[tid],
-                                   T.nx[tid], sq, S.lut, S.scr + tid, G1, G2);
+            bwd_epilogue<K, kTile>(T.x1 + tid * K, T.y1 + tid * K, T.x2 + tid * K, T.y2 + tid * K, T.g[tid], V,
+                                   S.scr + tid, G1, G2);
             store_plane<K>(gx1, k, G1.x);
             store_plane<K>(gy1, k, G1.y);
             store_plane<K>(gx2, k, G2.x);
