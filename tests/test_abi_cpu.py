@@ -101,7 +101,7 @@ def test_sass_is_sm100a_register_resident():
     assert "sm_100a" in out
     stats = _sass_stats()
     names = " ".join(stats)
-    for k in ("paired_fwd_kernelILi4", "paired_fwd_kernelILi8", "paired_bwd_kernelILi4",
+    for k in ("paired_fwd_direct_kernelILi4", "paired_fwd_kernelILi8", "paired_bwd_kernelILi4",
               "paired_bwd_kernelILi8", "pairwise_kernelILi4", "nms_keep_kernel", "nms_round_kernel"):
         assert k in names, k
     for name, c in stats.items():
