@@ -14,7 +14,7 @@ constexpr int kPwThreads = 256;         // 8 warps
 constexpr int kPwWarps = kPwThreads / 32;
 constexpr int kPwTileCols = 1024;       // column tile staged in shared memory
 constexpr int kPwRowsPerCta = 64;       // row block per CTA (8 rows per warp)
-constexpr int kPwQueueCap = 32 + 128;   // per-warp candidate queue (<=31 left + 128 pushed)
+// (the per-warp candidate queue is sized in dgal_pairwise.cu)
 
 constexpr int kNmsKeepThreads = 1024;   // single-CTA keep kernel
 constexpr int kNmsRoundThreads = 256;

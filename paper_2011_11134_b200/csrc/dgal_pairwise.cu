@@ -1,19 +1,20 @@
 // dgal_pairwise.cu — N x M pairwise IoU + NMS overlap mask (north_star; S:506-513
 // "cartesian").  DESIGN.md §4.3.
 //
-// CTA = 8 warps, one 1024-column tile of p2 polygons staged in shared memory
-// (vertices + bounding circles) and reused by the CTA's 64 rows.  A warp owns one
-// row at a time and sweeps the tile 128 columns per step, 4 consecutive columns
-// per lane:
+// CTA = 8 warps, a block of 64 rows and a 1024-column tile, both staged in shared
+// memory (vertices + bounding circles).  Warp w owns 8 of the rows.  It sweeps
+// the tile 128 columns per step, 4 consecutive columns per lane; a lane loads its
+// 4 column circles once per step and tests them against the warp's 8 row circles
+// (kept in registers), so every shared-memory load feeds 8 rows:
 //   * bounding-circle reject (exact: disjoint circles => disjoint polygons),
-//   * a float4 streaming store of zeros for the 4 columns (the output write is
-//     the binding roof of the large matrix),
-//   * survivors are compacted with __ballot_sync/__popc into a per-warp shared
-//     queue and evaluated 32 at a time, one per lane, so the clip runs with full
-//     SIMT efficiency however rare candidates are;
-//   * candidate results overwrite their zero, set their mask bit in a per-warp
-//     shared bitmap (atomicOr on shared), and (c < row) append to the row's
-//     suppressor list; the bitmap goes out as whole uint64 words at row end.
+//   * one float4 streaming zero store per (row, 4 columns) — the output write is
+//     the roof of the large matrix,
+//   * the 32 (row, column) candidate bits of a lane form one mask; one vote per
+//     step; survivors are compacted (warp prefix sum) into a per-warp queue that
+//     spans all the warp's rows and is evaluated 32 at a time (full SIMT width),
+//   * candidate results overwrite their zero, set a bit in the CTA's shared
+//     64 x 1024 bitmap (written out as whole uint64 words at the end) and, for
+//     c < row, append to the row's suppressor list.
 #include "dgal_core.cuh"
 #include "dgal_internal.h"
 
@@ -22,19 +23,21 @@ namespace dgal {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr int kRowsPerWarp = kPwRowsPerCta / kPwWarps;      // 8
+constexpr int kQueue = 32 + kRowsPerWarp * 128;             // <=31 left + one step's worth
 
 template <int K>
-__device__ __forceinline__ float4 bounding_circle(const Poly<K> &p)
+__device__ __forceinline__ float4 bounding_circle(const float *x, const float *y)
 {
     float cx = 0.f, cy = 0.f;
 #pragma unroll
-    for (int k = 0; k < K; ++k) { cx += p.x[k]; cy += p.y[k]; }
+    for (int k = 0; k < K; ++k) { cx += x[k]; cy += y[k]; }
     cx *= (1.f / K);
     cy *= (1.f / K);
     float r2 = 0.f;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        const float dx = p.x[k] - cx, dy = p.y[k] - cy;
+        const float dx = x[k] - cx, dy = y[k] - cy;
         r2 = fmaxf(r2, dx * dx + dy * dy);
     }
     // inflate: relative (sqrt/rounding) + absolute (ulp of the scene coordinates)
@@ -43,145 +46,149 @@ __device__ __forceinline__ float4 bounding_circle(const Poly<K> &p)
 }
 
 template <int K>
-__device__ __forceinline__ void load_poly_cached(const float *__restrict__ X, const float *__restrict__ Y,
-                                                 int64_t n, Poly<K> &p)
-{
-    const float4 *x4 = reinterpret_cast<const float4 *>(X + n * K);
-    const float4 *y4 = reinterpret_cast<const float4 *>(Y + n * K);
-#pragma unroll
-    for (int q = 0; q < K / 4; ++q) {
-        float4 a = __ldg(x4 + q), b = __ldg(y4 + q);
-        p.x[4 * q + 0] = a.x; p.x[4 * q + 1] = a.y; p.x[4 * q + 2] = a.z; p.x[4 * q + 3] = a.w;
-        p.y[4 * q + 0] = b.x; p.y[4 * q + 1] = b.y; p.y[4 * q + 2] = b.z; p.y[4 * q + 3] = b.w;
-    }
-}
-
-template <int K>
 struct PwSmem {
-    float x[kPwTileCols * K];
-    float y[kPwTileCols * K];
-    float4 circ[kPwTileCols];
-    int queue[kPwWarps][kPwQueueCap];
-    uint32_t bits[kPwWarps][kPwTileCols / 32];
+    float cx[kPwTileCols * K], cy[kPwTileCols * K];     // column tile, [col][k]
+    float4 ccirc[kPwTileCols];
+    float rx[kPwRowsPerCta * K], ry[kPwRowsPerCta * K];  // row block, [row][k]
+    uint32_t bits[kPwRowsPerCta][kPwTileCols / 32];
+    uint32_t queue[kPwWarps][kQueue];                    // row_local << 16 | col_local
 };
 
 }  // namespace
 
 template <int K>
 __global__ void __launch_bounds__(kPwThreads)
-pairwise_kernel(int64_t n_rows, const float *__restrict__ rx, const float *__restrict__ ry, int64_t m,
-                const float *__restrict__ cx, const float *__restrict__ cy, int64_t row_offset,
+pairwise_kernel(int64_t n_rows, const float *__restrict__ rxg, const float *__restrict__ ryg, int64_t m,
+                const float *__restrict__ cxg, const float *__restrict__ cyg, int64_t row_offset,
                 float *__restrict__ iou, float thr, uint64_t *__restrict__ mask, int64_t mask_words,
                 int32_t *__restrict__ nbr_count, int32_t *__restrict__ nbr_idx, int32_t cap)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PwSmem<K> &S = *reinterpret_cast<PwSmem<K> *>(smem_raw);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t c0 = (int64_t)blockIdx.y * kPwTileCols;
+    const int64_t r0 = (int64_t)blockIdx.x * kPwRowsPerCta;
     const int ncols = (int)min((int64_t)kPwTileCols, m - c0);
+    const int nrows = (int)min((int64_t)kPwRowsPerCta, n_rows - r0);
+    const float inf = __int_as_float(0x7f800000);
 
-    // ---- stage the column tile: vertices + bounding circles ----
-    for (int t = threadIdx.x; t < kPwTileCols; t += kPwThreads) {
-        if (t < ncols) {
-            Poly<K> q;
-            load_poly_cached<K>(cx, cy, c0 + t, q);
-#pragma unroll
-            for (int k = 0; k < K; ++k) { S.x[t * K + k] = q.x[k]; S.y[t * K + k] = q.y[k]; }
-            S.circ[t] = bounding_circle<K>(q);
-        } else {
-            S.circ[t] = make_float4(__int_as_float(0x7f800000), __int_as_float(0x7f800000), 0.f, 0.f);
-        }
+    // ---- stage the column tile and the row block ----
+    for (int t = tid; t < kPwTileCols * K; t += kPwThreads) {
+        const bool ok = t < ncols * K;
+        S.cx[t] = ok ? __ldg(cxg + c0 * K + t) : 0.f;
+        S.cy[t] = ok ? __ldg(cyg + c0 * K + t) : 0.f;
     }
-    for (int t = lane; t < kPwTileCols / 32; t += 32) S.bits[warp][t] = 0u;
+    for (int t = tid; t < kPwRowsPerCta * K; t += kPwThreads) {
+        const bool ok = t < nrows * K;
+        S.rx[t] = ok ? __ldg(rxg + r0 * K + t) : 0.f;
+        S.ry[t] = ok ? __ldg(ryg + r0 * K + t) : 0.f;
+    }
+    for (int t = tid; t < kPwRowsPerCta * kPwTileCols / 32; t += kPwThreads) (&S.bits[0][0])[t] = 0u;
+    __syncthreads();
+    for (int t = tid; t < kPwTileCols; t += kPwThreads)
+        S.ccirc[t] = (t < ncols) ? bounding_circle<K>(S.cx + t * K, S.cy + t * K)
+                                 : make_float4(inf, inf, 0.f, 0.f);
     __syncthreads();
 
-    const bool vec_store = iou != nullptr && (m % 4 == 0) &&
-                           ((reinterpret_cast<uintptr_t>(iou) & 15u) == 0);
-    const unsigned lt_mask = (1u << lane) - 1u;
-    int *queue = S.queue[warp];
-    uint32_t *bits = S.bits[warp];
-
-    const int64_t r_end = min(n_rows, (int64_t)(blockIdx.x + 1) * kPwRowsPerCta);
-    for (int64_t r = (int64_t)blockIdx.x * kPwRowsPerCta + warp; r < r_end; r += kPwWarps) {
-        Poly<K> P;
-        load_poly_cached<K>(rx, ry, r, P);  // warp-uniform row: broadcast loads
-        const float4 rc = bounding_circle<K>(P);
-        const float ox = P.x[0], oy = P.y[0];
-        Poly<K> Pc;
+    // ---- this warp's rows: circles in registers ----
+    float4 rc[kRowsPerWarp];
 #pragma unroll
-        for (int k = 0; k < K; ++k) { Pc.x[k] = __fsub_rn(P.x[k], ox); Pc.y[k] = __fsub_rn(P.y[k], oy); }
+    for (int q = 0; q < kRowsPerWarp; ++q) {
+        const int rl = warp * kRowsPerWarp + q;
+        rc[q] = (rl < nrows) ? bounding_circle<K>(S.rx + rl * K, S.ry + rl * K)
+                             : make_float4(-inf, -inf, 0.f, 0.f);
+    }
+    const bool vec_store = iou != nullptr && (m % 4 == 0) && ((reinterpret_cast<uintptr_t>(iou) & 15u) == 0);
+    uint32_t *queue = S.queue[warp];
+
+    auto evaluate = [&](uint32_t ent) {
+        const int rl = (int)(ent >> 16), cl = (int)(ent & 0xFFFFu);
+        const float *px = S.rx + rl * K, *py = S.ry + rl * K;
+        const float *qx = S.cx + cl * K, *qy = S.cy + cl * K;
+        const float ox = px[0], oy = py[0];
+        Poly<K> Pc, Qc;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            Pc.x[k] = __fsub_rn(px[k], ox); Pc.y[k] = __fsub_rn(py[k], oy);
+            Qc.x[k] = __fsub_rn(qx[k], ox); Qc.y[k] = __fsub_rn(qy[k], oy);
+        }
+        const float v = iou_fwd<K, false>(Pc, Qc).iou;
+        const int64_t r = r0 + rl, c = c0 + cl;
+        if (iou) iou[r * m + c] = v;
         const int64_t grow = row_offset + r;
-        float *iou_row = iou ? iou + r * m + c0 : nullptr;
-
-        auto evaluate = [&](int e) {
-            Poly<K> Qc;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                Qc.x[k] = __fsub_rn(S.x[e * K + k], ox);
-                Qc.y[k] = __fsub_rn(S.y[e * K + k], oy);
+        if (v > thr && c != grow) {
+            if (mask) atomicOr(&S.bits[rl][cl >> 5], 1u << (cl & 31));
+            if (nbr_count && c < grow) {
+                const int slot = atomicAdd(nbr_count + r, 1);
+                if (slot < cap) nbr_idx[r * cap + slot] = (int32_t)c;
             }
-            const float v = iou_fwd<K, false>(Pc, Qc).iou;
-            if (iou_row) iou_row[e] = v;
-            const int64_t c = c0 + e;
-            if (v > thr && c != grow) {
-                if (mask) atomicOr(&bits[e >> 5], 1u << (e & 31));
-                if (nbr_count && c < grow) {
-                    const int slot = atomicAdd(nbr_count + r, 1);
-                    if (slot < cap) nbr_idx[r * cap + slot] = (int32_t)c;
-                }
-            }
-        };
+        }
+    };
 
-        int qn = 0;
+    int qn = 0;
 #pragma unroll 1
-        for (int s = 0; s < kPwTileCols / 128; ++s) {
-            const int cb = s * 128 + lane * 4;
-            bool cand[4];
+    for (int s = 0; s < kPwTileCols / 128; ++s) {
+        const int cb = s * 128 + lane * 4;
+        float4 cc[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const float4 cc = S.circ[cb + q];
-                const float dx = cc.x - rc.x, dy = cc.y - rc.y, rs = cc.z + rc.z;
-                cand[q] = dx * dx + dy * dy < rs * rs;
+        for (int u = 0; u < 4; ++u) cc[u] = S.ccirc[cb + u];
+        uint32_t cand = 0;  // bit 4q + u: row q, column cb + u
+#pragma unroll
+        for (int q = 0; q < kRowsPerWarp; ++q) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float dx = cc[u].x - rc[q].x, dy = cc[u].y - rc[q].y, rs = cc[u].z + rc[q].z;
+                cand |= (uint32_t)(dx * dx + dy * dy < rs * rs) << (4 * q + u);
             }
-            if (iou_row) {
+            const int rl = warp * kRowsPerWarp + q;
+            if (iou && rl < nrows) {
+                float *dst = iou + (r0 + rl) * m + c0 + cb;
                 if (vec_store && cb + 3 < ncols) {
-                    __stcs(reinterpret_cast<float4 *>(iou_row + cb), make_float4(0.f, 0.f, 0.f, 0.f));
+                    __stcs(reinterpret_cast<float4 *>(dst), make_float4(0.f, 0.f, 0.f, 0.f));
                 } else {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (cb + q < ncols) __stcs(iou_row + cb + q, 0.f);
-                }
-            }
-            if (__any_sync(kFull, cand[0] | cand[1] | cand[2] | cand[3])) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const unsigned bal = __ballot_sync(kFull, cand[q]);
-                    if (cand[q]) queue[qn + __popc(bal & lt_mask)] = cb + q;
-                    qn += __popc(bal);
-                }
-                __syncwarp();
-                while (qn >= 32) {           // warp-uniform
-                    evaluate(queue[qn - 32 + lane]);
-                    qn -= 32;
-                    __syncwarp();
+                    for (int u = 0; u < 4; ++u)
+                        if (cb + u < ncols) __stcs(dst + u, 0.f);
                 }
             }
         }
-        __syncwarp();
-        if (lane < qn) evaluate(queue[lane]);
-        __syncwarp();
-        if (mask) {
-            const int nw = (ncols + 63) >> 6;
-            const int64_t w0 = c0 >> 6;
-            for (int w = lane; w < nw; w += 32) {
-                if (w0 + w < mask_words) {
-                    const uint64_t word = (uint64_t)bits[2 * w] | ((uint64_t)bits[2 * w + 1] << 32);
-                    mask[r * mask_words + w0 + w] = word;
-                }
-                bits[2 * w] = 0u;
-                bits[2 * w + 1] = 0u;
+        if (__any_sync(kFull, cand != 0)) {
+            // compact this step's candidates into the warp queue (warp prefix sum)
+            const int cnt = __popc(cand);
+            int incl = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int v = __shfl_up_sync(kFull, incl, d);
+                if (lane >= d) incl += v;
             }
+            int at = qn + incl - cnt;
+            while (cand) {
+                const int bit = __ffs(cand) - 1;
+                cand &= cand - 1;
+                queue[at++] = ((uint32_t)(warp * kRowsPerWarp + (bit >> 2)) << 16) | (uint32_t)(cb + (bit & 3));
+            }
+            qn += __shfl_sync(kFull, incl, 31);
             __syncwarp();
+            while (qn >= 32) {  // warp-uniform
+                evaluate(queue[qn - 32 + lane]);
+                qn -= 32;
+                __syncwarp();
+            }
+        }
+    }
+    __syncwarp();
+    if (lane < qn) evaluate(queue[lane]);
+    __syncthreads();
+
+    // ---- mask rows of the block: whole uint64 words ----
+    if (mask) {
+        const int nw = (ncols + 63) >> 6;
+        const int64_t w0 = c0 >> 6;
+        for (int t = tid; t < nrows * nw; t += kPwThreads) {
+            const int rl = t / nw, w = t - rl * nw;
+            if (w0 + w < mask_words)
+                mask[(r0 + rl) * mask_words + w0 + w] =
+                    (uint64_t)S.bits[rl][2 * w] | ((uint64_t)S.bits[rl][2 * w + 1] << 32);
         }
     }
 }
@@ -199,19 +206,23 @@ cudaError_t launch_pairwise(int K, int64_t n_rows, const float *rx, const float 
                     (unsigned)((m + kPwTileCols - 1) / kPwTileCols));
     if (K == 4) {
         const size_t sm = sizeof(PwSmem<4>);
-        static bool attr4 = false;
-        if (!attr4) {
+        static int attr = -1;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (attr != dev) {
             cudaFuncSetAttribute(pairwise_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            attr4 = true;
+            attr = dev;
         }
         pairwise_kernel<4><<<grid, kPwThreads, sm, st>>>(n_rows, rx, ry, m, cx, cy, row_offset, iou, thr,
                                                          mask, mask_words, nbr_count, nbr_idx, cap);
     } else {
         const size_t sm = sizeof(PwSmem<8>);
-        static bool attr8 = false;
-        if (!attr8) {
+        static int attr = -1;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (attr != dev) {
             cudaFuncSetAttribute(pairwise_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            attr8 = true;
+            attr = dev;
         }
         pairwise_kernel<8><<<grid, kPwThreads, sm, st>>>(n_rows, rx, ry, m, cx, cy, row_offset, iou, thr,
                                                          mask, mask_words, nbr_count, nbr_idx, cap);
