@@ -36,6 +36,7 @@
 #ifndef DGAL_H_
 #define DGAL_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -96,13 +97,24 @@ dgal_status dgal_iou_paired_bwd(int K, int64_t n,
  *         bit c of row r  <=>  c != row_offset + r  and  IoU(r, c) > nms_thresh
  *         (strict, R14).  Bits c > row_offset + r form the classic NMS
  *         suppression row; bits c < row_offset + r are the boxes that can
- *         suppress box row_offset + r.
+ *         suppress box row_offset + r.  Words beyond ceil(m/64) are untouched
+ *         by the tiled path and zeroed by the indexed path.
  *   nbr_count [n_rows], nbr_idx [n_rows * nbr_cap] int32, nullable (both or
  *         neither; requires mask):  the list of columns c < row_offset + r with
  *         IoU > nms_thresh, in no particular order; nbr_count[r] is the true
  *         count (it may exceed nbr_cap, then only nbr_cap entries are stored).
  *         The library zeroes nbr_count itself (cudaMemsetAsync on `stream`).
+ *   workspace, workspace_bytes: nullable.  With a device workspace of at least
+ *         dgal_pairwise_workspace_bytes(m) bytes the INDEXED path runs: the
+ *         outputs are zero-filled at streaming-write speed and only pairs whose
+ *         bounding circles intersect are evaluated, found through a uniform grid
+ *         over the column circles built in the workspace (best for large sparse
+ *         problems, e.g. 1e5 x 1e5).  Without one the TILED path sweeps every
+ *         pair through shared-memory column tiles.  Both give the same outputs
+ *         (mask/list bit-identical; IoU identical pair by pair).
  */
+size_t dgal_pairwise_workspace_bytes(int64_t m);
+
 dgal_status dgal_iou_pairwise(int K, int64_t n_rows,
                               const float *row_x, const float *row_y,
                               int64_t m,
@@ -112,6 +124,7 @@ dgal_status dgal_iou_pairwise(int K, int64_t n_rows,
                               float nms_thresh,
                               uint64_t *mask, int64_t mask_words,
                               int32_t *nbr_count, int32_t *nbr_idx, int32_t nbr_cap,
+                              void *workspace, size_t workspace_bytes,
                               dgal_stream stream);
 
 /*

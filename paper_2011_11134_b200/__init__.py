@@ -19,7 +19,7 @@ import torch
 
 from ._lib import DgalError, call, lib  # noqa: F401
 
-__all__ = ["iou_paired_fwd", "iou_paired_bwd", "iou_pairwise", "nms_round", "nms_keep",
+__all__ = ["iou_paired_fwd", "iou_paired_bwd", "iou_pairwise", "pairwise_workspace", "nms_round", "nms_keep",
            "nms", "PolyIoU", "DgalError", "build_info"]
 
 
@@ -87,11 +87,20 @@ def iou_paired_bwd(x1, y1, x2, y2, grad_iou, nx, xflags, K: int | None = None, o
     return gx1, gy1, gx2, gy2
 
 
+def pairwise_workspace(m: int, device=None) -> torch.Tensor:
+    """Device workspace for the indexed pairwise path (dgal_pairwise_workspace_bytes)."""
+    nb = int(lib().dgal_pairwise_workspace_bytes(int(m)))
+    return torch.empty(nb, dtype=torch.uint8, device=device or "cuda")
+
+
 def iou_pairwise(rx, ry, cx, cy, K: int | None = None, row_offset: int = 0, thr: float = 0.7,
-                 want_iou: bool = True, want_mask: bool = True, nbr_cap: int = 0, out=None):
+                 want_iou: bool = True, want_mask: bool = True, nbr_cap: int = 0, out=None,
+                 indexed: bool = True, workspace: torch.Tensor | None = None):
     """Pairwise IoU of rows x columns (dgal_iou_pairwise).  Returns
     (iou f32[nr, m] | None, mask u64[nr, ceil(m/64)] | None, nbr_count i32[nr] | None,
-     nbr_idx i32[nr, nbr_cap] | None).  mask/nbr semantics: include/dgal.h."""
+     nbr_idx i32[nr, nbr_cap] | None).  mask/nbr semantics: include/dgal.h.
+    indexed=True uses the grid-indexed path (a workspace is allocated unless given),
+    indexed=False the tiled sweep."""
     for t, nm in ((rx, "rx"), (ry, "ry"), (cx, "cx"), (cy, "cy")):
         _plane(t, nm)
     K, nr = _K_n(rx, K)
@@ -105,9 +114,13 @@ def iou_pairwise(rx, ry, cx, cy, K: int | None = None, row_offset: int = 0, thr:
         mask = torch.empty((nr, words), dtype=torch.int64, device=dev) if want_mask else None
         cnt = torch.empty(nr, dtype=torch.int32, device=dev) if nbr_cap > 0 else None
         idx = torch.empty((nr, nbr_cap), dtype=torch.int32, device=dev) if nbr_cap > 0 else None
+    if indexed and workspace is None:
+        workspace = pairwise_workspace(m, dev)
+    ws = workspace if indexed else None
     call("dgal_iou_pairwise", K, nr, _ptr(rx), _ptr(ry), m, _ptr(cx), _ptr(cy), int(row_offset), _ptr(iou),
          float(thr), _ptr(mask), words if mask is not None else 0, _ptr(cnt), _ptr(idx),
-         int(nbr_cap if cnt is not None else 0), _stream(dev))
+         int(idx.shape[1] if idx is not None else 0), _ptr(ws), int(ws.numel()) if ws is not None else 0,
+         _stream(dev))
     return iou, mask, cnt, idx
 
 

@@ -1,6 +1,7 @@
 // dgal_api.cu — the extern "C" boundary of libdgal.so (include/dgal.h): host-side
 // argument validation, K dispatch, launch on the caller's stream.  No
 // allocation, no global state, no host synchronisation.
+#include <climits>
 #include <cstdint>
 
 #include "../../include/dgal.h"
@@ -57,7 +58,8 @@ dgal_status dgal_iou_paired_bwd(int K, int64_t n, const float *x1, const float *
 dgal_status dgal_iou_pairwise(int K, int64_t n_rows, const float *row_x, const float *row_y, int64_t m,
                               const float *col_x, const float *col_y, int64_t row_offset, float *iou,
                               float nms_thresh, uint64_t *mask, int64_t mask_words, int32_t *nbr_count,
-                              int32_t *nbr_idx, int32_t nbr_cap, dgal_stream stream)
+                              int32_t *nbr_idx, int32_t nbr_cap, void *workspace, size_t workspace_bytes,
+                              dgal_stream stream)
 {
     if (K != 4 && K != 8) return DGAL_ERR_UNSUPPORTED_K;
     if (n_rows < 0 || m < 0 || row_offset < 0) return DGAL_ERR_INVALID_ARG;
@@ -75,9 +77,22 @@ dgal_status dgal_iou_pairwise(int K, int64_t n_rows, const float *row_x, const f
     if (!aligned(row_x, 16) || !aligned(row_y, 16) || !aligned(col_x, 16) || !aligned(col_y, 16) ||
         (iou && !aligned(iou, 4)))
         return DGAL_ERR_MISALIGNED;
+    if (workspace && workspace_bytes >= dgal::pairwise_workspace_bytes(m)) {
+        if (!aligned(workspace, 256)) return DGAL_ERR_MISALIGNED;
+        if (m > (int64_t)INT32_MAX) return DGAL_ERR_INVALID_ARG;
+        return from_cuda(dgal::launch_pairwise_indexed(K, n_rows, row_x, row_y, m, col_x, col_y, row_offset, iou,
+                                                       nms_thresh, mask, mask_words, nbr_count, nbr_idx,
+                                                       nbr_cap, workspace, as_cuda(stream)));
+    }
+    if (workspace) return DGAL_ERR_INVALID_ARG;  // too small
     return from_cuda(dgal::launch_pairwise(K, n_rows, row_x, row_y, m, col_x, col_y, row_offset, iou,
                                            nms_thresh, mask, mask_words, nbr_count, nbr_idx, nbr_cap,
                                            as_cuda(stream)));
+}
+
+size_t dgal_pairwise_workspace_bytes(int64_t m)
+{
+    return dgal::pairwise_workspace_bytes(m < 0 ? 0 : m);
 }
 
 dgal_status dgal_nms_round(int64_t n_total, int64_t n_rows, int64_t row_offset, const uint64_t *mask,

@@ -30,6 +30,11 @@ cudaError_t launch_pairwise(int K, int64_t n_rows, const float *rx, const float 
                             const float *cx, const float *cy, int64_t row_offset, float *iou,
                             float thr, uint64_t *mask, int64_t mask_words, int32_t *nbr_count,
                             int32_t *nbr_idx, int32_t cap, cudaStream_t st);
+size_t pairwise_workspace_bytes(int64_t m);
+cudaError_t launch_pairwise_indexed(int K, int64_t n_rows, const float *rx, const float *ry, int64_t m,
+                                    const float *cx, const float *cy, int64_t row_offset, float *iou,
+                                    float thr, uint64_t *mask, int64_t mask_words, int32_t *nbr_count,
+                                    int32_t *nbr_idx, int32_t cap, void *workspace, cudaStream_t st);
 cudaError_t launch_nms_round(int64_t n_total, int64_t n_rows, int64_t row_offset,
                              const uint64_t *mask, int64_t mask_words, const int32_t *nbr_count,
                              const int32_t *nbr_idx, int32_t cap, uint8_t *status, int32_t *undecided,

@@ -1,0 +1,380 @@
+// dgal_pwindex.cu — indexed pairwise path: for large, sparse
+// N x M problems the matrix is (1) zero-filled by a streaming kernel at HBM write
+// speed and (2) only the pairs whose bounding circles intersect are evaluated,
+// found through a uniform grid over the column circles (counting sort built on
+// the device in a caller-provided workspace).  Exactness: disjoint bounding
+// circles => disjoint polygons => IoU 0, which the zero-fill already wrote.
+#include "dgal_core.cuh"
+#include "dgal_internal.h"
+
+namespace dgal {
+
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr int kGridMaxCells = 1 << 16;  // <= 256 x 256 cells
+constexpr int kThreads = 256;
+
+struct GridHeader {
+    float xmin, ymin, xmax, ymax;  // extent of the column circle centres
+    float rmax;                    // largest column radius
+    float cell;                    // cell size (>= 2 rmax)
+    int nx, ny;                    // grid dims
+};
+
+struct Workspace {
+    GridHeader *hdr;
+    float4 *circ;       // [m] column circles
+    int32_t *cell_of;   // [m]
+    int32_t *sorted;    // [m] column ids grouped by cell
+    int32_t *start;     // [kGridMaxCells + 1] exclusive prefix of the counts
+    int32_t *fill;      // [kGridMaxCells]
+};
+
+__host__ __device__ inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+__host__ __device__ inline Workspace carve(void *ws, int64_t m)
+{
+    char *p = static_cast<char *>(ws);
+    Workspace w;
+    w.hdr = reinterpret_cast<GridHeader *>(p);
+    p += align256(sizeof(GridHeader));
+    w.circ = reinterpret_cast<float4 *>(p);
+    p += align256(sizeof(float4) * (size_t)m);
+    w.cell_of = reinterpret_cast<int32_t *>(p);
+    p += align256(sizeof(int32_t) * (size_t)m);
+    w.sorted = reinterpret_cast<int32_t *>(p);
+    p += align256(sizeof(int32_t) * (size_t)m);
+    w.start = reinterpret_cast<int32_t *>(p);
+    p += align256(sizeof(int32_t) * (kGridMaxCells + 1));
+    w.fill = reinterpret_cast<int32_t *>(p);
+    return w;
+}
+
+__device__ __forceinline__ void atomic_min_f(float *a, float v)
+{
+    int *ai = reinterpret_cast<int *>(a);
+    int old = *ai;
+    while (v < __int_as_float(old)) {
+        const int prev = atomicCAS(ai, old, __float_as_int(v));
+        if (prev == old) break;
+        old = prev;
+    }
+}
+__device__ __forceinline__ void atomic_max_f(float *a, float v)
+{
+    int *ai = reinterpret_cast<int *>(a);
+    int old = *ai;
+    while (v > __int_as_float(old)) {
+        const int prev = atomicCAS(ai, old, __float_as_int(v));
+        if (prev == old) break;
+        old = prev;
+    }
+}
+
+template <int K>
+__device__ __forceinline__ float4 circle_of(const float *__restrict__ X, const float *__restrict__ Y, int64_t c)
+{
+    float x[K], y[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) { x[k] = __ldg(X + c * K + k); y[k] = __ldg(Y + c * K + k); }
+    float cx = 0.f, cy = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) { cx += x[k]; cy += y[k]; }
+    cx *= (1.f / K);
+    cy *= (1.f / K);
+    float r2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const float dx = x[k] - cx, dy = y[k] - cy;
+        r2 = fmaxf(r2, dx * dx + dy * dy);
+    }
+    const float r = sqrtf(r2) * 1.0001f + 2e-6f * (fabsf(cx) + fabsf(cy)) + 1e-30f;
+    return make_float4(cx, cy, r, 0.f);
+}
+
+__global__ void pw_init(Workspace w)
+{
+    GridHeader &h = *w.hdr;
+    h.xmin = h.ymin = __int_as_float(0x7f800000);
+    h.xmax = h.ymax = -__int_as_float(0x7f800000);
+    h.rmax = 0.f;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kThreads) pw_circles(int64_t m, const float *__restrict__ cx,
+                                                       const float *__restrict__ cy, Workspace w)
+{
+    __shared__ float red[5][kThreads / 32];
+    const int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    float x0 = __int_as_float(0x7f800000), y0 = x0, x1 = -x0, y1 = -x0, r = 0.f;
+    if (c < m) {
+        const float4 q = circle_of<K>(cx, cy, c);
+        w.circ[c] = q;
+        x0 = x1 = q.x;
+        y0 = y1 = q.y;
+        r = q.z;
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        x0 = fminf(x0, __shfl_xor_sync(kFull, x0, d));
+        y0 = fminf(y0, __shfl_xor_sync(kFull, y0, d));
+        x1 = fmaxf(x1, __shfl_xor_sync(kFull, x1, d));
+        y1 = fmaxf(y1, __shfl_xor_sync(kFull, y1, d));
+        r = fmaxf(r, __shfl_xor_sync(kFull, r, d));
+    }
+    const int wp = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red[0][wp] = x0; red[1][wp] = y0; red[2][wp] = x1; red[3][wp] = y1; red[4][wp] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < kThreads / 32; ++i) {
+            x0 = fminf(x0, red[0][i]); y0 = fminf(y0, red[1][i]);
+            x1 = fmaxf(x1, red[2][i]); y1 = fmaxf(y1, red[3][i]); r = fmaxf(r, red[4][i]);
+        }
+        GridHeader &h = *w.hdr;
+        atomic_min_f(&h.xmin, x0);
+        atomic_min_f(&h.ymin, y0);
+        atomic_max_f(&h.xmax, x1);
+        atomic_max_f(&h.ymax, y1);
+        atomic_max_f(&h.rmax, r);
+    }
+}
+
+// grid geometry from the header: cells of size >= 2 rmax (>= the largest
+// possible centre distance of an intersecting row/column pair when the row
+// radius is <= rmax; larger rows scan more cells), at most 256 x 256 cells.
+__device__ __forceinline__ void grid_dims(const GridHeader &h, float &cell, int &nx, int &ny)
+{
+    const float ex = fmaxf(h.xmax - h.xmin, 0.f), ey = fmaxf(h.ymax - h.ymin, 0.f);
+    cell = fmaxf(fmaxf(2.f * h.rmax, fmaxf(ex, ey) * (1.f / 255.f)), 1e-20f);
+    nx = min(256, (int)(ex / cell) + 1);
+    ny = min(256, (int)(ey / cell) + 1);
+}
+
+__device__ __forceinline__ int cell_coord(float v, float lo, float cell, int n)
+{
+    return min(n - 1, max(0, (int)floorf((v - lo) / cell)));
+}
+
+__global__ void __launch_bounds__(kThreads) pw_count(int64_t m, Workspace w)
+{
+    const int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (c >= m) return;
+    float cell;
+    int nx, ny;
+    const GridHeader h = *w.hdr;
+    grid_dims(h, cell, nx, ny);
+    const float4 q = w.circ[c];
+    const int id = cell_coord(q.y, h.ymin, cell, ny) * nx + cell_coord(q.x, h.xmin, cell, nx);
+    w.cell_of[c] = id;
+    atomicAdd(w.start + id + 1, 1);
+    if (c == 0) {
+        w.hdr->cell = cell;
+        w.hdr->nx = nx;
+        w.hdr->ny = ny;
+    }
+}
+
+// exclusive scan of the (<= 65536) cell counts, one CTA
+__global__ void __launch_bounds__(1024) pw_scan(Workspace w)
+{
+    __shared__ int32_t part[1024];
+    constexpr int kPer = kGridMaxCells / 1024;
+    const int t = threadIdx.x;
+    int32_t *v = w.start + 1 + t * kPer;
+    int32_t s = 0;
+    for (int i = 0; i < kPer; ++i) s += v[i];
+    part[t] = s;
+    __syncthreads();
+    for (int d = 1; d < 1024; d <<= 1) {
+        const int32_t add = (t >= d) ? part[t - d] : 0;
+        __syncthreads();
+        part[t] += add;
+        __syncthreads();
+    }
+    int32_t run = part[t] - s;  // exclusive prefix of this chunk
+    for (int i = 0; i < kPer; ++i) {
+        const int32_t c = v[i];
+        v[i] = run;          // start[1 + t*kPer + i] = prefix up to (not incl.) this cell
+        run += c;
+    }
+    if (t == 1023) w.start[0] = 0;
+    // start[j+1] now holds the exclusive prefix of cell j; shift by one below
+}
+
+__global__ void __launch_bounds__(kThreads) pw_scatter(int64_t m, Workspace w)
+{
+    const int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (c >= m) return;
+    const int id = w.cell_of[c];
+    const int pos = w.start[id + 1] + atomicAdd(w.fill + id, 1);
+    w.sorted[pos] = (int32_t)c;
+}
+
+// streaming zero fill of a byte range (16 B vector stores, scalar head/tail)
+__global__ void __launch_bounds__(kThreads) pw_zero(char *p, size_t bytes)
+{
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const size_t head = ((16 - (a & 15)) & 15) < bytes ? ((16 - (a & 15)) & 15) : bytes;
+    const size_t nvec = (bytes - head) / 16;
+    const size_t tid = (size_t)blockIdx.x * kThreads + threadIdx.x;
+    const size_t stride = (size_t)gridDim.x * kThreads;
+    if (tid < head) p[tid] = 0;
+    int4 *v = reinterpret_cast<int4 *>(p + head);
+    for (size_t i = tid; i < nvec; i += stride) __stcs(v + i, make_int4(0, 0, 0, 0));
+    const size_t tail = bytes - head - nvec * 16;
+    if (tid < tail) p[head + nvec * 16 + tid] = 0;
+}
+
+// Candidate pass: one row per thread; the grid neighbourhood of the row circle
+// is scanned, circle-overlapping columns are pushed to a per-warp queue and
+// evaluated 32 at a time.
+template <int K>
+__global__ void __launch_bounds__(kThreads)
+pw_candidates(int64_t n_rows, const float *__restrict__ rx, const float *__restrict__ ry, int64_t m,
+              const float *__restrict__ cxg, const float *__restrict__ cyg, int64_t row_offset,
+              float *__restrict__ iou, float thr, uint64_t *__restrict__ mask, int64_t mask_words,
+              int32_t *__restrict__ nbr_count, int32_t *__restrict__ nbr_idx, int32_t cap, Workspace w)
+{
+    constexpr int kQ = 64;
+    __shared__ uint32_t queue_r[kThreads / 32][kQ];
+    __shared__ int32_t queue_c[kThreads / 32][kQ];
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const int64_t r = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    const bool live = r < n_rows;
+    const GridHeader h = *w.hdr;
+
+    auto evaluate = [&](uint32_t rl, int32_t c) {
+        const int64_t rr = (int64_t)blockIdx.x * kThreads + rl;
+        Poly<K> P, Q;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            P.x[k] = __ldg(rx + rr * K + k); P.y[k] = __ldg(ry + rr * K + k);
+            Q.x[k] = __ldg(cxg + (int64_t)c * K + k); Q.y[k] = __ldg(cyg + (int64_t)c * K + k);
+        }
+        const float ox = P.x[0], oy = P.y[0];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            P.x[k] = __fsub_rn(P.x[k], ox); P.y[k] = __fsub_rn(P.y[k], oy);
+            Q.x[k] = __fsub_rn(Q.x[k], ox); Q.y[k] = __fsub_rn(Q.y[k], oy);
+        }
+        const float v = iou_fwd<K, false>(P, Q).iou;
+        if (iou && v != 0.f) iou[rr * m + c] = v;
+        const int64_t grow = row_offset + rr;
+        if (v > thr && c != grow) {
+            if (mask) atomicOr(reinterpret_cast<unsigned long long *>(mask + rr * mask_words + (c >> 6)),
+                               1ull << (c & 63));
+            if (nbr_count && c < grow) {
+                const int slot = atomicAdd(nbr_count + rr, 1);
+                if (slot < cap) nbr_idx[rr * cap + slot] = c;
+            }
+        }
+    };
+
+    // row circle and its cell range (rows larger than rmax scan a wider range)
+    float4 rc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int cx0 = 0, cx1 = -1, cy0 = 0, cy1 = -1;
+    if (live) {
+        rc = circle_of<K>(rx, ry, r);
+        const float reach = rc.z + h.rmax;
+        cx0 = cell_coord(rc.x - reach, h.xmin, h.cell, h.nx);
+        cx1 = cell_coord(rc.x + reach, h.xmin, h.cell, h.nx);
+        cy0 = cell_coord(rc.y - reach, h.ymin, h.cell, h.ny);
+        cy1 = cell_coord(rc.y + reach, h.ymin, h.cell, h.ny);
+    }
+    const int ncells = h.nx * h.ny;
+    auto cell_end = [&](int id) { return (id + 1 < ncells) ? w.start[2 + id] : (int)m; };
+    int qn = 0;
+    int gy = cy0, gx = cx0;
+    int pos = 0, end = 0;
+    if (live) {
+        pos = w.start[1 + cy0 * h.nx + cx0];
+        end = cell_end(cy0 * h.nx + cx0);
+    }
+    bool more = live;
+    for (;;) {
+        // each lane finds its next candidate (or runs out); then the warp pushes
+        int32_t found = -1;
+        while (more && found < 0) {
+            if (pos < end) {
+                const int32_t c = w.sorted[pos++];
+                const float4 q = w.circ[c];
+                const float dx = q.x - rc.x, dy = q.y - rc.y, rs = q.z + rc.z;
+                if (dx * dx + dy * dy < rs * rs) found = c;
+            } else {
+                if (++gx > cx1) { gx = cx0; ++gy; }
+                if (gy > cy1) { more = false; break; }
+                const int id = gy * h.nx + gx;
+                pos = w.start[1 + id];
+                end = cell_end(id);
+            }
+        }
+        const unsigned bal = __ballot_sync(kFull, found >= 0);
+        if (bal == 0) break;
+        if (found >= 0) {
+            const int at = qn + __popc(bal & ((1u << lane) - 1u));
+            queue_r[wp][at] = (uint32_t)threadIdx.x;
+            queue_c[wp][at] = found;
+        }
+        qn += __popc(bal);
+        __syncwarp();
+        if (qn >= 32) {
+            evaluate(queue_r[wp][qn - 32 + lane], queue_c[wp][qn - 32 + lane]);
+            qn -= 32;
+            __syncwarp();
+        }
+    }
+    __syncwarp();
+    if (lane < qn) evaluate(queue_r[wp][lane], queue_c[wp][lane]);
+}
+
+}  // namespace
+
+size_t pairwise_workspace_bytes(int64_t m)
+{
+    return align256(sizeof(GridHeader)) + align256(sizeof(float4) * (size_t)m) +
+           2 * align256(sizeof(int32_t) * (size_t)m) + align256(sizeof(int32_t) * (kGridMaxCells + 1)) +
+           align256(sizeof(int32_t) * kGridMaxCells);
+}
+
+cudaError_t launch_pairwise_indexed(int K, int64_t n_rows, const float *rx, const float *ry, int64_t m,
+                                    const float *cx, const float *cy, int64_t row_offset, float *iou,
+                                    float thr, uint64_t *mask, int64_t mask_words, int32_t *nbr_count,
+                                    int32_t *nbr_idx, int32_t cap, void *workspace, cudaStream_t st)
+{
+    const Workspace w = carve(workspace, m);
+    cudaError_t e;
+    // (1) zero-fill the outputs at streaming-write speed
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned zgrid = (unsigned)(sms > 0 ? sms * 8 : 1184);
+    if (iou) pw_zero<<<zgrid, kThreads, 0, st>>>(reinterpret_cast<char *>(iou), sizeof(float) * (size_t)n_rows * m);
+    if (mask)
+        pw_zero<<<zgrid, kThreads, 0, st>>>(reinterpret_cast<char *>(mask),
+                                            sizeof(uint64_t) * (size_t)n_rows * mask_words);
+    if (nbr_count && (e = cudaMemsetAsync(nbr_count, 0, sizeof(int32_t) * (size_t)n_rows, st))) return e;
+    // (2) grid index of the column circles
+    if ((e = cudaMemsetAsync(w.start, 0, sizeof(int32_t) * (kGridMaxCells + 1), st))) return e;
+    if ((e = cudaMemsetAsync(w.fill, 0, sizeof(int32_t) * kGridMaxCells, st))) return e;
+    pw_init<<<1, 1, 0, st>>>(w);
+    const unsigned mg = (unsigned)((m + kThreads - 1) / kThreads);
+    if (K == 4) pw_circles<4><<<mg, kThreads, 0, st>>>(m, cx, cy, w);
+    else pw_circles<8><<<mg, kThreads, 0, st>>>(m, cx, cy, w);
+    pw_count<<<mg, kThreads, 0, st>>>(m, w);
+    pw_scan<<<1, 1024, 0, st>>>(w);
+    pw_scatter<<<mg, kThreads, 0, st>>>(m, w);
+    // (3) candidates
+    const unsigned rg = (unsigned)((n_rows + kThreads - 1) / kThreads);
+    if (K == 4)
+        pw_candidates<4><<<rg, kThreads, 0, st>>>(n_rows, rx, ry, m, cx, cy, row_offset, iou, thr, mask,
+                                                  mask_words, nbr_count, nbr_idx, cap, w);
+    else
+        pw_candidates<8><<<rg, kThreads, 0, st>>>(n_rows, rx, ry, m, cx, cy, row_offset, iou, thr, mask,
+                                                  mask_words, nbr_count, nbr_idx, cap, w);
+    return cudaGetLastError();
+}
+
+}  // namespace dgal

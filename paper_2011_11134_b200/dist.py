@@ -80,7 +80,7 @@ def pairwise_nms_sharded(x, y, thr: float = 0.7, nbr_cap: int = 64, want_iou: bo
     lo, hi = shard_range(n, world, rank, B)
     rx, ry = x[lo:hi].contiguous(), y[lo:hi].contiguous()
     iou, mask, cnt, idx = iou_pairwise(rx, ry, x, y, row_offset=lo, thr=thr, want_iou=want_iou,
-                                       want_mask=True, nbr_cap=nbr_cap)
+                                       want_mask=True, nbr_cap=nbr_cap, indexed=True)
     status = torch.zeros(world * B, dtype=torch.uint8, device=x.device)
     undecided = torch.zeros(1, dtype=torch.int32, device=x.device)
 

@@ -25,8 +25,8 @@ def _declared():
 def test_header_declares_the_boundary():
     names = _declared()
     assert names == sorted(["dgal_iou_paired_fwd", "dgal_iou_paired_bwd", "dgal_iou_pairwise",
-                            "dgal_nms_round", "dgal_nms_keep", "dgal_status_string",
-                            "dgal_build_info"])
+                            "dgal_pairwise_workspace_bytes", "dgal_nms_round", "dgal_nms_keep",
+                            "dgal_status_string", "dgal_build_info"])
 
 
 def test_library_exports_every_declared_symbol():
@@ -68,12 +68,14 @@ def test_host_side_validation_without_gpu():
     assert L.dgal_iou_paired_bwd(4, 0, *([None] * 11), None) == 0
     # pairwise: nothing requested, negative threshold with a mask, short mask rows
     args = [4, 8, P(a), P(a), 8, P(a), P(a), 0]
-    assert L.dgal_iou_pairwise(*args, None, 0.5, None, 0, None, None, 0, None) == 1
-    assert L.dgal_iou_pairwise(*args, None, -0.1, P(a), 1, None, None, 0, None) == 1
+    assert L.dgal_iou_pairwise(*args, None, 0.5, None, 0, None, None, 0, None, 0, None) == 1
+    assert L.dgal_iou_pairwise(*args, None, -0.1, P(a), 1, None, None, 0, None, 0, None) == 1
     assert L.dgal_iou_pairwise(*[4, 8, P(a), P(a), 200, P(a), P(a), 0], None, 0.5, P(a), 1, None, None,
-                               0, None) == 1
-    # lists without a mask
-    assert L.dgal_iou_pairwise(*args, P(a), 0.5, None, 0, P(a), P(a), 4, None) == 1
+                               0, None, 0, None) == 1
+    # lists without a mask; a workspace that is too small
+    assert L.dgal_iou_pairwise(*args, P(a), 0.5, None, 0, P(a), P(a), 4, None, 0, None) == 1
+    assert L.dgal_iou_pairwise(*args, P(a), 0.5, None, 0, None, None, 0, P(a), 16, None) == 1
+    assert L.dgal_pairwise_workspace_bytes(100_000) > 100_000 * 24
     # NMS: row block outside the problem
     assert L.dgal_nms_round(10, 8, 4, P(a), 1, None, None, 0, P(a), P(a), None) == 1
     assert L.dgal_nms_keep(0, None, 0, None, None, 0, None, None, None) == 0

@@ -44,12 +44,13 @@ def _check_lists(gpu_bits, cnt, idx, row_offset=0):
             assert set(idx[r, :cnt[r]].tolist()) == want
 
 
+@pytest.mark.parametrize("indexed", [True, False])
 @pytest.mark.parametrize("thr", [0.7, 0.3])
-def test_cfg2_full(thr):
+def test_cfg2_full(thr, indexed):
     sc = synth.gen_cfg2_scene()
     p = sc.polys
     x, y = to_dev(p)
-    iou, mask, cnt, idx = dgal.iou_pairwise(x, y, x, y, thr=thr, nbr_cap=64)
+    iou, mask, cnt, idx = dgal.iou_pairwise(x, y, x, y, thr=thr, nbr_cap=64, indexed=indexed)
     keep = dgal.nms_keep(mask, cnt, idx)
     torch.cuda.synchronize()
     ref = oracle.iou_pairwise(p, p)
@@ -87,8 +88,9 @@ def test_pairwise_equals_paired_forward():
     assert d.max() <= 2e-6, d.max()
 
 
+@pytest.mark.parametrize("indexed", [True, False])
 @pytest.mark.parametrize("nr,m", [(1, 1), (37, 1500), (65, 1031), (200, 2049)])
-def test_ragged_shapes_and_row_blocks(nr, m):
+def test_ragged_shapes_and_row_blocks(nr, m, indexed):
     sc = synth.gen_cfg5_scene(n_objects=max(1, (m + 49) // 50), per_object=50, seed=m)
     cols = sc.polys.take(np.arange(m))
     off = min(3, m - 1)
@@ -96,7 +98,8 @@ def test_ragged_shapes_and_row_blocks(nr, m):
     nr = rows.n
     rx, ry = to_dev(rows)
     cx, cy = to_dev(cols)
-    iou, mask, cnt, idx = dgal.iou_pairwise(rx, ry, cx, cy, row_offset=off, thr=0.1, nbr_cap=8)
+    iou, mask, cnt, idx = dgal.iou_pairwise(rx, ry, cx, cy, row_offset=off, thr=0.1, nbr_cap=8,
+                                            indexed=indexed)
     torch.cuda.synchronize()
     ref = oracle.iou_pairwise(rows, cols)
     assert np.abs(iou.cpu().numpy() - ref).max() <= IOU_ATOL
@@ -105,12 +108,13 @@ def test_ragged_shapes_and_row_blocks(nr, m):
     _check_lists(bits, cnt.cpu().numpy(), idx.cpu().numpy(), row_offset=off)
 
 
-def test_mask_only_and_k8():
+@pytest.mark.parametrize("indexed", [True, False])
+def test_mask_only_and_k8(indexed):
     b = synth.gen_cfg4_pairs(600, seed=3)
     p = b.p1
     x, y = to_dev(p)
-    iou, mask, _, _ = dgal.iou_pairwise(x, y, x, y, thr=0.2)
-    _, mask2, _, _ = dgal.iou_pairwise(x, y, x, y, thr=0.2, want_iou=False)
+    iou, mask, _, _ = dgal.iou_pairwise(x, y, x, y, thr=0.2, indexed=indexed)
+    _, mask2, _, _ = dgal.iou_pairwise(x, y, x, y, thr=0.2, want_iou=False, indexed=indexed)
     torch.cuda.synchronize()
     ref = oracle.iou_pairwise(p, p)
     assert np.abs(iou.cpu().numpy() - ref).max() <= IOU_ATOL
@@ -172,3 +176,27 @@ def test_cfg5_full_size_sampled():
     k = keep.cpu().numpy()
     assert np.array_equal(k, oracle.nms_scan_mask(mask.cpu().numpy().view(np.uint64)))
     assert 0.05 < k.mean() < 0.9
+
+
+def test_indexed_and_tiled_paths_agree():
+    """The grid-indexed path (zero fill + circle-grid candidates) and the tiled sweep
+    give bitwise the same matrix, mask and suppressor sets."""
+    sc = synth.gen_cfg5_scene(n_objects=300, per_object=50, seed=17)
+    x, y = to_dev(sc.polys)
+    n = sc.polys.n
+    a = dgal.iou_pairwise(x, y, x, y, thr=sc.thr, nbr_cap=64, indexed=True)
+    b = dgal.iou_pairwise(x, y, x, y, thr=sc.thr, nbr_cap=64, indexed=False)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and torch.equal(a[2], b[2])
+    ia, ib = a[3].cpu().numpy(), b[3].cpu().numpy()
+    c = a[2].cpu().numpy()
+    for r in range(n):
+        k = min(c[r], 64)
+        assert set(ia[r, :k].tolist()) == set(ib[r, :k].tolist())
+    # degenerate scene: every box identical (one grid cell holds everything)
+    xs = x[:1].repeat(700, 1).contiguous()
+    ys = y[:1].repeat(700, 1).contiguous()
+    u = dgal.iou_pairwise(xs, ys, xs, ys, thr=0.5, indexed=True)
+    v = dgal.iou_pairwise(xs, ys, xs, ys, thr=0.5, indexed=False)
+    assert torch.equal(u[0], v[0]) and torch.equal(u[1], v[1])
+    assert bool((u[0] == 1.0).all())
