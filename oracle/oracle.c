@@ -23,7 +23,9 @@
  *   2. < 3 points -> empty;
  *   3. CCW order by atan2 about the mean;
  *   4. shoelace area; area <= 0 -> empty (R7);
- *   5. canonical rotation: start at the smallest flag byte (R3);
+ *   5. canonical start (R3): the first vertex met walking p1's boundary
+ *      counter-clockwise from p1's vertex 0 (FromP2(0) when p1's boundary does
+ *      not touch p1 ∩ p2, i.e. p2 inside p1);
  *   6. IoU.
  * The backward is the analytic chain rule of S:303 over the oracle's own
  * vertices/flags: area_grad of the intersection, routed by flag
@@ -86,8 +88,28 @@ typedef struct {
  * polygon: cross(b - a, q - a) >= 0 means left of (inside) the edge line. */
 static double side(vec2 a, vec2 b, vec2 q) { return vcross(vsub(b, a), vsub(q, a)); }
 
-static int min_byte_index(const uint8_t *f, int n)
+/*
+ * Canonical start (R3): the vertex with the smallest position along p1's boundary,
+ * measured CCW from p1's vertex 0: FromP1(i) sits at i, Cross(i, j) at i + t with
+ * t its parameter on p1 edge i; FromP2 vertices are not on p1's boundary.  If no
+ * vertex is on p1's boundary (p2 inside p1) the sequence starts at its smallest
+ * byte (FromP2 with the smallest index).
+ */
+static int canonical_start(int K, const vec2 *P, const vec2 *v, const uint8_t *f, int n)
 {
+    int best = -1;
+    double bkey = 0.0;
+    for (int k = 0; k < n; ++k) {
+        int tag = f[k] >> 6, i = (f[k] >> 3) & 7, j = f[k] & 7;
+        double key;
+        if (tag == 1) key = (double)j;
+        else if (tag == 3) {
+            vec2 a = P[i], e = vsub(P[(i + 1) % K], P[i]);
+            key = (double)i + vdot(vsub(v[k], a), e) / vdot(e, e);
+        } else continue;
+        if (best < 0 || key < bkey) { best = k; bkey = key; }
+    }
+    if (best >= 0) return best;
     int m = 0;
     for (int k = 1; k < n; ++k)
         if (f[k] < f[m]) m = k;
@@ -164,8 +186,8 @@ static void intersect_by_definition(int K, const vec2 *P, const vec2 *Q, isect_t
     double A = shoelace(cand, nc);
     if (!(A > 0.0)) return;
 
-    /* (5) canonical rotation: start at the smallest flag byte (R3) */
-    int s = min_byte_index(cflag, nc);
+    /* (5) canonical start (R3) */
+    int s = canonical_start(K, P, cand, cflag, nc);
     for (int c = 0; c < nc; ++c) {
         out->v[c] = cand[(s + c) % nc];
         out->flag[c] = cflag[(s + c) % nc];
@@ -482,7 +504,7 @@ int oracle_nms_scan_mask(int64_t n, int64_t words, const uint64_t *mask, uint8_t
  * side >= 0 (boundary-inclusive, R5).  A crossing on an edge with id P1-i is
  * Cross(i,j); on an edge with id P2-j1 it snaps to the shared p2 vertex when
  * j1, j are adjacent (FromP2), else CrossP2P2 (tag 00) (R8).
- * Output: canonical rotation (R3), empty when < 3 vertices or area <= 0.
+ * Output: canonical start (R3), empty when < 3 vertices or area <= 0.
  */
 int oracle_sh_intersect(int K, int64_t n,
                         const double *x1, const double *y1,
@@ -550,7 +572,7 @@ int oracle_sh_intersect(int K, int64_t n,
             nx[k] = 0; if (area_i) area_i[k] = 0.0;
             continue;
         }
-        int s = min_byte_index(cf, nc);
+        int s = canonical_start(K, P, cur, cf, nc);
         for (int c = 0; c < nc; ++c) xflags[k * cap + c] = cf[(s + c) % nc];
         nx[k] = (uint8_t)nc;
         if (area_i) area_i[k] = A;

@@ -15,7 +15,8 @@
 //   * nx / xflags: walking p1's edges in order emits FromP1(i) or
 //     the entering Cross(i, j_in), then the exiting Cross(i, j_out) followed by
 //     the run of p2 vertices strictly inside p1 — the CCW vertex sequence of
-//     p1 ∩ p2 — rotated to start at its smallest byte (R3);
+//     p1 ∩ p2, which starts at the first vertex along p1's boundary from v0:
+//     exactly the canonical order of reading R3;
 //   * iou_grad: dA_i/dv moves only the boundary pieces lying on the edges
 //     incident to v (shape derivative); with n = perp(edge vector),
 //       dA_i/dv_i += n_i ∫_{t0}^{t1} (1-t) dt,   dA_i/dv_i+1 += n_i ∫_{t0}^{t1} t dt,
@@ -147,39 +148,6 @@ __device__ __forceinline__ uint32_t seq_byte(const Seq<K> &s, int p)  // p stati
 {
     const uint64_t w = s.w[p >> 3];
     return (uint32_t)(w >> (8 * (p & 7))) & 0xFFu;
-}
-
-// Canonical form (R3): rotate the n valid bytes so the smallest byte comes first.
-// The minimum and its position come from one min over keys (byte << 4 | pos).
-template <int K>
-__device__ __forceinline__ Seq<K> seq_canonical(const Seq<K> &s, int n)
-{
-    uint32_t best = 0xFFFFFFFFu;
-#pragma unroll
-    for (int p = 0; p < 2 * K; ++p) {
-        const uint32_t key = (seq_byte<K>(s, p) << 4) | (uint32_t)p;
-        best = (p < n) ? min(best, key) : best;
-    }
-    const uint32_t r = best & 15u;
-    Seq<K> o;
-    if (K == 4) {
-        const uint64_t x = s.w[0];
-        const uint64_t m = shl64(~0ull, 8u * (uint32_t)n);  // bytes >= n
-        o.w[0] = (shr64(x, 8u * r) | shl64(x, 8u * ((uint32_t)n - r))) & ~m;
-    } else {
-        o.w[0] = 0;
-        o.w[Seq<K>::NW - 1] = 0;
-#pragma unroll
-        for (int p = 0; p < 2 * K; ++p) {
-            int q = p + (int)r;
-            q = (q >= n) ? q - n : q;
-            // byte q of s, q dynamic: select the word, then shift
-            const uint64_t w = (q >= 8) ? s.w[Seq<K>::NW - 1] : s.w[0];
-            const uint64_t b = (p < n) ? ((w >> (8 * (q & 7))) & 0xFFull) : 0ull;
-            o.w[p >> 3] |= b << (8 * (p & 7));
-        }
-    }
-    return o;
 }
 
 // ---------------------------------------------------------------------------
@@ -358,9 +326,11 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
             else { s.w[0] = 0x8786858483828180ull; s.w[Seq<K>::NW - 1] = 0; }
             pos = K;
         }
+        // The walk from p1's edge 0 IS the canonical order (R3: start at the first
+        // vertex along p1's boundary from v0; FromP2(0) when p2 lies inside p1).
         nonempty = nonempty && pos >= 3 && pos <= 2 * K;
         if (nonempty) {
-            out.seq = seq_canonical<K>(s, pos);
+            out.seq = s;
             out.nx = pos;
         }
     }

@@ -58,7 +58,7 @@ def test_degenerate_zoo():
         assert all(np.all(g.reshape(-1, 4)[k] == 0) for g in gr)
     assert list(xf[4][:4]) == [0x40, 0x41, 0x42, 0x43]
     assert list(xf[5][:4]) == [0x80, 0x81, 0x82, 0x83]
-    assert list(xf[6][:4]) == [0x42, 0xD3, 0x80, 0xC8]
+    assert list(xf[6][:4]) == [0xC8, 0x42, 0xD3, 0x80]
     assert abs(iou[6] - 1 / 7) < 1e-6
     ref = oracle.iou_paired_fwd(b.p1, b.p2)
     assert_iou_close(iou, ref["iou"])

@@ -142,7 +142,7 @@ def test_symmetry_and_role_swap():
         assert n1 == n2
         a = [int(x) for x in f["xflags"][k][:n1]]
         bb = [int(x) for x in r["xflags"][k][:n2]]
-        assert _canon(_relabel_swap(bb)) == a
+        assert _canon(_relabel_swap(bb)) == _canon(a)
 
 
 @pytest.mark.parametrize("cfg", [1, 3, 4])
@@ -335,3 +335,40 @@ def test_sh_degenerate_zoo_matches_definition():
         assert abs(s["area_i"][0] - ai) < 1e-15
     assert fwd1(SQ, SQ + [1.0, 0.0])[0] == 0.0
     assert fwd1(SQ, SQ + [1.0, 1.0])[0] == 0.0
+
+
+def _p1_key(P, v, b):
+    """position along p1's boundary from v0 (reading R3): FromP1(i) -> i,
+    Cross(i, j) -> i + t; FromP2 -> None (not on p1's boundary)."""
+    t, i, j = decode(b)
+    K = len(P)
+    if t == 1:
+        return float(j)
+    if t == 3:
+        a, e = P[i], P[(i + 1) % K] - P[i]
+        return i + float(np.dot(v - a, e) / np.dot(e, e))
+    return None
+
+
+@pytest.mark.parametrize("cfg", [1, 3, 4])
+def test_canonical_start_convention(cfg):
+    """R3: xflags start at the vertex met first walking p1's boundary CCW from v0
+    (the smallest byte when no vertex lies on p1's boundary), and the sequence is
+    CCW (positive signed area of the listed vertices)."""
+    b = margin_batch(cfg, 400)
+    x1, y1 = b.p1.xy64()
+    x2, y2 = b.p2.xy64()
+    for k in range(b.n):
+        P = np.stack([x1[k], y1[k]], 1)
+        Q = np.stack([x2[k], y2[k]], 1)
+        verts, flags, _ = oracle.intersect_one(P, Q)
+        if not flags:
+            continue
+        keys = [_p1_key(P, v, f) for v, f in zip(verts, flags)]
+        on = [x for x in keys if x is not None]
+        if on:
+            assert keys[0] == min(on)
+        else:
+            assert flags[0] == min(flags)
+        a = 0.5 * np.sum(verts[:, 0] * np.roll(verts[:, 1], -1) - np.roll(verts[:, 0], -1) * verts[:, 1])
+        assert a > 0
