@@ -300,6 +300,34 @@ def bench_e2e(ctx, K, planes, g, iou_dev, steps):
             "path": "pinned host buffers -> 3-stream chunked pipeline (H2D, fwd, bwd, D2H) per GPU"}
 
 
+def bench_fused(ctx, n, steps, warmup, peak):
+    """the same cfg3 batch through the fused loss kernel
+    (dgal_iou_paired_fused, dL/dIoU = -1/n known up front): one launch per step."""
+    import paper_2011_11134_b200 as dgal
+    torch = ctx.torch
+    K, planes, _, _ = paired_inputs(ctx, 3, n)
+    out = (torch.empty(n, dtype=torch.float32, device=ctx.dev),
+           *(torch.empty((n, K), dtype=torch.float32, device=ctx.dev) for _ in range(4)))
+    for _ in range(warmup):
+        dgal.iou_paired_fused(*planes, scale=-1.0 / n, out=out)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(ctx.dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.barrier()
+    a.record(stream)
+    for _ in range(steps):
+        dgal.iou_paired_fused(*planes, scale=-1.0 / n, out=out)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = ctx.max_over_ranks(a.elapsed_time(b)) / steps
+    nbytes = 16 * K + 4 + 16 * K   # polygons in, IoU + vertex gradients out
+    return {"workload": "cfg3 batch, fused IoU-loss fwd+bwd (dgal_iou_paired_fused, SURVEY f2)",
+            "scaling": "weak", "pairs_per_s": n * ctx.world / (ms * 1e-3), "ms_per_step": ms,
+            "roofline": {"bound": "hbm", "kernel": "paired_fused_kernel<4>",
+                         "achieved": n * nbytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": n * nbytes / (ms * 1e-3) / 1e9 / peak, "algorithmic_bytes_per_pair": nbytes}}
+
+
 def bench_cfg5(ctx, steps, warmup, peak):
     """Pairwise 100k x 100k IoU matrix + NMS mask/lists + greedy keep; rows sharded."""
     import paper_2011_11134_b200 as dgal
@@ -430,6 +458,7 @@ def main(argv=None):
                            "frac": n4 * bb4 / (b4 * 1e-3) / 1e9 / peak}}
         del planes4, g4
         torch.cuda.empty_cache()
+        secondary["cfg3_fused"] = bench_fused(ctx, n, max(10, args.steps // 4), args.warmup, peak)
         secondary["cfg5"] = bench_cfg5(ctx, steps=5, warmup=2, peak=peak)
 
     if ctx.dist:

@@ -87,6 +87,24 @@ dgal_status dgal_iou_paired_bwd(int K, int64_t n,
                                 dgal_stream stream);
 
 /*
+ * Fused forward + backward for an IoU loss whose upstream gradient is known
+ * before the forward (e.g. L = mean(1 - IoU): dL/dIoU = -1/n).
+ * One pass per pair computes the IoU and dL/d(vertices) from the same clip
+ * intervals — no nx/xflags round trip through memory (the split API above is
+ * the paper's; this is its fusion).  dL/dIoU of pair k is grad_iou[k] when
+ * grad_iou != NULL, else grad_scale.  iou [n] nullable; gx1, gy1, gx2, gy2
+ * [n * K] overwritten (same values as dgal_iou_paired_fwd + _bwd up to rounding;
+ * IoU bit-identical to dgal_iou_pairwise).
+ */
+dgal_status dgal_iou_paired_fused(int K, int64_t n,
+                                  const float *x1, const float *y1,
+                                  const float *x2, const float *y2,
+                                  const float *grad_iou, float grad_scale,
+                                  float *iou,
+                                  float *gx1, float *gy1, float *gx2, float *gy2,
+                                  dgal_stream stream);
+
+/*
  * Pairwise IoU of a row block against all columns ("cartesian";
  * north_star "full N x M pairwise matrices (detection/NMS)"), forward only.
  * Rows play p1, columns p2 (R4).  Row r has global index row_offset + r; column c

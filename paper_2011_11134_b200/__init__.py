@@ -19,7 +19,7 @@ import torch
 
 from ._lib import DgalError, call, lib  # noqa: F401
 
-__all__ = ["iou_paired_fwd", "iou_paired_bwd", "iou_pairwise", "pairwise_workspace", "nms_round", "nms_keep",
+__all__ = ["iou_paired_fwd", "iou_paired_bwd", "iou_paired_fused", "PolyIoULoss", "iou_pairwise", "pairwise_workspace", "nms_round", "nms_keep",
            "nms", "PolyIoU", "DgalError", "build_info"]
 
 
@@ -85,6 +85,43 @@ def iou_paired_bwd(x1, y1, x2, y2, grad_iou, nx, xflags, K: int | None = None, o
     call("dgal_iou_paired_bwd", K, n, _ptr(x1), _ptr(y1), _ptr(x2), _ptr(y2), _ptr(grad_iou), _ptr(nx),
          _ptr(xflags), _ptr(gx1), _ptr(gy1), _ptr(gx2), _ptr(gy2), _stream(x1.device))
     return gx1, gy1, gx2, gy2
+
+
+def iou_paired_fused(x1, y1, x2, y2, grad=None, scale: float = 1.0, K: int | None = None, out=None,
+                     want_iou: bool = True):
+    """Fused loss forward + backward (dgal_iou_paired_fused): dL/dIoU = grad[k] (a
+    CUDA float tensor [n]) or the scalar `scale`.  Returns (iou | None, gx1, gy1, gx2, gy2)."""
+    for t, nm in ((x1, "x1"), (y1, "y1"), (x2, "x2"), (y2, "y2")):
+        _plane(t, nm)
+    if grad is not None:
+        _plane(grad, "grad")
+    K, n = _K_n(x1, K)
+    if out is None:
+        iou = torch.empty(n, dtype=torch.float32, device=x1.device) if want_iou else None
+        g4 = tuple(torch.empty_like(x1) for _ in range(4))
+    else:
+        iou, g4 = out[0], out[1:]
+    call("dgal_iou_paired_fused", K, n, _ptr(x1), _ptr(y1), _ptr(x2), _ptr(y2), _ptr(grad), float(scale),
+         _ptr(iou), *[_ptr(t) for t in g4], _stream(x1.device))
+    return (iou, *g4)
+
+
+class PolyIoULoss(torch.autograd.Function):
+    """L = mean(1 - IoU) over the pairs, forward and backward in ONE kernel pass
+    (dgal_iou_paired_fused with dL/dIoU = -1/n; the backward scales the stored
+    vertex gradients by the incoming dL — exact, the kernel is linear in it)."""
+
+    @staticmethod
+    def forward(ctx, x1, y1, x2, y2):
+        x1, y1, x2, y2 = (t.contiguous() for t in (x1, y1, x2, y2))
+        n = x1.shape[0]
+        iou, g1x, g1y, g2x, g2y = iou_paired_fused(x1, y1, x2, y2, scale=-1.0 / max(n, 1))
+        ctx.save_for_backward(g1x, g1y, g2x, g2y)
+        return (1.0 - iou).mean()
+
+    @staticmethod
+    def backward(ctx, dl):
+        return tuple(g * dl for g in ctx.saved_tensors)
 
 
 def pairwise_workspace(m: int, device=None) -> torch.Tensor:

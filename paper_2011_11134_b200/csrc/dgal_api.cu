@@ -55,6 +55,21 @@ dgal_status dgal_iou_paired_bwd(int K, int64_t n, const float *x1, const float *
                                              gy2, as_cuda(stream)));
 }
 
+dgal_status dgal_iou_paired_fused(int K, int64_t n, const float *x1, const float *y1, const float *x2,
+                                  const float *y2, const float *grad_iou, float grad_scale, float *iou,
+                                  float *gx1, float *gy1, float *gx2, float *gy2, dgal_stream stream)
+{
+    if (K != 4 && K != 8) return DGAL_ERR_UNSUPPORTED_K;
+    if (n < 0) return DGAL_ERR_INVALID_ARG;
+    if (n == 0) return DGAL_OK;
+    if (!x1 || !y1 || !x2 || !y2 || !gx1 || !gy1 || !gx2 || !gy2) return DGAL_ERR_INVALID_ARG;
+    if (!aligned(x1, 16) || !aligned(y1, 16) || !aligned(x2, 16) || !aligned(y2, 16) ||
+        !aligned(gx1, 16) || !aligned(gy1, 16) || !aligned(gx2, 16) || !aligned(gy2, 16))
+        return DGAL_ERR_MISALIGNED;
+    return from_cuda(dgal::launch_paired_fused(K, n, x1, y1, x2, y2, grad_iou, grad_scale, iou, gx1, gy1, gx2,
+                                               gy2, as_cuda(stream)));
+}
+
 dgal_status dgal_iou_pairwise(int K, int64_t n_rows, const float *row_x, const float *row_y, int64_t m,
                               const float *col_x, const float *col_y, int64_t row_offset, float *iou,
                               float nms_thresh, uint64_t *mask, int64_t mask_words, int32_t *nbr_count,

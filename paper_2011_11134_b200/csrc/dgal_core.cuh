@@ -160,14 +160,25 @@ struct FwdOut {
     Seq<K> seq;
 };
 
+// The edge-interval clip shared by the paired forward, the pairwise path and the
+// fused loss kernel: edge vectors, shoelace terms, the Cyrus-Beck interval of
+// every edge of both polygons (FLAGS: p1 intervals carry their line index in the
+// low mantissa bits) and the Green area of p1 ∩ p2.
+template <int K>
+struct Clip {
+    float gx[K], gy[K], fx[K], fy[K];  // edge vectors of p1, p2
+    float C1[K], C2[K];                // shoelace terms v_i x v_i+1, w_j x w_j+1
+    float t0[K], t1[K], s0[K], s1[K];  // boundary pieces on p1 / p2 edges
+    float A1x2, A2x2, Aix2;            // twice the areas
+    bool nonempty;
+};
+
 // p1, p2 must already be recentred on o = p1.v0 (p1.x[0] == p1.y[0] == 0).
 template <int K, bool FLAGS>
-__device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly<K> &Q)
+__device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &Q, Clip<K> &c)
 {
-    constexpr uint32_t KMASK = (1u << K) - 1u;
-
     // edge vectors g_i = v_i+1 - v_i (p1), f_j = w_j+1 - w_j (p2); shoelace terms
-    float gx[K], gy[K], fx[K], fy[K], C1[K], C2[K];
+    float *gx = c.gx, *gy = c.gy, *fx = c.fx, *fy = c.fy, *C1 = c.C1, *C2 = c.C2;
     float A1x2 = 0.f, A2x2 = 0.f;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
@@ -213,7 +224,7 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
     // above, b == a keeps all (a > 0: t* = +inf) or nothing (a < 0: t* = -inf).
     // Both-outside end points give t* > 1 (below) or t* < 0 (above): the interval
     // empties itself.  (m t* is NaN when m = 0 and t* = inf: max/min ignore it.)
-    float t0[K], t1[K], s0[K], s1[K];
+    float *t0 = c.t0, *t1 = c.t1, *s0 = c.s0, *s1 = c.s1;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         const int i1 = (i + 1) % K;
@@ -261,7 +272,23 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
         Aix2 = fmaf(fmaxf(s1[k] - s0[k], 0.f), C2[k], Aix2);
     }
     Aix2 = fminf(Aix2, fminf(A1x2, A2x2));
-    bool nonempty = !separated && (Aix2 > 0.f);
+    c.A1x2 = A1x2;
+    c.A2x2 = A2x2;
+    c.Aix2 = Aix2;
+    c.nonempty = !separated && (Aix2 > 0.f);
+
+}
+
+// p1, p2 must already be recentred on o = p1.v0 (p1.x[0] == p1.y[0] == 0).
+template <int K, bool FLAGS>
+__device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly<K> &Q)
+{
+    constexpr uint32_t KMASK = (1u << K) - 1u;
+    Clip<K> c;
+    clip_intervals<K, FLAGS>(P, Q, c);
+    const float *t0 = c.t0, *t1 = c.t1, *s0 = c.s0, *s1 = c.s1;
+    const float A1x2 = c.A1x2, A2x2 = c.A2x2, Aix2 = c.Aix2;
+    bool nonempty = c.nonempty;
 
     FwdOut<K, FLAGS> out;
 #pragma unroll
@@ -339,6 +366,58 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
         out.iou = (Aux2 > 0.f) ? fminf(Aix2 / Aux2, 1.f) : 0.f;
     }
     return out;
+}
+
+// ---------------------------------------------------------------------------
+// fused IoU forward + backward for a loss whose dL/dIoU is known up front
+// (e.g. L = mean(1 - IoU) has dL/dIoU = -1/n)
+// ---------------------------------------------------------------------------
+// The gradient uses the very intervals the forward computes (no xflags round
+// trip, no crossing recomputation): dA_i/dv_i += n_i ∫(1-t)dt, dA_i/dv_i+1 +=
+// n_i ∫t dt over each boundary piece, then the S:303 chain.
+// p1, p2 recentred on p1.v0.  Returns IoU (identical to the pairwise path).
+template <int K>
+__device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, float g, Poly<K> &G1,
+                                           Poly<K> &G2)
+{
+#pragma unroll
+    for (int k = 0; k < K; ++k) { G1.x[k] = 0.f; G1.y[k] = 0.f; G2.x[k] = 0.f; G2.y[k] = 0.f; }
+    Clip<K> c;
+    clip_intervals<K, false>(P, Q, c);
+    if (!c.nonempty) return 0.f;
+    const float Aux2 = (c.A1x2 + c.A2x2) - c.Aix2;
+    if (!(Aux2 > 0.f)) return 0.f;
+    const float iou = fminf(c.Aix2 / Aux2, 1.f);
+
+    // piece weights (saturate: dead edges carry arbitrary end points, length 0)
+    float al1[K], be1[K], al2[K], be2[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        const float a0 = __saturatef(c.t0[i]), a1 = __saturatef(c.t1[i]);
+        const float b0 = __saturatef(c.s0[i]), b1 = __saturatef(c.s1[i]);
+        const float l1 = fmaxf(a1 - a0, 0.f), l2 = fmaxf(b1 - b0, 0.f);
+        const float h1 = 0.5f * (a0 + a1), h2 = 0.5f * (b0 + b1);
+        al1[i] = l1 - l1 * h1; be1[i] = l1 * h1;
+        al2[i] = l2 - l2 * h2; be2[i] = l2 * h2;
+    }
+    // dIoU/dA_i = (A_u + A_i)/A_u^2, dIoU/dA_1,2 = -A_i/A_u^2
+    const float Ai = 0.5f * c.Aix2, Au = 0.5f * Aux2;
+    const float inv = 1.f / Au;
+    const float q = Ai * inv;
+    const float ci = g * ((1.f + q) * inv);
+    const float cu = g * (-q * inv);
+    const float hu = 0.5f * cu;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int km = (k + K - 1) % K;
+        const float wa1 = fmaf(ci, al1[k], hu), wb1 = fmaf(ci, be1[km], hu);
+        const float wa2 = fmaf(ci, al2[k], hu), wb2 = fmaf(ci, be2[km], hu);
+        G1.x[k] = fmaf(wa1, c.gy[k], wb1 * c.gy[km]);
+        G1.y[k] = -fmaf(wa1, c.gx[k], wb1 * c.gx[km]);
+        G2.x[k] = fmaf(wa2, c.fy[k], wb2 * c.fy[km]);
+        G2.y[k] = -fmaf(wa2, c.fx[k], wb2 * c.fx[km]);
+    }
+    return iou;
 }
 
 // ---------------------------------------------------------------------------

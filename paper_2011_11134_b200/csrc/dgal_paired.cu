@@ -348,4 +348,44 @@ cudaError_t launch_paired_bwd(int K, int64_t n, const float *x1, const float *y1
     return launch_bwd_k<8>(n, x1, y1, x2, y2, grad, nx, xflags, gx1, gy1, gx2, gy2, st);
 }
 
+// ---------------------------------------------------------------------------
+// Fused loss forward + backward, one pair per thread
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(kPairedThreads)
+paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
+                    const float *__restrict__ x2, const float *__restrict__ y2,
+                    const float *__restrict__ grad, float scale, float *__restrict__ iou,
+                    float *__restrict__ gx1, float *__restrict__ gy1,
+                    float *__restrict__ gx2, float *__restrict__ gy2)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    Poly<K> P, Q, G1, G2;
+    load_poly<K>(x1, y1, k, P);
+    load_poly<K>(x2, y2, k, Q);
+    const float g = grad ? __ldcs(grad + k) : scale;
+    recentre<K>(P, Q);
+    const float v = iou_fused<K>(P, Q, g, G1, G2);
+    if (iou) __stcs(iou + k, v);
+    store_plane<K>(gx1, k, G1.x);
+    store_plane<K>(gy1, k, G1.y);
+    store_plane<K>(gx2, k, G2.x);
+    store_plane<K>(gy2, k, G2.y);
+}
+
+cudaError_t launch_paired_fused(int K, int64_t n, const float *x1, const float *y1, const float *x2,
+                                const float *y2, const float *grad, float scale, float *iou, float *gx1,
+                                float *gy1, float *gx2, float *gy2, cudaStream_t st)
+{
+    const unsigned grid = (unsigned)((n + kPairedThreads - 1) / kPairedThreads);
+    if (K == 4)
+        paired_fused_kernel<4><<<grid, kPairedThreads, 0, st>>>(n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1,
+                                                                gx2, gy2);
+    else
+        paired_fused_kernel<8><<<grid, kPairedThreads, 0, st>>>(n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1,
+                                                                gx2, gy2);
+    return cudaGetLastError();
+}
+
 }  // namespace dgal

@@ -24,7 +24,8 @@ def _declared():
 
 def test_header_declares_the_boundary():
     names = _declared()
-    assert names == sorted(["dgal_iou_paired_fwd", "dgal_iou_paired_bwd", "dgal_iou_pairwise",
+    assert names == sorted(["dgal_iou_paired_fwd", "dgal_iou_paired_bwd", "dgal_iou_paired_fused",
+                            "dgal_iou_pairwise",
                             "dgal_pairwise_workspace_bytes", "dgal_nms_round", "dgal_nms_keep",
                             "dgal_status_string", "dgal_build_info"])
 
@@ -104,6 +105,7 @@ def test_sass_is_sm100a_register_resident():
     stats = _sass_stats()
     names = " ".join(stats)
     for k in ("paired_fwd_direct_kernelILi4", "paired_fwd_kernelILi8", "paired_bwd_kernelILi4",
+              "paired_fused_kernelILi4", "paired_fused_kernelILi8",
               "paired_bwd_kernelILi8", "pairwise_kernelILi4", "nms_keep_kernel", "nms_round_kernel"):
         assert k in names, k
     for name, c in stats.items():

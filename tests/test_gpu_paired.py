@@ -175,3 +175,60 @@ def test_backward_unaligned_side_inputs():
     got = dgal.iou_paired_bwd(x1, y1, x2, y2, gb, nb, xf)
     for a, c in zip(ref, got):
         assert torch.equal(a, c)
+
+
+# ---------------------------------------------------------------------------
+# fused loss forward + backward
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("cfg,n", [(1, 1024), (3, 40_000), (4, 20_000)])
+def test_fused_matches_oracle(cfg, n):
+    b = margin_batch(cfg, n)
+    x1, y1 = to_dev(b.p1)
+    x2, y2 = to_dev(b.p2)
+    g = torch.from_numpy(b.grad).to(dev())
+    iou, *gr = dgal.iou_paired_fused(x1, y1, x2, y2, grad=g)
+    torch.cuda.synchronize()
+    ref = oracle.iou_paired_fwd(b.p1, b.p2)
+    assert_iou_close(iou.cpu().numpy(), ref["iou"])
+    rg = oracle.iou_paired_bwd(b.p1, b.p2, b.grad)
+    for got, want in zip(gr, rg):
+        assert_grad_close(got.cpu().numpy().reshape(want.shape), want)
+
+
+def test_fused_consistent_with_split_and_pairwise():
+    b = margin_batch(3, 20_000)
+    x1, y1 = to_dev(b.p1)
+    x2, y2 = to_dev(b.p2)
+    g = torch.from_numpy(b.grad).to(dev())
+    iou_f, *gf = dgal.iou_paired_fused(x1, y1, x2, y2, grad=g)
+    iou_s, nx, xf = dgal.iou_paired_fwd(x1, y1, x2, y2)
+    gs = dgal.iou_paired_bwd(x1, y1, x2, y2, g, nx, xf)
+    assert torch.allclose(iou_f, iou_s, atol=2e-6, rtol=0)
+    for a, c in zip(gf, gs):
+        assert torch.allclose(a, c, atol=1e-4, rtol=1e-3)
+    # the fused IoU is bitwise the pairwise (flag-free) IoU of the same pairs
+    m = 256
+    pw, _, _, _ = dgal.iou_pairwise(x1[:m].contiguous(), y1[:m].contiguous(), x2[:m].contiguous(),
+                                    y2[:m].contiguous(), want_mask=False)
+    assert torch.equal(pw.diagonal(), iou_f[:m])
+    # scalar mode == constant array; bitwise linearity in dL/dIoU
+    s = -1.0 / 4096
+    _, *ga = dgal.iou_paired_fused(x1, y1, x2, y2, scale=s)
+    _, *gb = dgal.iou_paired_fused(x1, y1, x2, y2, grad=torch.full_like(g, s))
+    _, *gc = dgal.iou_paired_fused(x1, y1, x2, y2, scale=2 * s)
+    for a, c, d in zip(ga, gb, gc):
+        assert torch.equal(a, c) and torch.equal(d, 2 * a)
+
+
+def test_fused_loss_autograd():
+    b = margin_batch(1, 1000)
+    x1, y1 = to_dev(b.p1)
+    x2, y2 = to_dev(b.p2)
+    ts = [t.clone().requires_grad_(True) for t in (x1, y1, x2, y2)]
+    loss = dgal.PolyIoULoss.apply(*ts)
+    loss.backward()
+    iou = oracle.iou_paired_fwd(b.p1, b.p2)["iou"]
+    assert abs(loss.item() - float(np.mean(1 - iou))) < 1e-5
+    rg = oracle.iou_paired_bwd(b.p1, b.p2, np.full(b.n, -1.0 / b.n))
+    for t, want in zip(ts, rg):
+        assert_grad_close(t.grad.cpu().numpy().reshape(want.shape), want)
