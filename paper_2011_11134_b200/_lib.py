@@ -6,7 +6,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libdgal.so")
+# DGAL_CHECKED=1 selects the bounds-checked build (device asserts), see build.py
+SO_PATH = os.path.join(HERE, "libdgal_checked.so" if os.environ.get("DGAL_CHECKED") == "1" else "libdgal.so")
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

@@ -25,29 +25,38 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
-def _stale() -> bool:
-    if not os.path.exists(SO):
+def _stale(so: str = SO) -> bool:
+    if not os.path.exists(so):
         return True
-    t = os.path.getmtime(SO)
+    t = os.path.getmtime(so)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + [HEADER]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not (force or _stale()):
-        return SO
+SO_CHECKED = os.path.join(HERE, "libdgal_checked.so")
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """Release library (or, checked=True, libdgal_checked.so with device-side
+    bounds asserts: -DDGAL_CHECKED, selected at load time by DGAL_CHECKED=1)."""
+    out = SO_CHECKED if checked else SO
+    if not (force or _stale(out)):
+        return out
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", SO + ".tmp", *sources()]
+    extra = ["-DDGAL_CHECKED"] if checked else []
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", out + ".tmp", *sources()]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
     if verbose:
         print(r.stderr)
-    os.replace(SO + ".tmp", SO)
-    with open(os.path.join(HERE, "ptxas_report.txt"), "w") as f:
-        f.write(r.stderr)
-    return SO
+    os.replace(out + ".tmp", out)
+    if not checked:
+        with open(os.path.join(HERE, "ptxas_report.txt"), "w") as f:
+            f.write(r.stderr)
+    return out
 
 
 if __name__ == "__main__":
-    build(force=True, verbose=True)
+    import sys
+    build(force=True, verbose=True, checked="--checked" in sys.argv)

@@ -33,8 +33,17 @@
 // a line gives exactly 0: identical polygons give IoU == 1 exactly.
 #pragma once
 
+#include <cassert>
 #include <cstdint>
 #include <cuda_runtime.h>
+
+#ifndef DGAL_ASSERT
+#ifdef DGAL_CHECKED
+#define DGAL_ASSERT(x) assert(x)
+#else
+#define DGAL_ASSERT(x) ((void)0)
+#endif
+#endif
 
 namespace dgal {
 
@@ -480,6 +489,7 @@ __device__ __forceinline__ void bwd_crossing(const float *sPx, const float *sPy,
     const float t = __saturatef((Dx * hy - Dy * hx) * r);      // along p1 edge i
     const float s = __saturatef((Dx * ey - Dy * ex) * r);      // along p2 edge j
     const bool enter = den < 0.f;
+    DGAL_ASSERT(i >= 0 && i < K && j >= 0 && j < K);
     scr[(enter ? i : K + i) * TILE] = t;
     scr[(enter ? 3 * K + j : 2 * K + j) * TILE] = s;
 }

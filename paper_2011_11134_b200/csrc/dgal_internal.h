@@ -2,8 +2,18 @@
 // .cu translation units of libdgal.so (not part of the public ABI).
 #pragma once
 
+#include <cassert>
 #include <cstdint>
 #include <cuda_runtime.h>
+
+// Checked build (-DDGAL_CHECKED, libdgal_checked.so): device-side bounds asserts on
+// every dynamic shared / global index (compute-sanitizer is not available on the
+// GPU pool).  Compiled out of the release library.
+#ifdef DGAL_CHECKED
+#define DGAL_ASSERT(x) assert(x)
+#else
+#define DGAL_ASSERT(x) ((void)0)
+#endif
 
 namespace dgal {
 

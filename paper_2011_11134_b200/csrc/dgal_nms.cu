@@ -22,6 +22,7 @@ __device__ __forceinline__ int decide(int64_t r, int64_t i, const uint64_t *__re
     if (cnt >= 0 && cnt <= cap) {
         const int32_t *lst = nbr_idx + r * cap;
         for (int k = 0; k < cnt; ++k) {
+            DGAL_ASSERT(lst[k] >= 0 && lst[k] < i);
             const uint8_t s = status[lst[k]];
             any_kept |= (s == 1);
             all_removed &= (s == 2);

@@ -202,6 +202,7 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
         if (tid == 0 && next < nfull) issue(next, s ^ 1);
         typename BwdSmem<K>::Stage &T = S.st[s];
         const int64_t k = tile * kTile + tid;
+        DGAL_ASSERT(tile < ntiles && (tile >= nfull || (tile + 1) * kTile <= n));
         if (tile < nfull) {
             mbar_wait(&S.bar[s], (uint32_t)(it >> 1) & 1u);
         } else if (k < n) {  // direct path: this thread stages its own pair
@@ -243,7 +244,10 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
 #pragma unroll
         for (int p = 0; p < 2 * K; ++p) {
             const uint32_t b = (p < m) ? seq_byte<K>(sq, p) : 0u;
-            if (b >= 0xC0u) queue[at++] = (uint16_t)((lane << 8) | b);
+            if (b >= 0xC0u) {
+                DGAL_ASSERT(at >= 0 && at < 32 * 2 * K);
+                queue[at++] = (uint16_t)((lane << 8) | b);
+            }
         }
         bwd_prologue<K, kTile>(S.scr + tid);
         __syncwarp();
@@ -251,7 +255,9 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
         for (int base = 0; base < total; base += 32) {   // warp-uniform trip count
             const int e = base + lane;
             if (e < total) {
+                DGAL_ASSERT(e < 32 * 2 * K);
                 const uint32_t ent = queue[e];
+                DGAL_ASSERT((int)(ent >> 8) < 32);
                 const int pt = warp * 32 + (int)(ent >> 8);
                 bwd_crossing<K, kTile>(T.x1 + pt * K, T.y1 + pt * K, T.x2 + pt * K, T.y2 + pt * K,
                                        ent & 0xFFu, S.scr + pt);

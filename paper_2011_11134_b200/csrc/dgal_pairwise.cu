@@ -103,6 +103,7 @@ pairwise_kernel(int64_t n_rows, const float *__restrict__ rxg, const float *__re
 
     auto evaluate = [&](uint32_t ent) {
         const int rl = (int)(ent >> 16), cl = (int)(ent & 0xFFFFu);
+        DGAL_ASSERT(rl < nrows && cl < ncols);
         const float *px = S.rx + rl * K, *py = S.ry + rl * K;
         const float *qx = S.cx + cl * K, *qy = S.cy + cl * K;
         const float ox = px[0], oy = py[0];
@@ -165,6 +166,7 @@ pairwise_kernel(int64_t n_rows, const float *__restrict__ rxg, const float *__re
             while (cand) {
                 const int bit = __ffs(cand) - 1;
                 cand &= cand - 1;
+                DGAL_ASSERT(at < kQueue);
                 queue[at++] = ((uint32_t)(warp * kRowsPerWarp + (bit >> 2)) << 16) | (uint32_t)(cb + (bit & 3));
             }
             qn += __shfl_sync(kFull, incl, 31);

@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(kThreads) pw_scatter(int64_t m, Workspace w)
     if (c >= m) return;
     const int id = w.cell_of[c];
     const int pos = w.start[id + 1] + atomicAdd(w.fill + id, 1);
+    DGAL_ASSERT(id >= 0 && id < kGridMaxCells && pos >= 0 && pos < m);
     w.sorted[pos] = (int32_t)c;
     const float4 q = w.circ[c];
     w.csorted[pos] = make_float4(q.x, q.y, q.z, __int_as_float((int)c));
@@ -284,6 +285,7 @@ pw_candidates(int64_t n_rows, const float *__restrict__ rx, const float *__restr
             P.x[k] = __fsub_rn(P.x[k], ox); P.y[k] = __fsub_rn(P.y[k], oy);
             Q.x[k] = __fsub_rn(Q.x[k], ox); Q.y[k] = __fsub_rn(Q.y[k], oy);
         }
+        DGAL_ASSERT(rr >= 0 && rr < n_rows && c >= 0 && c < m);
         const float v = iou_fwd<K, false>(P, Q).iou;
         if (iou && v != 0.f) iou[rr * m + c] = v;
         const int64_t grow = row_offset + rr;
@@ -315,6 +317,7 @@ pw_candidates(int64_t n_rows, const float *__restrict__ rx, const float *__restr
                 bool hit = false;
                 int32_t c = 0;
                 if (pos < hi) {
+                    DGAL_ASSERT(pos >= 0 && pos < m);
                     const float4 q = w.csorted[pos];
                     const float dx = q.x - rc.x, dy = q.y - rc.y, rs = q.z + rc.z;
                     hit = dx * dx + dy * dy < rs * rs;
@@ -323,6 +326,7 @@ pw_candidates(int64_t n_rows, const float *__restrict__ rx, const float *__restr
                 const unsigned bal = __ballot_sync(kFull, hit);
                 if (hit) {
                     const int at = qn + __popc(bal & ((1u << lane) - 1u));
+                    DGAL_ASSERT(at < kQ && c >= 0 && c < m);
                     qrow[wp][at] = r;
                     qcol[wp][at] = c;
                 }
