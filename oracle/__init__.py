@@ -55,6 +55,9 @@ def lib():
         L.oracle_nms_scan_mask.argtypes = [_I64, _I64, _P, _P]
         L.oracle_sh_intersect.argtypes = [ctypes.c_int, _I64, _P, _P, _P, _P, _P, _P, _P]
         L.oracle_margin.argtypes = [ctypes.c_int, _I64, _P, _P, _P, _P, _P, _P, ctypes.c_int]
+        L.oracle_box_iou_paired.argtypes = [ctypes.c_int, _I64, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int]
+        L.oracle_box_corners.argtypes = [_I64, _P, _P, _P]
+        L.oracle_box_corners_vjp.argtypes = [_I64, _P, _P, _P, _P]
         L.oracle_max_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -213,3 +216,44 @@ MARGIN_SIN = 1e-2
 def margin_ok(p1, p2, K=None, nthreads=0):
     d, s = margin(p1, p2, K, nthreads)
     return (d >= MARGIN_DIST) & (s >= MARGIN_SIN)
+
+
+# ---------------------------------------------------------------------------
+# rotated boxes: rows (cx, cy, w, h, theta) or (cx, cy, cz, w, h, d, theta)
+# ---------------------------------------------------------------------------
+def box_iou_paired(b1, b2, grad=None, nthreads=0):
+    """-> dict(iou, nx, xflags[n, 8], gb1, gb2 (if grad))"""
+    b1, b2 = _d(b1), _d(b2)
+    n, npar = b1.shape
+    dims = 3 if npar == 7 else 2
+    iou = np.empty(n, np.float64)
+    nx = np.empty(n, np.uint8)
+    xf = np.empty((n, 8), np.uint8)
+    g = None if grad is None else _d(grad).reshape(-1)
+    gb1 = np.empty_like(b1) if g is not None else None
+    gb2 = np.empty_like(b2) if g is not None else None
+    assert lib().oracle_box_iou_paired(dims, n, _ptr(b1), _ptr(b2), _ptr(iou), _ptr(nx), _ptr(xf), _ptr(g),
+                                       _ptr(gb1), _ptr(gb2), nthreads) == 0
+    out = dict(iou=iou, nx=nx, xflags=xf)
+    if g is not None:
+        out.update(gb1=gb1, gb2=gb2)
+    return out
+
+
+def box_corners(b):
+    """(n, 5) 2D box params -> (x, y) each (n, 4) float64."""
+    b = _d(b)
+    n = b.shape[0]
+    x = np.empty(n * 4, np.float64)
+    y = np.empty(n * 4, np.float64)
+    assert lib().oracle_box_corners(n, _ptr(b), _ptr(x), _ptr(y)) == 0
+    return x.reshape(n, 4), y.reshape(n, 4)
+
+
+def box_corners_vjp(b, gx, gy):
+    """box_to_polygon_grad: (n, 5) params, (n, 4) corner cotangents -> (n, 5)."""
+    b, gx, gy = _d(b), _d(gx), _d(gy)
+    n = b.shape[0]
+    out = np.empty((n, 5), np.float64)
+    assert lib().oracle_box_corners_vjp(n, _ptr(b), _ptr(gx), _ptr(gy), _ptr(out)) == 0
+    return out

@@ -336,38 +336,30 @@ static vec2 line_cross(vec2 P, vec2 Q, vec2 R, vec2 S)
     return vadd(P, vscale(e, t));
 }
 
-static void iou_grad_pair(int K, const vec2 *P, const vec2 *Q, double g,
-                          vec2 *g1, vec2 *g2)
+/*
+ * Vertex gradients of  ci * A(p1 ∩ p2) + cu1 * A(p1) + cu2 * A(p2)  (the A_i, A_1,
+ * A_2 paths of S:303): area_grad of p1 and p2 plus the area_grad of the
+ * intersection routed by flag through the crossing VJP.
+ */
+static void area_paths_grad(int K, const vec2 *P, const vec2 *Q, const isect_t *I, double ci, double cu1,
+                            double cu2, vec2 *g1, vec2 *g2)
 {
-    for (int k = 0; k < K; ++k) { g1[k] = v2(0.0, 0.0); g2[k] = v2(0.0, 0.0); }
-    isect_t I;
-    double A1, A2;
-    (void)iou_pair(K, P, Q, &I, &A1, &A2);
-    double Ai = I.area, Au = A1 + A2 - Ai;
-    if (I.n == 0 || !(Au > 0.0)) return;                 /* zero subgradient, S:303 */
-
-    /* dIoU/dAi = (Au + Ai)/Au^2, dIoU/dA1 = dIoU/dA2 = -Ai/Au^2 (S:303) */
-    double ci = g * (Au + Ai) / (Au * Au);
-    double cu = -g * Ai / (Au * Au);
-
-    /* A1, A2 paths: area_grad of p1 and p2 */
     for (int k = 0; k < K; ++k) {
-        g1[k] = vadd(g1[k], vscale(area_grad_at(P, K, k), cu));
-        g2[k] = vadd(g2[k], vscale(area_grad_at(Q, K, k), cu));
+        g1[k] = vscale(area_grad_at(P, K, k), cu1);
+        g2[k] = vscale(area_grad_at(Q, K, k), cu2);
     }
-    /* Ai path: area_grad of the intersection routed by flag;
-     * vertices are rebuilt from the flags, ascending order. */
+    /* vertices rebuilt from the flags, ascending order */
     vec2 X[OR_MAXC];
-    for (int c = 0; c < I.n; ++c) {
-        uint8_t b = I.flag[c];
+    for (int c = 0; c < I->n; ++c) {
+        uint8_t b = I->flag[c];
         int tag = b >> 6, i = (b >> 3) & 7, j = b & 7;
         if (tag == 1) X[c] = P[j];
         else if (tag == 2) X[c] = Q[j];
         else X[c] = line_cross(P[i], P[(i + 1) % K], Q[j], Q[(j + 1) % K]);
     }
-    for (int c = 0; c < I.n; ++c) {
-        vec2 G = vscale(area_grad_at(X, I.n, c), ci);
-        uint8_t b = I.flag[c];
+    for (int c = 0; c < I->n; ++c) {
+        vec2 G = vscale(area_grad_at(X, I->n, c), ci);
+        uint8_t b = I->flag[c];
         int tag = b >> 6, i = (b >> 3) & 7, j = b & 7;
         if (tag == 1) {
             g1[j] = vadd(g1[j], G);
@@ -382,6 +374,22 @@ static void iou_grad_pair(int K, const vec2 *P, const vec2 *Q, double g,
             g2[(j + 1) % K] = vadd(g2[(j + 1) % K], gS);
         }
     }
+}
+
+static void iou_grad_pair(int K, const vec2 *P, const vec2 *Q, double g,
+                          vec2 *g1, vec2 *g2)
+{
+    for (int k = 0; k < K; ++k) { g1[k] = v2(0.0, 0.0); g2[k] = v2(0.0, 0.0); }
+    isect_t I;
+    double A1, A2;
+    (void)iou_pair(K, P, Q, &I, &A1, &A2);
+    double Ai = I.area, Au = A1 + A2 - Ai;
+    if (I.n == 0 || !(Au > 0.0)) return;                 /* zero subgradient, S:303 */
+
+    /* dIoU/dAi = (Au + Ai)/Au^2, dIoU/dA1 = dIoU/dA2 = -Ai/Au^2 (S:303) */
+    double ci = g * (Au + Ai) / (Au * Au);
+    double cu = -g * Ai / (Au * Au);
+    area_paths_grad(K, P, Q, &I, ci, cu, cu, g1, g2);
 }
 
 /*
@@ -631,6 +639,152 @@ int oracle_margin(int K, int64_t n, const double *x1, const double *y1,
         }
         dist[k] = dmin / sqrt(fmin(A1, A2));
         sinmin[k] = smin;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Rotated boxes: 2D (cx, cy, w, h, theta) and yaw-only 3D (cx, cy, cz, w, h, d,
+ * theta) — SURVEY §8(f) f1 / f3, SPEC metrics-boxes             */
+/* ------------------------------------------------------------------------ */
+/* box_to_polygon: corners c + R(theta)(+-w/2, +-h/2), CCW, starting
+ * at (-w/2, -h/2). */
+static const double kBoxSx[4] = {-0.5, 0.5, 0.5, -0.5};
+static const double kBoxSy[4] = {-0.5, -0.5, 0.5, 0.5};
+
+static void box_corners(double cx, double cy, double w, double h, double th, vec2 *P)
+{
+    double c = cos(th), s = sin(th);
+    for (int k = 0; k < 4; ++k) {
+        double lx = kBoxSx[k] * w, ly = kBoxSy[k] * h;
+        P[k] = v2(cx + c * lx - s * ly, cy + s * lx + c * ly);
+    }
+}
+
+/* box_to_polygon_grad: VJP of the corner map.  out[0..4] += dL/d(cx,
+ * cy, w, h, theta) for corner cotangents G[0..3]. */
+static void box_corners_vjp(double w, double h, double th, const vec2 *G, double *out)
+{
+    double c = cos(th), s = sin(th);
+    for (int k = 0; k < 4; ++k) {
+        double lx = kBoxSx[k] * w, ly = kBoxSy[k] * h;
+        out[0] += G[k].x;                                           /* d/dcx */
+        out[1] += G[k].y;                                           /* d/dcy */
+        out[2] += G[k].x * c * kBoxSx[k] + G[k].y * s * kBoxSx[k];  /* d/dw  */
+        out[3] += -G[k].x * s * kBoxSy[k] + G[k].y * c * kBoxSy[k]; /* d/dh  */
+        /* d/dtheta: d(R u)/dtheta = (-s ux - c uy, c ux - s uy) */
+        out[4] += G[k].x * (-s * lx - c * ly) + G[k].y * (c * lx - s * ly);
+    }
+}
+
+/* overlap of the vertical extents [cz - d/2, cz + d/2] */
+static double z_overlap(double z1, double d1, double z2, double d2, int *top1, int *bot1)
+{
+    double t1 = z1 + 0.5 * d1, t2 = z2 + 0.5 * d2, b1 = z1 - 0.5 * d1, b2 = z2 - 0.5 * d2;
+    *top1 = t1 <= t2;
+    *bot1 = b1 >= b2;
+    double dz = fmin(t1, t2) - fmax(b1, b2);
+    return dz > 0.0 ? dz : 0.0;
+}
+
+/*
+ * One box pair.  dims = 2: boxes are (cx, cy, w, h, theta); dims = 3: (cx, cy, cz,
+ * w, h, d, theta) and IoU = V_i / (V_1 + V_2 - V_i), V_i = A_i dz.
+ * Fills iou, the BEV intersection I, and (if g1/g2) dL/d(box params) for dL/dIoU = g.
+ */
+static double box_pair(int dims, const double *b1, const double *b2, isect_t *I, double g,
+                       double *gb1, double *gb2)
+{
+    const int np = dims == 3 ? 7 : 5;
+    double w1, h1, th1, w2, h2, th2, z1 = 0, d1 = 1, z2 = 0, d2 = 1;
+    if (dims == 3) {
+        z1 = b1[2]; w1 = b1[3]; h1 = b1[4]; d1 = b1[5]; th1 = b1[6];
+        z2 = b2[2]; w2 = b2[3]; h2 = b2[4]; d2 = b2[5]; th2 = b2[6];
+    } else {
+        w1 = b1[2]; h1 = b1[3]; th1 = b1[4];
+        w2 = b2[2]; h2 = b2[3]; th2 = b2[4];
+    }
+    vec2 P[4], Q[4];
+    box_corners(b1[0], b1[1], w1, h1, th1, P);
+    box_corners(b2[0], b2[1], w2, h2, th2, Q);
+    double A1, A2;
+    (void)iou_pair(4, P, Q, I, &A1, &A2);
+    int top1 = 1, bot1 = 1;
+    double dz = dims == 3 ? z_overlap(z1, d1, z2, d2, &top1, &bot1) : 1.0;
+    double V1 = A1 * d1, V2 = A2 * d2, Vi = I->area * dz, Vu = V1 + V2 - Vi;
+    if (gb1) for (int p = 0; p < np; ++p) { gb1[p] = 0.0; gb2[p] = 0.0; }
+    if (I->n == 0 || !(Vi > 0.0) || !(Vu > 0.0)) return 0.0;
+    double iou = Vi / Vu;
+    if (!gb1) return iou;
+    /* dIoU/dVi = (Vu + Vi)/Vu^2, dIoU/dV1 = dIoU/dV2 = -Vi/Vu^2 (S:303 with V for A) */
+    double cVi = g * (Vu + Vi) / (Vu * Vu), cVu = -g * Vi / (Vu * Vu);
+    vec2 g1[4], g2[4];
+    area_paths_grad(4, P, Q, I, cVi * dz, cVu * d1, cVu * d2, g1, g2);
+    double o1[5] = {0, 0, 0, 0, 0}, o2[5] = {0, 0, 0, 0, 0};
+    box_corners_vjp(w1, h1, th1, g1, o1);
+    box_corners_vjp(w2, h2, th2, g2, o2);
+    if (dims == 3) {
+        /* product rule through dz (+-1/0 subgradient of min/max) and d */
+        double gdz = cVi * I->area;
+        gb1[0] = o1[0]; gb1[1] = o1[1]; gb1[3] = o1[2]; gb1[4] = o1[3]; gb1[6] = o1[4];
+        gb2[0] = o2[0]; gb2[1] = o2[1]; gb2[3] = o2[2]; gb2[4] = o2[3]; gb2[6] = o2[4];
+        gb1[2] = gdz * ((top1 ? 1.0 : 0.0) - (bot1 ? 1.0 : 0.0));
+        gb2[2] = gdz * ((top1 ? 0.0 : 1.0) - (bot1 ? 0.0 : 1.0));
+        gb1[5] = cVu * A1 + gdz * 0.5 * ((top1 ? 1.0 : 0.0) + (bot1 ? 1.0 : 0.0));
+        gb2[5] = cVu * A2 + gdz * 0.5 * ((top1 ? 0.0 : 1.0) + (bot1 ? 0.0 : 1.0));
+    } else {
+        for (int p = 0; p < 5; ++p) { gb1[p] = o1[p]; gb2[p] = o2[p]; }
+    }
+    return iou;
+}
+
+/*
+ * oracle_box_iou_paired: boxes as n x (5 | 7) row-major doubles.  Outputs iou[n],
+ * nx[n], xflags[n*8] (of the BEV intersection, as for Poly2<float,4>), and — if
+ * grad_iou != NULL — dL/d(box params) in gb1, gb2 (same shape as the boxes).
+ */
+int oracle_box_iou_paired(int dims, int64_t n, const double *b1, const double *b2, double *iou,
+                          uint8_t *nx, uint8_t *xflags, const double *grad_iou, double *gb1, double *gb2,
+                          int nthreads)
+{
+    if ((dims != 2 && dims != 3) || n < 0) return 1;
+    const int np = dims == 3 ? 7 : 5;
+    int nt = resolve_threads(nthreads);
+#pragma omp parallel for schedule(static) num_threads(nt)
+    for (int64_t k = 0; k < n; ++k) {
+        isect_t I;
+        double g = grad_iou ? grad_iou[k] : 0.0;
+        double v = box_pair(dims, b1 + k * np, b2 + k * np, &I, g, grad_iou ? gb1 + k * np : NULL,
+                            grad_iou ? gb2 + k * np : NULL);
+        if (iou) iou[k] = v;
+        int nv = v > 0.0 ? (I.n < 8 ? I.n : 8) : 0;
+        if (nx) nx[k] = (uint8_t)nv;
+        if (xflags)
+            for (int c = 0; c < 8; ++c) xflags[k * 8 + c] = c < nv ? I.flag[c] : 0;
+    }
+    return 0;
+}
+
+/* Corners of n boxes (2D params, n x 5) as SoA x[n*4], y[n*4] (tests: margin filter). */
+int oracle_box_corners(int64_t n, const double *b, double *x, double *y)
+{
+    for (int64_t k = 0; k < n; ++k) {
+        vec2 P[4];
+        box_corners(b[k * 5 + 0], b[k * 5 + 1], b[k * 5 + 2], b[k * 5 + 3], b[k * 5 + 4], P);
+        for (int v = 0; v < 4; ++v) { x[k * 4 + v] = P[v].x; y[k * 4 + v] = P[v].y; }
+    }
+    return 0;
+}
+
+/* box_to_polygon_grad for n 2D boxes (n x 5) with corner cotangents gx, gy (n x 4). */
+int oracle_box_corners_vjp(int64_t n, const double *b, const double *gx, const double *gy, double *out)
+{
+    for (int64_t k = 0; k < n; ++k) {
+        vec2 G[4];
+        for (int v = 0; v < 4; ++v) G[v] = v2(gx[k * 4 + v], gy[k * 4 + v]);
+        double o[5] = {0, 0, 0, 0, 0};
+        box_corners_vjp(b[k * 5 + 2], b[k * 5 + 3], b[k * 5 + 4], G, o);
+        for (int p = 0; p < 5; ++p) out[k * 5 + p] = o[p];
     }
     return 0;
 }

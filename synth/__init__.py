@@ -9,7 +9,9 @@ from .generators import (  # noqa: F401
     Polys,
     PairBatch,
     Scene,
+    BoxPairBatch,
     boxes_to_polys,
+    gen_box_pairs,
     gen_cfg1_pairs,
     gen_cfg2_scene,
     gen_cfg3_pairs,

@@ -210,6 +210,79 @@ def gen_cfg3_pairs(n: int = 1 << 24, seed: int | None = None) -> PairBatch:
                      a[10].astype(np.float32))
 
 
+# ----------------------------------------------------------------------------
+# rotated-box parameter batches: the cfg3 distribution
+# kept as box parameters instead of corners
+# ----------------------------------------------------------------------------
+# KITTI vertical extent (mean, sd) per class and the LiDAR-frame centre height
+_KITTI_D = np.array([(1.53, 0.14), (1.76, 0.11), (1.74, 0.09)])
+_KITTI_CZ = (-1.0, 0.4)
+
+
+@dataclass
+class BoxPairBatch:
+    """b1 = prediction, b2 = ground truth, float32 parameter planes [P, n]:
+    P = 5 (cx, cy, w, h, theta) or P = 7 (cx, cy, cz, w, h, d, theta) (S:80)."""
+    b1: np.ndarray
+    b2: np.ndarray
+    grad: np.ndarray  # float32 [n], dL/dIoU ~ U(-1, 1)
+
+    @property
+    def n(self) -> int:
+        return self.b1.shape[1]
+
+    @property
+    def dims(self) -> int:
+        return 3 if self.b1.shape[0] == 7 else 2
+
+    def take(self, idx) -> "BoxPairBatch":
+        idx = np.asarray(idx)
+        return BoxPairBatch(np.ascontiguousarray(self.b1[:, idx]), np.ascontiguousarray(self.b2[:, idx]),
+                            np.ascontiguousarray(self.grad[idx]))
+
+    def rows64(self):
+        """(n, P) float64 rows of the float32 parameters (exact conversion), oracle layout."""
+        return self.b1.T.astype(np.float64), self.b2.T.astype(np.float64)
+
+
+def _box_chunk(rng, m, dims):
+    cls = rng.choice(len(_KITTI), size=m, p=_KITTI[:, 0])
+    row = _KITTI[cls]
+    length = np.maximum(rng.normal(row[:, 1], row[:, 2]), 0.25 * row[:, 1])
+    width = np.maximum(rng.normal(row[:, 3], row[:, 4]), 0.25 * row[:, 3])
+    cx = rng.uniform(0.0, 70.4, size=m)
+    cy = rng.uniform(-40.0, 40.0, size=m)
+    th = rng.uniform(-math.pi, math.pi, size=m)
+    gt = (cx, cy, length, width, th)
+    good = _jitter(rng, *gt, 0.1, 0.1, 0.1)
+    poor = _jitter(rng, *gt, 0.5, 0.3, math.pi / 2)
+    is_poor = rng.uniform(size=m) < 0.10
+    pred = tuple(np.where(is_poor, p, g) for g, p in zip(good, poor))
+    g = rng.uniform(-1, 1, size=m)
+    if dims == 2:
+        return (*pred, *gt, g)
+    rd = _KITTI_D[cls]
+    d = np.maximum(rng.normal(rd[:, 0], rd[:, 1]), 0.25 * rd[:, 0])
+    cz = rng.normal(_KITTI_CZ[0], _KITTI_CZ[1], size=m)
+    s_c = np.where(is_poor, 0.5, 0.1)
+    s_d = np.where(is_poor, 0.3, 0.1)
+    pz = cz + rng.normal(0, 1, size=m) * s_c * d
+    pd = d * np.exp(rng.normal(0, 1, size=m) * s_d)
+    pcx, pcy, pl, pw, pt = pred
+    return (pcx, pcy, pz, pl, pw, pd, pt, cx, cy, cz, length, width, d, th, g)
+
+
+def gen_box_pairs(n: int = 1 << 24, dims: int = 2, seed: int | None = None) -> BoxPairBatch:
+    """cfg3's KITTI matched/poor prediction-target distribution as box parameters
+    (dims=2: RotatedBox2, dims=3: yaw-only Box3 with KITTI heights)."""
+    seed = seed_for(3) + 101 * dims if seed is None else seed
+    a = _chunked(n, seed, lambda rng, m: _box_chunk(rng, m, dims))
+    P = 5 if dims == 2 else 7
+    b1 = np.ascontiguousarray(np.stack(a[0:P]).astype(np.float32))
+    b2 = np.ascontiguousarray(np.stack(a[P:2 * P]).astype(np.float32))
+    return BoxPairBatch(b1, b2, a[2 * P].astype(np.float32))
+
+
 def _scene_from_objects(rng, objs, per_object, thr):
     cx, cy, length, width, th = (np.repeat(a, per_object) for a in objs)
     props = _jitter(rng, cx, cy, length, width, th, 0.2, 0.15, 0.2, flip=0.10)

@@ -62,3 +62,33 @@ def margin_batch(cfg: int, n: int, oversample: float = 1.25):
     """cfg (1, 3 or 4) pairs, margin-filtered, prefix-stable."""
     raw = synth.gen_config(cfg, int(n * oversample) + 64)
     return margin_filter(raw, n)
+
+
+def footprint(rows):
+    """(n, 5|7) box rows -> (n, 5) BEV rows (cx, cy, w, h, theta)."""
+    rows = np.asarray(rows, np.float64)
+    return rows if rows.shape[1] == 5 else rows[:, [0, 1, 3, 4, 6]]
+
+
+def box_margin_ok(rows1, rows2, zmargin=1e-3):
+    """R13 margin filter on the BEV corners (oracle, double) and, for 3D boxes, a
+    gap of the z extents away from ties (so min/max subgradients are unambiguous)."""
+    x1, y1 = oracle.box_corners(footprint(rows1))
+    x2, y2 = oracle.box_corners(footprint(rows2))
+    ok = oracle.margin_ok((x1, y1), (x2, y2))
+    if np.asarray(rows1).shape[1] == 7:
+        r1, r2 = np.asarray(rows1, np.float64), np.asarray(rows2, np.float64)
+        t1, t2 = r1[:, 2] + r1[:, 5] / 2, r2[:, 2] + r2[:, 5] / 2
+        b1, b2 = r1[:, 2] - r1[:, 5] / 2, r2[:, 2] - r2[:, 5] / 2
+        s = np.maximum(r1[:, 5], r2[:, 5])
+        ok &= (np.abs(t1 - t2) > zmargin * s) & (np.abs(b1 - b2) > zmargin * s)
+        ok &= np.abs(np.minimum(t1, t2) - np.maximum(b1, b2)) > zmargin * s
+    return ok
+
+
+def box_margin_batch(dims, n, seed=None):
+    """First n margin-passing pairs of the box generator (raw draw is 2n)."""
+    raw = synth.gen_box_pairs(2 * n, dims, seed=seed)
+    r1, r2 = raw.rows64()
+    idx = np.nonzero(box_margin_ok(r1, r2))[0][:n]
+    return raw.take(idx)
