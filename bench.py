@@ -9,7 +9,9 @@ GPU): weak scaling, each rank owns its own 2^24-pair shard, no collective on the
 data path; elapsed = max over ranks of the CUDA-event time.
 
 Secondary lines in the same JSON object ("secondary"): cfg4 (paired K=8
-octagons, 2^22 pairs per GPU, weak) and cfg5 (pairwise 100k x 100k IoU matrix +
+octagons, 2^22 pairs per GPU, weak), cfg3_fused (fused loss kernel, f2),
+box2d / box3d (rotated-box front end f1 / yaw-only 3D f3 on the cfg3 KITTI
+distribution as box parameters, 2^24 pairs per GPU, weak) and cfg5 (pairwise 100k x 100k IoU matrix +
 NMS mask + greedy keep, rows sharded over the GPUs: strong scaling).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
@@ -328,6 +330,71 @@ def bench_fused(ctx, n, steps, warmup, peak):
                          "frac": n * nbytes / (ms * 1e-3) / 1e9 / peak, "algorithmic_bytes_per_pair": nbytes}}
 
 
+def bench_box(ctx, dims, n, steps, warmup, peak):
+    """SURVEY §8(f) f1 (dims 2) / f3 (dims 3): the cfg3 KITTI distribution as box
+    parameters, [P, n] planes; split fwd + bwd (CUDA events per kernel) and the
+    fused loss kernel.  Algorithmic bytes: parameters in, IoU/nx/xflags out (fwd);
+    parameters + grad + nx + xflags in, parameter gradients out (bwd)."""
+    import paper_2011_11134_b200 as dgal
+    import synth
+    torch = ctx.torch
+    b = synth.gen_box_pairs(n, dims, seed=synth.seed_for(3, ctx.rank) + 101 * dims)
+    P = b.b1.shape[0]
+    B1, B2 = torch.from_numpy(b.b1).to(ctx.dev), torch.from_numpy(b.b2).to(ctx.dev)
+    g = torch.full((n,), -1.0 / n, dtype=torch.float32, device=ctx.dev)
+    fo = (torch.empty(n, dtype=torch.float32, device=ctx.dev), torch.empty(n, dtype=torch.uint8, device=ctx.dev),
+          torch.empty((n, 8), dtype=torch.uint8, device=ctx.dev))
+    go = (torch.empty_like(B1), torch.empty_like(B2))
+    uo = (fo[0], torch.empty_like(B1), torch.empty_like(B2))
+    for _ in range(warmup):
+        dgal.box_iou_paired_fwd(B1, B2, out=fo)
+        dgal.box_iou_paired_bwd(B1, B2, g, fo[1], fo[2], out=go)
+        dgal.box_iou_paired_fused(B1, B2, scale=-1.0 / n, out=uo)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(ctx.dev)
+    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    ev = [(E(), E(), E()) for _ in range(steps)]
+    ctx.barrier()
+    a, z = E(), E()
+    a.record(stream)
+    for e0, e1, e2 in ev:
+        e0.record(stream)
+        dgal.box_iou_paired_fwd(B1, B2, out=fo)
+        e1.record(stream)
+        dgal.box_iou_paired_bwd(B1, B2, g, fo[1], fo[2], out=go)
+        e2.record(stream)
+    z.record(stream)
+    torch.cuda.synchronize()
+    ms = ctx.max_over_ranks(a.elapsed_time(z)) / steps
+    fwd_ms = sum(x.elapsed_time(y) for x, y, _ in ev) / steps
+    bwd_ms = sum(y.elapsed_time(w) for _, y, w in ev) / steps
+    fa, fz = E(), E()
+    fa.record(stream)
+    for _ in range(steps):
+        dgal.box_iou_paired_fused(B1, B2, scale=-1.0 / n, out=uo)
+    fz.record(stream)
+    torch.cuda.synchronize()
+    ums = ctx.max_over_ranks(fa.elapsed_time(fz)) / steps
+    fb = 2 * 4 * P + 4 + 1 + 8
+    bb = 2 * 4 * P + 4 + 1 + 8 + 2 * 4 * P
+    ub = 2 * 4 * P + 4 + 2 * 4 * P
+    gbs = lambda nb, t: n * nb / (t * 1e-3) / 1e9  # noqa: E731
+    return {"workload": f"2^{n.bit_length() - 1} KITTI {'3D yaw-only' if dims == 3 else '2D rotated'} box pairs, "
+                        f"[{P}, n] planes (SURVEY {'f3' if dims == 3 else 'f1'})",
+            "scaling": "weak", "pairs_per_s": n * ctx.world / (ms * 1e-3), "ms_per_step": ms,
+            "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
+            "fwd_roofline": {"bound": "hbm", "kernel": f"box_fwd_kernel<{dims}>", "achieved": gbs(fb, fwd_ms),
+                             "peak": peak, "unit": "GB/s", "frac": gbs(fb, fwd_ms) / peak,
+                             "algorithmic_bytes_per_pair": fb},
+            "bwd_roofline": {"bound": "hbm", "kernel": f"box_bwd_kernel<{dims}>", "achieved": gbs(bb, bwd_ms),
+                             "peak": peak, "unit": "GB/s", "frac": gbs(bb, bwd_ms) / peak,
+                             "algorithmic_bytes_per_pair": bb},
+            "fused": {"pairs_per_s": n * ctx.world / (ums * 1e-3), "ms_per_step": ums,
+                      "roofline": {"bound": "hbm", "kernel": f"box_fused_kernel<{dims}>", "achieved": gbs(ub, ums),
+                                   "peak": peak, "unit": "GB/s", "frac": gbs(ub, ums) / peak,
+                                   "algorithmic_bytes_per_pair": ub}}}
+
+
 def bench_cfg5(ctx, steps, warmup, peak):
     """Pairwise 100k x 100k IoU matrix + NMS mask/lists + greedy keep; rows sharded."""
     import paper_2011_11134_b200 as dgal
@@ -459,6 +526,8 @@ def main(argv=None):
         del planes4, g4
         torch.cuda.empty_cache()
         secondary["cfg3_fused"] = bench_fused(ctx, n, max(10, args.steps // 4), args.warmup, peak)
+        secondary["box2d"] = bench_box(ctx, 2, n, max(10, args.steps // 4), args.warmup, peak)
+        secondary["box3d"] = bench_box(ctx, 3, n, max(10, args.steps // 4), args.warmup, peak)
         secondary["cfg5"] = bench_cfg5(ctx, steps=5, warmup=2, peak=peak)
 
     if ctx.dist:

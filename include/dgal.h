@@ -105,6 +105,50 @@ dgal_status dgal_iou_paired_fused(int K, int64_t n,
                                   dgal_stream stream);
 
 /*
+ * Rotated-box front end (SPEC metrics-boxes S:336-418;
+ * P:73, "2D IoU Loss and 3D IoU Loss for rotated bounding boxes").
+ * Boxes are given as parameters and converted to Poly2<float,4> inside the
+ * kernels by box_to_polygon: corners c + R(theta)(+-w/2, +-h/2), CCW,
+ * starting at (-w/2, -h/2) — so nx / xflags are those of dgal_iou_paired_fwd
+ * on these corners (K = 4, 8 flag bytes per pair).
+ *   dims 2: RotatedBox2 (cx, cy, w, h, theta)          P = 5 parameters
+ *   dims 3: yaw-only Box3 (cx, cy, cz, w, h, d, theta)  P = 7 parameters;
+ *           IoU = V_i / (V_1 + V_2 - V_i), V_i = A_i dz, dz = overlap of the
+ *           z extents [cz - d/2, cz + d/2]; dz == 0 -> IoU 0, nx 0.
+ * theta is in radians, unbounded; w, h, d > 0 (inputs are trusted).
+ * layout DGAL_BOX_PLANES: parameter p of box k at b[p * n + k] (a [P, n] tensor,
+ *        coalesced: the fast layout); DGAL_BOX_ROWS: at b[k * P + p] ([n, P]).
+ * Gradients use the layout of the inputs and are OVERWRITTEN; they are the
+ * chain of the polygon backward with box_to_polygon_grad and, in 3D,
+ * the product rule through dz (+-1/0 subgradient of min/max; ties -> box 1)
+ * and V = A d.  Pointers: 4-byte aligned floats; xflags 8-byte aligned.
+ * Errors: dims not 2/3 or bad layout -> DGAL_ERR_INVALID_ARG; the rest as above.
+ */
+typedef enum { DGAL_BOX_PLANES = 0, DGAL_BOX_ROWS = 1 } dgal_box_layout;
+
+dgal_status dgal_box_iou_paired_fwd(int dims, int layout, int64_t n,
+                                    const float *b1, const float *b2,
+                                    float *iou /*[n]*/, uint8_t *nx /*[n]*/,
+                                    uint8_t *xflags /*[n * 8]*/,
+                                    dgal_stream stream);
+
+dgal_status dgal_box_iou_paired_bwd(int dims, int layout, int64_t n,
+                                    const float *b1, const float *b2,
+                                    const float *grad_iou /*[n]*/,
+                                    const uint8_t *nx, const uint8_t *xflags,
+                                    float *grad_b1, float *grad_b2 /*like b1, b2*/,
+                                    dgal_stream stream);
+
+/* fused forward + backward (f2 on boxes): dL/dIoU = grad_iou[k], or grad_scale
+ * when grad_iou == NULL; iou nullable. */
+dgal_status dgal_box_iou_paired_fused(int dims, int layout, int64_t n,
+                                      const float *b1, const float *b2,
+                                      const float *grad_iou, float grad_scale,
+                                      float *iou,
+                                      float *grad_b1, float *grad_b2,
+                                      dgal_stream stream);
+
+/*
  * Pairwise IoU of a row block against all columns ("cartesian";
  * north_star "full N x M pairwise matrices (detection/NMS)"), forward only.
  * Rows play p1, columns p2 (R4).  Row r has global index row_offset + r; column c

@@ -129,19 +129,30 @@ static void intersect_by_definition(int K, const vec2 *P, const vec2 *Q, isect_t
         scale = fmax(scale, fmax(fabs(Q[k].x), fabs(Q[k].y)));
     }
     const double tol = 1e-9 * scale;
+    /* on-boundary tolerance: absorbs the double rounding of coordinates (~1e-16
+     * scale), far below any float32 input resolution (~1e-7 scale) */
+    const double ton = 1e-12 * scale;
 
-    /* (1a) p1 vertices inside-or-on p2 (boundary-inclusive, R5) */
+    /* (1a) p1 vertices inside-or-on p2 (boundary-inclusive, R5).  "On" is taken
+     * within a rounding tolerance (distance to the edge line >= -ton): a vertex
+     * that lies on the other polygon's edge in exact arithmetic (collinear edges,
+     * nested boxes) must not be lost to the rounding of its coordinates. */
     for (int i = 0; i < K; ++i) {
         int in = 1;
-        for (int j = 0; j < K; ++j)
-            if (side(Q[j], Q[(j + 1) % K], P[i]) < 0.0) { in = 0; break; }
+        for (int j = 0; j < K; ++j) {
+            vec2 f = vsub(Q[(j + 1) % K], Q[j]);
+            if (side(Q[j], Q[(j + 1) % K], P[i]) < -ton * sqrt(vdot(f, f))) { in = 0; break; }
+        }
         if (in) { cand[nc] = P[i]; cflag[nc] = (uint8_t)(0x40 | i); ++nc; }
     }
-    /* (1b) p2 vertices inside-or-on p1, unless coincident with an accepted point */
+    /* (1b) p2 vertices inside-or-on p1 (same rounding tolerance), unless coincident with
+     * an accepted point */
     for (int j = 0; j < K; ++j) {
         int in = 1;
-        for (int i = 0; i < K; ++i)
-            if (side(P[i], P[(i + 1) % K], Q[j]) < 0.0) { in = 0; break; }
+        for (int i = 0; i < K; ++i) {
+            vec2 e = vsub(P[(i + 1) % K], P[i]);
+            if (side(P[i], P[(i + 1) % K], Q[j]) < -ton * sqrt(vdot(e, e))) { in = 0; break; }
+        }
         if (!in) continue;
         int dup = 0;
         for (int c = 0; c < nc; ++c)

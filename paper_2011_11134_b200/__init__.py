@@ -19,7 +19,8 @@ import torch
 
 from ._lib import DgalError, call, lib  # noqa: F401
 
-__all__ = ["iou_paired_fwd", "iou_paired_bwd", "iou_paired_fused", "PolyIoULoss", "iou_pairwise", "pairwise_workspace", "nms_round", "nms_keep",
+__all__ = ["iou_paired_fwd", "iou_paired_bwd", "iou_paired_fused", "PolyIoULoss",
+           "box_iou_paired_fwd", "box_iou_paired_bwd", "box_iou_paired_fused", "BoxIoU", "BoxIoULoss", "iou_pairwise", "pairwise_workspace", "nms_round", "nms_keep",
            "nms", "PolyIoU", "DgalError", "build_info"]
 
 
@@ -122,6 +123,105 @@ class PolyIoULoss(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dl):
         return tuple(g * dl for g in ctx.saved_tensors)
+
+
+# ---------------------------------------------------------------------------
+# rotated boxes: dims 2 -> (cx, cy, w, h, theta), dims 3 ->
+# (cx, cy, cz, w, h, d, theta).  layout "planes": a [P, n] tensor (coalesced, the
+# fast layout); "rows": an [n, P] tensor.
+# ---------------------------------------------------------------------------
+_LAYOUT = {"planes": 0, "rows": 1}
+
+
+def _box_args(b1, b2, layout):
+    if layout not in _LAYOUT:
+        raise ValueError("layout must be 'planes' or 'rows'")
+    _plane(b1, "b1")
+    _plane(b2, "b2")
+    if b1.dim() != 2 or b1.shape != b2.shape:
+        raise ValueError("b1, b2 must be 2-D tensors of the same shape")
+    P, n = (b1.shape[0], b1.shape[1]) if layout == "planes" else (b1.shape[1], b1.shape[0])
+    if P not in (5, 7):
+        raise ValueError(f"{P} box parameters: expected 5 (2D) or 7 (3D) for layout {layout!r}")
+    return (3 if P == 7 else 2), _LAYOUT[layout], n
+
+
+def box_iou_paired_fwd(b1, b2, layout: str = "planes", out=None):
+    """IoU of n box pairs (dgal_box_iou_paired_fwd).  Returns (iou f32[n], nx u8[n],
+    xflags u8[n, 8]) — nx / xflags of the BEV corner polygons (K = 4)."""
+    dims, lay, n = _box_args(b1, b2, layout)
+    if out is None:
+        dev = b1.device
+        out = (torch.empty(n, dtype=torch.float32, device=dev), torch.empty(n, dtype=torch.uint8, device=dev),
+               torch.empty(n, 8, dtype=torch.uint8, device=dev))
+    iou, nx, xf = out
+    call("dgal_box_iou_paired_fwd", dims, lay, n, _ptr(b1), _ptr(b2), _ptr(iou), _ptr(nx), _ptr(xf),
+         _stream(b1.device))
+    return iou, nx, xf
+
+
+def box_iou_paired_bwd(b1, b2, grad_iou, nx, xflags, layout: str = "planes", out=None):
+    """dL/d(box parameters) from dL/dIoU through the recorded nx / xflags
+    (dgal_box_iou_paired_bwd).  Returns (grad_b1, grad_b2) shaped like b1, b2."""
+    dims, lay, n = _box_args(b1, b2, layout)
+    _plane(grad_iou, "grad_iou")
+    if out is None:
+        out = (torch.empty_like(b1), torch.empty_like(b2))
+    call("dgal_box_iou_paired_bwd", dims, lay, n, _ptr(b1), _ptr(b2), _ptr(grad_iou), _ptr(nx), _ptr(xflags),
+         _ptr(out[0]), _ptr(out[1]), _stream(b1.device))
+    return out
+
+
+def box_iou_paired_fused(b1, b2, grad=None, scale: float = 1.0, layout: str = "planes", out=None,
+                         want_iou: bool = True):
+    """Fused forward + backward on boxes (dgal_box_iou_paired_fused).  Returns
+    (iou | None, grad_b1, grad_b2)."""
+    dims, lay, n = _box_args(b1, b2, layout)
+    if grad is not None:
+        _plane(grad, "grad")
+    if out is None:
+        iou = torch.empty(n, dtype=torch.float32, device=b1.device) if want_iou else None
+        out = (iou, torch.empty_like(b1), torch.empty_like(b2))
+    iou, g1, g2 = out
+    call("dgal_box_iou_paired_fused", dims, lay, n, _ptr(b1), _ptr(b2), _ptr(grad), float(scale), _ptr(iou),
+         _ptr(g1), _ptr(g2), _stream(b1.device))
+    return iou, g1, g2
+
+
+class BoxIoU(torch.autograd.Function):
+    """Differentiable rotated-box IoU (2D or yaw-only 3D): forward =
+    dgal_box_iou_paired_fwd, backward = dgal_box_iou_paired_bwd (P:73, P:96)."""
+
+    @staticmethod
+    def forward(ctx, b1, b2, layout="planes"):
+        b1, b2 = b1.contiguous(), b2.contiguous()
+        iou, nx, xf = box_iou_paired_fwd(b1, b2, layout)
+        ctx.layout = layout
+        ctx.save_for_backward(b1, b2, nx, xf)
+        return iou
+
+    @staticmethod
+    def backward(ctx, g):
+        b1, b2, nx, xf = ctx.saved_tensors
+        g1, g2 = box_iou_paired_bwd(b1, b2, g.contiguous().float(), nx, xf, ctx.layout)
+        return g1, g2, None
+
+
+class BoxIoULoss(torch.autograd.Function):
+    """L = mean(1 - IoU) over box pairs in one fused kernel pass (dL/dIoU = -1/n)."""
+
+    @staticmethod
+    def forward(ctx, b1, b2, layout="planes"):
+        b1, b2 = b1.contiguous(), b2.contiguous()
+        n = b1.shape[1] if layout == "planes" else b1.shape[0]
+        iou, g1, g2 = box_iou_paired_fused(b1, b2, scale=-1.0 / max(n, 1), layout=layout)
+        ctx.save_for_backward(g1, g2)
+        return (1.0 - iou).mean()
+
+    @staticmethod
+    def backward(ctx, dl):
+        g1, g2 = ctx.saved_tensors
+        return g1 * dl, g2 * dl, None
 
 
 def pairwise_workspace(m: int, device=None) -> torch.Tensor:

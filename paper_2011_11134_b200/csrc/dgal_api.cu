@@ -70,6 +70,55 @@ dgal_status dgal_iou_paired_fused(int K, int64_t n, const float *x1, const float
                                                gy2, as_cuda(stream)));
 }
 
+namespace {
+inline dgal_status box_check(int dims, int layout, int64_t n, const float *b1, const float *b2)
+{
+    if (dims != 2 && dims != 3) return DGAL_ERR_INVALID_ARG;
+    if (layout != DGAL_BOX_PLANES && layout != DGAL_BOX_ROWS) return DGAL_ERR_INVALID_ARG;
+    if (n < 0) return DGAL_ERR_INVALID_ARG;
+    if (n > 0 && (!b1 || !b2)) return DGAL_ERR_INVALID_ARG;
+    if (n > 0 && (!aligned(b1, 4) || !aligned(b2, 4))) return DGAL_ERR_MISALIGNED;
+    return DGAL_OK;
+}
+}  // namespace
+
+dgal_status dgal_box_iou_paired_fwd(int dims, int layout, int64_t n, const float *b1, const float *b2, float *iou,
+                                    uint8_t *nx, uint8_t *xflags, dgal_stream stream)
+{
+    const dgal_status c = box_check(dims, layout, n, b1, b2);
+    if (c != DGAL_OK || n == 0) return c;
+    if (!iou || !nx || !xflags) return DGAL_ERR_INVALID_ARG;
+    if (!aligned(iou, 4) || !aligned(xflags, 8)) return DGAL_ERR_MISALIGNED;
+    return from_cuda(dgal::launch_box_fwd(dims, layout, n, b1, b2, iou, nx, xflags, as_cuda(stream)));
+}
+
+dgal_status dgal_box_iou_paired_bwd(int dims, int layout, int64_t n, const float *b1, const float *b2,
+                                    const float *grad_iou, const uint8_t *nx, const uint8_t *xflags, float *grad_b1,
+                                    float *grad_b2, dgal_stream stream)
+{
+    const dgal_status c = box_check(dims, layout, n, b1, b2);
+    if (c != DGAL_OK || n == 0) return c;
+    if (!grad_iou || !nx || !xflags || !grad_b1 || !grad_b2) return DGAL_ERR_INVALID_ARG;
+    if (!aligned(grad_iou, 4) || !aligned(xflags, 8) || !aligned(grad_b1, 4) || !aligned(grad_b2, 4))
+        return DGAL_ERR_MISALIGNED;
+    return from_cuda(dgal::launch_box_bwd(dims, layout, n, b1, b2, grad_iou, nx, xflags, grad_b1, grad_b2,
+                                          as_cuda(stream)));
+}
+
+dgal_status dgal_box_iou_paired_fused(int dims, int layout, int64_t n, const float *b1, const float *b2,
+                                      const float *grad_iou, float grad_scale, float *iou, float *grad_b1,
+                                      float *grad_b2, dgal_stream stream)
+{
+    const dgal_status c = box_check(dims, layout, n, b1, b2);
+    if (c != DGAL_OK || n == 0) return c;
+    if (!grad_b1 || !grad_b2) return DGAL_ERR_INVALID_ARG;
+    if ((grad_iou && !aligned(grad_iou, 4)) || (iou && !aligned(iou, 4)) || !aligned(grad_b1, 4) ||
+        !aligned(grad_b2, 4))
+        return DGAL_ERR_MISALIGNED;
+    return from_cuda(dgal::launch_box_fused(dims, layout, n, b1, b2, grad_iou, grad_scale, iou, grad_b1, grad_b2,
+                                            as_cuda(stream)));
+}
+
 dgal_status dgal_iou_pairwise(int K, int64_t n_rows, const float *row_x, const float *row_y, int64_t m,
                               const float *col_x, const float *col_y, int64_t row_offset, float *iou,
                               float nms_thresh, uint64_t *mask, int64_t mask_words, int32_t *nbr_count,

@@ -1,0 +1,326 @@
+// dgal_box.cu — rotated-box front end of the paired IoU path (SURVEY §8(f) f1 and
+// f3; SPEC metrics-boxes S:336-418; "2D IoU Loss and 3D IoU Loss for
+// rotated bounding boxes").  DESIGN.md §4.7.
+//
+// The boxes are read as parameters (20 B per 2D box, 28 B per yaw-only 3D box
+// instead of 32 B of corners) and turned into Poly<4> in registers:
+//   box_to_polygon: corners c + R(theta)(+-w/2, +-h/2), CCW from (-w/2, -h/2),
+// taken relative to the centre of box 1 (IoU is translation invariant; corners
+// near 0 keep the decision predicates accurate).  The clip, the flags and the
+// backward phases are the polygon path's (dgal_core.cuh).  3D: V = A d, V_i =
+// A_i dz with dz the overlap of the z extents.  The backward maps the
+// corner gradients to the box parameters (box_to_polygon_grad) and adds
+// the dz / d terms of the product rule.
+//
+// Layout: parameter p of box k is b[k * sk + p * sp]; planes (sk = 1, sp = n:
+// coalesced, the fast layout) or rows (sk = P, sp = 1: a torch [n, P] tensor).
+// Parameter order: 2D (cx, cy, w, h, theta), 3D (cx, cy, cz, w, h, d, theta).
+#include "dgal_core.cuh"
+#include "dgal_internal.h"
+
+namespace dgal {
+
+namespace {
+
+constexpr int kBoxTile = 256;  // backward tile = CTA size
+
+template <int DIMS>
+struct Box {
+    float cx, cy, cz, w, h, d, th;
+};
+
+template <int DIMS>
+__device__ __forceinline__ Box<DIMS> load_box(const float *__restrict__ b, int64_t k, int64_t sk, int64_t sp)
+{
+    const float *p = b + k * sk;
+    Box<DIMS> r;
+    r.cx = __ldg(p);
+    r.cy = __ldg(p + sp);
+    if (DIMS == 3) {
+        r.cz = __ldg(p + 2 * sp); r.w = __ldg(p + 3 * sp); r.h = __ldg(p + 4 * sp);
+        r.d = __ldg(p + 5 * sp); r.th = __ldg(p + 6 * sp);
+    } else {
+        r.cz = 0.f; r.w = __ldg(p + 2 * sp); r.h = __ldg(p + 3 * sp); r.d = 1.f; r.th = __ldg(p + 4 * sp);
+    }
+    return r;
+}
+
+// cos / sin of theta: exact reduction of theta / pi (no Payne-Hanek slow path, no
+// local memory); theta is accepted unbounded.
+__device__ __forceinline__ void box_sincos(float th, float &s, float &c)
+{
+    sincospif(th * 0.318309886183790672f, &s, &c);
+}
+
+// box_to_polygon relative to the origin o: (cx - ox, cy - oy) = (dcx, dcy).
+// Contraction-free, so the same parameters always give bitwise the same corners
+// (forward and backward agree; identical boxes give identical polygons).
+__device__ __forceinline__ void box_poly(float dcx, float dcy, float w, float h, float c, float s, Poly<4> &P)
+{
+    const float hw = 0.5f * w, hh = 0.5f * h;
+    const float cw = __fmul_rn(c, hw), sw = __fmul_rn(s, hw);
+    const float ch = __fmul_rn(c, hh), sh = __fmul_rn(s, hh);
+    // R (lx, ly) = (c lx - s ly, s lx + c ly) at (-hw,-hh), (hw,-hh), (hw,hh), (-hw,hh)
+    P.x[0] = __fadd_rn(dcx, __fsub_rn(sh, cw)); P.y[0] = __fsub_rn(dcy, __fadd_rn(sw, ch));
+    P.x[1] = __fadd_rn(dcx, __fadd_rn(cw, sh)); P.y[1] = __fadd_rn(dcy, __fsub_rn(sw, ch));
+    P.x[2] = __fadd_rn(dcx, __fsub_rn(cw, sh)); P.y[2] = __fadd_rn(dcy, __fadd_rn(sw, ch));
+    P.x[3] = __fsub_rn(dcx, __fadd_rn(cw, sh)); P.y[3] = __fadd_rn(dcy, __fsub_rn(ch, sw));
+}
+
+struct Trig {
+    float c1, s1, c2, s2;
+};
+
+template <int DIMS>
+__device__ __forceinline__ Trig box_pair_polys(const Box<DIMS> &a, const Box<DIMS> &b, Poly<4> &P, Poly<4> &Q)
+{
+    Trig t;
+    box_sincos(a.th, t.s1, t.c1);
+    box_sincos(b.th, t.s2, t.c2);
+    box_poly(0.f, 0.f, a.w, a.h, t.c1, t.s1, P);
+    box_poly(__fsub_rn(b.cx, a.cx), __fsub_rn(b.cy, a.cy), b.w, b.h, t.c2, t.s2, Q);
+    return t;
+}
+
+// overlap of the z extents [cz - d/2, cz + d/2]; top1 / bot1: the top /
+// bottom of the overlap is box 1's (ties to box 1, as in the oracle)
+struct ZOver {
+    float dz;
+    bool top1, bot1;
+};
+
+template <int DIMS>
+__device__ __forceinline__ ZOver z_overlap(const Box<DIMS> &a, const Box<DIMS> &b)
+{
+    ZOver z{1.f, true, true};
+    if (DIMS == 3) {
+        const float t1 = fmaf(0.5f, a.d, a.cz), t2 = fmaf(0.5f, b.d, b.cz);
+        const float b1 = fmaf(-0.5f, a.d, a.cz), b2 = fmaf(-0.5f, b.d, b.cz);
+        z.top1 = t1 <= t2;
+        z.bot1 = b1 >= b2;
+        z.dz = fmaxf(fminf(t1, t2) - fmaxf(b1, b2), 0.f);
+    }
+    return z;
+}
+
+// box_to_polygon_grad: corner cotangents G -> (cx, cy, w, h, theta).
+//   d/dc = sum G_k;  d/dw = sum sx_k R^T G_k . e_x;  d/dh = sum sy_k R^T G_k . e_y;
+//   d/dtheta = sum G_k . R' u_k = w (-s ax + c ay) + h (-c bx - s by),
+// with (ax, ay) = sum sx_k G_k, (bx, by) = sum sy_k G_k, sx = (-,+,+,-)/2, sy = (-,-,+,+)/2.
+struct BoxGrad {
+    float cx, cy, w, h, th;
+};
+
+__device__ __forceinline__ BoxGrad box_vjp(float w, float h, float c, float s, const Poly<4> &G)
+{
+    BoxGrad o;
+    o.cx = (G.x[0] + G.x[1]) + (G.x[2] + G.x[3]);
+    o.cy = (G.y[0] + G.y[1]) + (G.y[2] + G.y[3]);
+    const float ax = 0.5f * ((G.x[1] + G.x[2]) - (G.x[0] + G.x[3]));
+    const float ay = 0.5f * ((G.y[1] + G.y[2]) - (G.y[0] + G.y[3]));
+    const float bx = 0.5f * ((G.x[2] + G.x[3]) - (G.x[0] + G.x[1]));
+    const float by = 0.5f * ((G.y[2] + G.y[3]) - (G.y[0] + G.y[1]));
+    o.w = fmaf(c, ax, s * ay);
+    o.h = fmaf(c, by, -s * bx);
+    o.th = fmaf(w, fmaf(c, ay, -s * ax), -h * fmaf(c, bx, s * by));
+    return o;
+}
+
+template <int DIMS>
+__device__ __forceinline__ void store_box_grad(float *__restrict__ gb, int64_t k, int64_t sk, int64_t sp,
+                                               const BoxGrad &g, float gcz, float gd)
+{
+    float *p = gb + k * sk;
+    p[0] = g.cx;
+    p[sp] = g.cy;
+    if (DIMS == 3) {
+        p[2 * sp] = gcz; p[3 * sp] = g.w; p[4 * sp] = g.h; p[5 * sp] = gd; p[6 * sp] = g.th;
+    } else {
+        p[2 * sp] = g.w; p[3 * sp] = g.h; p[4 * sp] = g.th;
+    }
+}
+
+// dz / d terms of the 3D product rule: dL/d(dz) = cvi A_i; dz/dcz = +-1 / 0
+// and dz/dd = 1/2 per end owned; dL/dd1 += cvu A_1 (through V_1 = A_1 d1).
+template <int DIMS>
+__device__ __forceinline__ void z_grads(const VolCoef &co, const ZOver &z, float &gcz1, float &gd1, float &gcz2,
+                                        float &gd2)
+{
+    gcz1 = gd1 = gcz2 = gd2 = 0.f;
+    if (DIMS == 3) {
+        const float gdz = co.cvi * co.ai;
+        const float t1 = z.top1 ? 1.f : 0.f, b1 = z.bot1 ? 1.f : 0.f;
+        gcz1 = gdz * (t1 - b1);
+        gcz2 = gdz * ((1.f - t1) - (1.f - b1));
+        gd1 = fmaf(co.cvu, co.a1, gdz * 0.5f * (t1 + b1));
+        gd2 = fmaf(co.cvu, co.a2, gdz * 0.5f * ((1.f - t1) + (1.f - b1)));
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// forward: IoU (2D) or 3D IoU, nx / xflags of the BEV intersection
+// ---------------------------------------------------------------------------
+template <int DIMS>
+__global__ void __launch_bounds__(kPairedThreads)
+box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict__ b2, int64_t sk, int64_t sp,
+               float *__restrict__ iou, uint8_t *__restrict__ nx, uint8_t *__restrict__ xflags)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const Box<DIMS> a = load_box<DIMS>(b1, k, sk, sp), b = load_box<DIMS>(b2, k, sk, sp);
+    Poly<4> P, Q;
+    box_pair_polys<DIMS>(a, b, P, Q);
+    const FwdOut<4, true> r = iou_fwd<4, true>(P, Q);
+    float v = r.iou;
+    int m = r.nx;
+    uint64_t seq = r.seq.w[0];
+    if (DIMS == 3) {
+        const ZOver z = z_overlap<DIMS>(a, b);
+        const float Vix2 = r.Aix2 * z.dz;
+        const float Vux2 = (r.A1x2 * a.d + r.A2x2 * b.d) - Vix2;
+        const bool ok = m > 0 && Vix2 > 0.f && Vux2 > 0.f;
+        v = ok ? fminf(Vix2 / Vux2, 1.f) : 0.f;
+        m = ok ? m : 0;
+        seq = ok ? seq : 0ull;
+    }
+    __stcs(iou + k, v);
+    nx[k] = (uint8_t)m;
+    __stcs(reinterpret_cast<unsigned long long *>(xflags) + k, (unsigned long long)seq);
+}
+
+// ---------------------------------------------------------------------------
+// backward through the recorded nx / xflags (the polygon path's phases)
+// ---------------------------------------------------------------------------
+struct BoxBwdSmem {
+    float x1[kBoxTile * 4], y1[kBoxTile * 4], x2[kBoxTile * 4], y2[kBoxTile * 4];  // corners, [pair][k]
+    float scr[4 * 4 * kBoxTile];                                                 // [slot][pair]
+    uint16_t queue[kBoxTile / 32][32 * 8];
+    FlagLut lut;
+};
+
+template <int DIMS>
+__global__ void __launch_bounds__(kBoxTile)
+box_bwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict__ b2, int64_t sk, int64_t sp,
+               const float *__restrict__ grad, const uint8_t *__restrict__ nx, const uint8_t *__restrict__ xflags,
+               float *__restrict__ gb1, float *__restrict__ gb2)
+{
+    __shared__ __align__(16) BoxBwdSmem S;
+    const int tid = threadIdx.x;
+    const int64_t k = (int64_t)blockIdx.x * kBoxTile + tid;
+    const bool live = k < n;
+    fill_flag_lut(S.lut, tid, kBoxTile);
+    Box<DIMS> a{}, b{};
+    Poly<4> P, Q;
+    Trig t{1.f, 0.f, 1.f, 0.f};
+    Seq<4> sq;
+    sq.w[0] = 0ull;
+    int m = 0;
+    float g = 0.f;
+    if (live) {
+        a = load_box<DIMS>(b1, k, sk, sp);
+        b = load_box<DIMS>(b2, k, sk, sp);
+        t = box_pair_polys<DIMS>(a, b, P, Q);
+        sq.w[0] = __ldcs(reinterpret_cast<const unsigned long long *>(xflags) + k);
+        m = nx[k];
+        g = __ldcs(grad + k);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { P.x[q] = P.y[q] = Q.x[q] = Q.y[q] = 0.f; }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        S.x1[tid * 4 + q] = P.x[q]; S.y1[tid * 4 + q] = P.y[q];
+        S.x2[tid * 4 + q] = Q.x[q]; S.y2[tid * 4 + q] = Q.y[q];
+    }
+    const ZOver z = z_overlap<DIMS>(a, b);
+    __syncthreads();  // flag table and corner tile
+    Poly<4> G1, G2;
+    VolCoef co;
+    bwd_tile_pair<4, kBoxTile>(S.x1, S.y1, S.x2, S.y2, sq, m, g, live, S.scr, S.queue[tid >> 5], S.lut, G1, G2,
+                               Extrude{z.dz, a.d, b.d}, &co);
+    if (!live) return;
+    float gcz1, gd1, gcz2, gd2;
+    z_grads<DIMS>(co, z, gcz1, gd1, gcz2, gd2);
+    store_box_grad<DIMS>(gb1, k, sk, sp, box_vjp(a.w, a.h, t.c1, t.s1, G1), gcz1, gd1);
+    store_box_grad<DIMS>(gb2, k, sk, sp, box_vjp(b.w, b.h, t.c2, t.s2, G2), gcz2, gd2);
+}
+
+// ---------------------------------------------------------------------------
+// fused loss forward + backward (f2 on boxes): no nx / xflags round trip
+// ---------------------------------------------------------------------------
+template <int DIMS>
+__global__ void __launch_bounds__(kPairedThreads)
+box_fused_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict__ b2, int64_t sk, int64_t sp,
+                 const float *__restrict__ grad, float scale, float *__restrict__ iou, float *__restrict__ gb1,
+                 float *__restrict__ gb2)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const Box<DIMS> a = load_box<DIMS>(b1, k, sk, sp), b = load_box<DIMS>(b2, k, sk, sp);
+    const float g = grad ? __ldcs(grad + k) : scale;
+    Poly<4> P, Q, G1, G2;
+    const Trig t = box_pair_polys<DIMS>(a, b, P, Q);
+    const ZOver z = z_overlap<DIMS>(a, b);
+    VolCoef co;
+    const float v = iou_fused<4>(P, Q, g, G1, G2, Extrude{z.dz, a.d, b.d}, &co);
+    if (iou) __stcs(iou + k, v);
+    float gcz1, gd1, gcz2, gd2;
+    z_grads<DIMS>(co, z, gcz1, gd1, gcz2, gd2);
+    store_box_grad<DIMS>(gb1, k, sk, sp, box_vjp(a.w, a.h, t.c1, t.s1, G1), gcz1, gd1);
+    store_box_grad<DIMS>(gb2, k, sk, sp, box_vjp(b.w, b.h, t.c2, t.s2, G2), gcz2, gd2);
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+namespace {
+inline void box_strides(int dims, int layout, int64_t n, int64_t &sk, int64_t &sp)
+{
+    const int P = dims == 3 ? 7 : 5;
+    if (layout == 0) { sk = 1; sp = n; }   // planes [P][n]
+    else { sk = P; sp = 1; }               // rows [n][P]
+}
+}  // namespace
+
+cudaError_t launch_box_fwd(int dims, int layout, int64_t n, const float *b1, const float *b2, float *iou,
+                           uint8_t *nx, uint8_t *xflags, cudaStream_t st)
+{
+    int64_t sk, sp;
+    box_strides(dims, layout, n, sk, sp);
+    const unsigned grid = (unsigned)((n + kPairedThreads - 1) / kPairedThreads);
+    if (dims == 3)
+        box_fwd_kernel<3><<<grid, kPairedThreads, 0, st>>>(n, b1, b2, sk, sp, iou, nx, xflags);
+    else
+        box_fwd_kernel<2><<<grid, kPairedThreads, 0, st>>>(n, b1, b2, sk, sp, iou, nx, xflags);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_box_bwd(int dims, int layout, int64_t n, const float *b1, const float *b2, const float *grad,
+                           const uint8_t *nx, const uint8_t *xflags, float *gb1, float *gb2, cudaStream_t st)
+{
+    int64_t sk, sp;
+    box_strides(dims, layout, n, sk, sp);
+    const unsigned grid = (unsigned)((n + kBoxTile - 1) / kBoxTile);
+    if (dims == 3)
+        box_bwd_kernel<3><<<grid, kBoxTile, 0, st>>>(n, b1, b2, sk, sp, grad, nx, xflags, gb1, gb2);
+    else
+        box_bwd_kernel<2><<<grid, kBoxTile, 0, st>>>(n, b1, b2, sk, sp, grad, nx, xflags, gb1, gb2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_box_fused(int dims, int layout, int64_t n, const float *b1, const float *b2, const float *grad,
+                             float scale, float *iou, float *gb1, float *gb2, cudaStream_t st)
+{
+    int64_t sk, sp;
+    box_strides(dims, layout, n, sk, sp);
+    const unsigned grid = (unsigned)((n + kPairedThreads - 1) / kPairedThreads);
+    if (dims == 3)
+        box_fused_kernel<3><<<grid, kPairedThreads, 0, st>>>(n, b1, b2, sk, sp, grad, scale, iou, gb1, gb2);
+    else
+        box_fused_kernel<2><<<grid, kPairedThreads, 0, st>>>(n, b1, b2, sk, sp, grad, scale, iou, gb1, gb2);
+    return cudaGetLastError();
+}
+
+}  // namespace dgal

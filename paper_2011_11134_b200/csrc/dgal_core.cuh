@@ -167,25 +167,74 @@ struct FwdOut {
     float iou;
     int nx;
     Seq<K> seq;
+    float A1x2, A2x2, Aix2;  // twice the areas (the 3D box forward extrudes them)
+};
+
+// Extrusion of the footprints for the yaw-only 3D IoU:
+// V_1 = A_1 d1, V_2 = A_2 d2, V_i = A_i dz.  The 2D path passes {1, 1, 1}, which
+// folds away (x * 1.0f == x), leaving the plain IoU arithmetic.
+struct Extrude {
+    float dz, d1, d2;
+};
+__device__ __forceinline__ Extrude flat() { return Extrude{1.f, 1.f, 1.f}; }
+
+// Scalars of the S:303 chain the box front end needs: dL/dV_i, dL/dV_1 (= dL/dV_2)
+// and the footprint areas (zero for an empty pair).
+struct VolCoef {
+    float cvi, cvu, ai, a1, a2;
 };
 
 // The edge-interval clip shared by the paired forward, the pairwise path and the
-// fused loss kernel: edge vectors, shoelace terms, the Cyrus-Beck interval of
-// every edge of both polygons (FLAGS: p1 intervals carry their line index in the
-// low mantissa bits) and the Green area of p1 ∩ p2.
+// fused loss kernel.
+//
+//   * p1 side: the Cyrus-Beck interval [t0, t1] of every edge of p1 against the
+//     closed half-planes of p2; the line that bounds it rides in the low mantissa
+//     bits.  A piece that starts inside the edge is an ENTRY of p1's boundary
+//     into p2 (through p2 line j_in), one that ends inside it an EXIT (through
+//     p2 line j_out).  All of these come from one set of decision values d, so
+//     they are mutually consistent: the inside part of p1's boundary is a set
+//     of arcs, each from an entry to an exit.
+//   * p2 side: derived from the p1 events, not decided separately.  After an
+//     exit through line j the boundary of p1 ∩ p2 follows p2 edge j from that
+//     very crossing point X_out; it leaves p2's boundary at the next entry, at
+//     that crossing point X_in.  So the piece on p2 edge j runs from X_out (or
+//     w_j) to X_in (or w_j+1), and p2 vertex j is inside p1 iff the last event
+//     before it along p2 is an exit (segmented scan of the events around p2).
+//     Only when there are no events at all is p2's inside-ness decided on its
+//     own (all vertices strictly inside the open half-planes of p1).
+//
+// Events are taken from SIGNS, not from rounded parameters: p1 vertex i is inside
+// p2 iff all its d[i][j] > 0 (one bit per vertex, shared by both edges at it);
+// an edge has an entry iff it has a piece and its start is outside, an exit iff
+// its end is outside, and an inside end point pins that end of the piece to 0 or
+// 1 exactly.  So the arcs are well formed whatever the rounding (a t* within an
+// ulp of 1 no longer hides an exit, a line index is never lost).
+//
+// Each crossing point is therefore ONE point shared by the two pieces that meet
+// there, and the Green sum below is the area of a closed polygon: exact up to
+// rounding of the points, independent of the origin, and stable when edges of
+// p1 and p2 nearly coincide (prediction ~ target) — where independent t / s
+// parameters of a near-parallel crossing are each ill-conditioned (~1/sin) and
+// disagree.  DESIGN.md §4.1.
 template <int K>
 struct Clip {
     float gx[K], gy[K], fx[K], fy[K];  // edge vectors of p1, p2
     float C1[K], C2[K];                // shoelace terms v_i x v_i+1, w_j x w_j+1
-    float t0[K], t1[K], s0[K], s1[K];  // boundary pieces on p1 / p2 edges
+    float t0[K], t1[K];                // boundary piece [t0, t1] on p1 edge i (empty if t0 > t1)
+    uint32_t jin, jout;                // line index of the entry / exit of p1 edge i (4 bits each)
+    uint32_t valid, enter, leave;      // p1 edges with a piece / an entry / an exit (bit i)
+    float ax[K], ay[K], bx[K], by[K];  // boundary piece on p2 edge j: from (ax, ay) to (bx, by)
+    uint32_t on2;                      // p2 edges carrying a boundary piece
+    uint32_t in2;                      // p2 vertices inside p1 (consistent with the events)
     float A1x2, A2x2, Aix2;            // twice the areas
     bool nonempty;
 };
 
-// p1, p2 must already be recentred on o = p1.v0 (p1.x[0] == p1.y[0] == 0).
-template <int K, bool FLAGS>
+// p1, p2 must already be recentred (coordinates near 0; p1.v0 or a box centre).
+template <int K>
 __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &Q, Clip<K> &c)
 {
+    constexpr uint32_t KMASK = (1u << K) - 1u;
     // edge vectors g_i = v_i+1 - v_i (p1), f_j = w_j+1 - w_j (p2); shoelace terms
     float *gx = c.gx, *gy = c.gy, *fx = c.fx, *fy = c.fy, *C1 = c.C1, *C2 = c.C2;
     float A1x2 = 0.f, A2x2 = 0.f;
@@ -227,65 +276,119 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
         separated |= (m1 <= kTiny) | (m2 <= 0.f);
     }
 
-    // Cyrus-Beck intervals.  For the edge a -> b against one line (a, b = the
-    // shifted decision values of its end points, never 0): the inside set is
-    // {t : a + t (b - a) > 0}; b > a bounds it below by t* = a / (a - b), b < a
-    // above, b == a keeps all (a > 0: t* = +inf) or nothing (a < 0: t* = -inf).
-    // Both-outside end points give t* > 1 (below) or t* < 0 (above): the interval
-    // empties itself.  (m t* is NaN when m = 0 and t* = inf: max/min ignore it.)
-    float *t0 = c.t0, *t1 = c.t1, *s0 = c.s0, *s1 = c.s1;
+    // p1 vertices inside p2 (closed test, d never 0)
+    uint32_t in1 = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        float mn = d[i][0];
+#pragma unroll
+        for (int j = 1; j < K; ++j) mn = fminf(mn, d[i][j]);
+        in1 |= (uint32_t)(mn > 0.f) << i;
+    }
+
+    // Cyrus-Beck intervals of p1's edges.  For the edge a -> b against one line
+    // (a, b = the shifted decision values of its end points, never 0): the inside
+    // set is {t : a + t (b - a) > 0}; b > a bounds it below by t* = a / (a - b),
+    // b < a above, b == a keeps all (a > 0) or nothing (a < 0).  t* is formed from
+    // the end point nearer the line — a/(a-b) if |a| <= |b|, else 1 + b/(a-b) — so
+    // no cancellation, and an end point on the line gives exactly 0 or 1.
+    // den + tiny keeps r finite (a == b: r = 1e30, t* = +-huge), so every candidate
+    // is finite and carries the index j of its line.  hi starts just above 1 so a
+    // candidate that rounds to 1 still wins and keeps its index.
+    float *t0 = c.t0, *t1 = c.t1;
+    uint32_t jin = 0, jout = 0, valid = 0, enter = 0, leave = 0;
+    const float hi0 = __int_as_float(0x3F800008);
+    // Events and the p2 pieces they delimit (same pass): an exit of p1 edge i through
+    // p2 line j_out starts the piece on p2 edge j_out at X_out = v_i + t1 g_i; an
+    // entry through line j_in ends the piece on p2 edge j_in at X_in = v_i + t0 g_i.
+    float *ax = c.ax, *ay = c.ay, *bx = c.bx, *by = c.by;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const int j1 = (j + 1) % K;
+        ax[j] = Q.x[j]; ay[j] = Q.y[j];
+        bx[j] = Q.x[j1]; by[j] = Q.y[j1];
+    }
+    uint32_t ev_out = 0, ev_in = 0;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         const int i1 = (i + 1) % K;
-        float lo = 0.f, hi = 1.f, lo2 = 0.f, hi2 = 1.f;
+        float lo = 0.f, hi = hi0;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-            // t* = a/(a-b) near 0 (lower bounds) and as 1 + b/(a-b) near 1 (upper
-            // bounds): an end point lying on the line (|a| or |b| = tiny) then gives
-            // t* = 0 or 1 exactly, so identical polygons keep [0, 1] intervals.
-            {   // p1 edge i vs p2 line j
-                const float a = d[i][j], b = d[i1][j];
-                if (FLAGS) {
-                    // den + tiny keeps r finite (a == b: r = 1e30, t* = +-huge): the
-                    // candidates stay finite, so the index bits survive
-                    const float den = (a - b) + kTiny;
-                    const float r = rcp_approx(den);
-                    const float m = __saturatef(-den * kBig);  // 1: bounds below
-                    lo = fmaxf(lo, enc_idx(m * (a * r), j));
-                    hi = fminf(hi, enc_idx(fmaf(m, kBig, fmaf(b, r, 1.f)), j));
-                } else {
-                    const float den = a - b;
-                    const float r = rcp_approx(den);
-                    const float m = __saturatef(-den * kBig);  // 1: bounds below
-                    lo = fmaxf(lo, m * (a * r));               // finite or NaN (ignored)
-                    hi = fminf(hi, fmaf(m, kBig, fmaf(b, r, 1.f)));  // +-inf when a == b
-                }
-            }
-            {   // p2 edge i vs p1 line j
-                const float a = e[i][j], b = e[i1][j];
-                const float den = a - b;
-                const float r = rcp_approx(den);
-                const float m = __saturatef(-den * kBig);
-                lo2 = fmaxf(lo2, m * (a * r));
-                hi2 = fminf(hi2, fmaf(m, kBig, fmaf(b, r, 1.f)));
-            }
+            const float a = d[i][j], b = d[i1][j];
+            const float den = (a - b) + kTiny;
+            const float r = rcp_approx(den);
+            const float m = __saturatef(-den * kBig);  // 1: bounds below
+            const float v = (fabsf(a) <= fabsf(b)) ? a * r : fmaf(b, r, 1.f);
+            lo = fmaxf(lo, enc_idx(m * v, j));
+            hi = fminf(hi, enc_idx(fmaf(m, kBig, v), j));
         }
-        t0[i] = lo; t1[i] = hi; s0[i] = lo2; s1[i] = hi2;
+        const bool in_s = (in1 >> i) & 1u, in_e = (in1 >> i1) & 1u;
+        const float a0 = in_s ? 0.f : lo;
+        const float a1 = in_e ? 1.f : fminf(hi, 1.f);
+        // compare without the index bits (they may lift a t0 of 1 above a t1 of 1)
+        const bool ok = __int_as_float(__float_as_int(a0) & ~7) <= __int_as_float(__float_as_int(a1) & ~7);
+        const bool has_in = ok && !in_s, has_out = ok && !in_e;
+        t0[i] = a0; t1[i] = a1;
+        valid |= (uint32_t)ok << i;
+        enter |= (uint32_t)has_in << i;
+        leave |= (uint32_t)has_out << i;
+        const uint32_t ljin = (uint32_t)dec_idx(lo), ljout = (uint32_t)dec_idx(hi);
+        jin |= ljin << (4 * i);
+        jout |= ljout << (4 * i);
+        const int ji = has_in ? (int)ljin : 8;   // 8: no event
+        const int jo = has_out ? (int)ljout : 8;
+        ev_in |= has_in ? (1u << ji) : 0u;
+        ev_out |= has_out ? (1u << jo) : 0u;
+        const float xix = fmaf(a0, gx[i], P.x[i]), xiy = fmaf(a0, gy[i], P.y[i]);
+        const float xox = fmaf(a1, gx[i], P.x[i]), xoy = fmaf(a1, gy[i], P.y[i]);
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            ax[j] = (jo == j) ? xox : ax[j];
+            ay[j] = (jo == j) ? xoy : ay[j];
+            bx[j] = (ji == j) ? xix : bx[j];
+            by[j] = (ji == j) ? xiy : by[j];
+        }
     }
+    c.jin = jin; c.jout = jout; c.valid = valid; c.enter = enter; c.leave = leave;
 
-    // area of p1 ∩ p2 (Green), interleaved so identical polygons reproduce A1x2 bitwise
+    // p2 vertex j inside p1 <=> the last event on p2 edges j-1, j-2, ... (cyclic) is
+    // an exit without an entry after it.  Segmented scan over the doubled cycle:
+    // position p carries the end state of the nearest event edge <= p.
+    // With no event at all p1's boundary is entirely inside p2 or entirely
+    // outside; in the latter case p2 lies inside p1 unless they are separated.
+    const uint32_t ev = ev_out | ev_in;
+    uint32_t in2;
+    if (ev == 0u) {
+        in2 = (valid == 0u && !separated) ? KMASK : 0u;
+    } else {
+        uint32_t evd = ev | (ev << K);
+        uint32_t st = (ev_out & ~ev_in) | ((ev_out & ~ev_in) << K);
+#pragma unroll
+        for (int sh = 1; sh < 2 * K; sh <<= 1) {
+            st = (st & evd) | ((st << sh) & ~evd);
+            evd |= evd << sh;
+        }
+        in2 = (st >> (K - 1)) & KMASK;               // state after edge j-1, j = 0..K-1
+    }
+    const uint32_t on2 = ev | in2;
+
+    // area of p1 ∩ p2 (Green over the closed boundary), interleaved so identical
+    // polygons (no events, no p2 piece) reproduce A1x2 bitwise
     float Aix2 = 0.f;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         Aix2 = fmaf(fmaxf(t1[k] - t0[k], 0.f), C1[k], Aix2);
-        Aix2 = fmaf(fmaxf(s1[k] - s0[k], 0.f), C2[k], Aix2);
+        const float c2 = cross_rn(ax[k], ay[k], bx[k], by[k]);
+        Aix2 = __fadd_rn(Aix2, ((on2 >> k) & 1u) ? c2 : 0.f);
     }
     Aix2 = fminf(Aix2, fminf(A1x2, A2x2));
     c.A1x2 = A1x2;
     c.A2x2 = A2x2;
     c.Aix2 = Aix2;
+    c.on2 = on2;
+    c.in2 = in2;
     c.nonempty = !separated && (Aix2 > 0.f);
-
 }
 
 // p1, p2 must already be recentred on o = p1.v0 (p1.x[0] == p1.y[0] == 0).
@@ -294,8 +397,8 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
 {
     constexpr uint32_t KMASK = (1u << K) - 1u;
     Clip<K> c;
-    clip_intervals<K, FLAGS>(P, Q, c);
-    const float *t0 = c.t0, *t1 = c.t1, *s0 = c.s0, *s1 = c.s1;
+    clip_intervals<K>(P, Q, c);
+    const float *t0 = c.t0, *t1 = c.t1;
     const float A1x2 = c.A1x2, A2x2 = c.A2x2, Aix2 = c.Aix2;
     bool nonempty = c.nonempty;
 
@@ -304,12 +407,13 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
     for (int k = 0; k < Seq<K>::NW; ++k) out.seq.w[k] = 0;
     out.nx = 0;
     out.iou = 0.f;
+    out.A1x2 = A1x2;
+    out.A2x2 = A2x2;
+    out.Aix2 = 0.f;
 
     if (FLAGS) {
-        // p2 vertex j strictly inside p1 <=> its edge interval starts at 0 unclipped
-        uint32_t in2 = 0;
-#pragma unroll
-        for (int j = 0; j < K; ++j) in2 |= (uint32_t)((s0[j] <= 0.f) & (s0[j] < s1[j])) << j;
+        // p2 vertices inside p1, consistent with the crossings (clip_intervals)
+        const uint32_t in2 = c.in2;
         const uint32_t in2dup = in2 | (in2 << K);
 
         // Walk p1's edges in order: [FromP1(i) | Cross(i, j_in)] [Cross(i, j_out) run of FromP2]
@@ -319,11 +423,11 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
         int pos = 0;
 #pragma unroll
         for (int i = 0; i < K; ++i) {
-            const bool valid = t0[i] < t1[i];
-            const bool has_in = t0[i] > kTiny;
-            const bool has_out = t1[i] < 1.f;
-            const uint32_t b0 = has_in ? (0xC0u | (i << 3) | (uint32_t)dec_idx(t0[i])) : (0x40u | i);
-            const uint32_t jo = (uint32_t)dec_idx(t1[i]);
+            const bool valid = (c.valid >> i) & 1u;
+            const bool has_in = (c.enter >> i) & 1u;
+            const bool has_out = (c.leave >> i) & 1u;
+            const uint32_t b0 = has_in ? (0xC0u | (i << 3) | ((c.jin >> (4 * i)) & 7u)) : (0x40u | i);
+            const uint32_t jo = (c.jout >> (4 * i)) & 7u;
             const uint32_t b1 = 0xC0u | (i << 3) | jo;
             // run of p2 vertices inside p1 after p2 edge j_out: trailing ones of in2 rotated
             const uint32_t p0 = (jo + 1u) & (K - 1u);
@@ -373,6 +477,7 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
     if (nonempty) {
         const float Aux2 = (A1x2 + A2x2) - Aix2;
         out.iou = (Aux2 > 0.f) ? fminf(Aix2 / Aux2, 1.f) : 0.f;
+        out.Aix2 = Aix2;
     }
     return out;
 }
@@ -387,40 +492,50 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
 // p1, p2 recentred on p1.v0.  Returns IoU (identical to the pairwise path).
 template <int K>
 __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, float g, Poly<K> &G1,
-                                           Poly<K> &G2)
+                                           Poly<K> &G2, const Extrude ex = flat(), VolCoef *co = nullptr)
 {
 #pragma unroll
     for (int k = 0; k < K; ++k) { G1.x[k] = 0.f; G1.y[k] = 0.f; G2.x[k] = 0.f; G2.y[k] = 0.f; }
+    if (co) *co = VolCoef{0.f, 0.f, 0.f, 0.f, 0.f};
     Clip<K> c;
-    clip_intervals<K, false>(P, Q, c);
+    clip_intervals<K>(P, Q, c);
     if (!c.nonempty) return 0.f;
-    const float Aux2 = (c.A1x2 + c.A2x2) - c.Aix2;
-    if (!(Aux2 > 0.f)) return 0.f;
-    const float iou = fminf(c.Aix2 / Aux2, 1.f);
+    // V = A d (2D: d = 1); IoU = V_i / V_u
+    const float Vix2 = c.Aix2 * ex.dz;
+    const float Vux2 = (c.A1x2 * ex.d1 + c.A2x2 * ex.d2) - Vix2;
+    if (!(Vux2 > 0.f) || !(Vix2 > 0.f)) return 0.f;
+    const float iou = fminf(Vix2 / Vux2, 1.f);
 
     // piece weights (saturate: dead edges carry arbitrary end points, length 0)
+    // p2 pieces: parameters of their end points along the edge (projection; exact
+    // 0 at w_j, 1 up to rounding at w_j+1)
     float al1[K], be1[K], al2[K], be2[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         const float a0 = __saturatef(c.t0[i]), a1 = __saturatef(c.t1[i]);
-        const float b0 = __saturatef(c.s0[i]), b1 = __saturatef(c.s1[i]);
-        const float l1 = fmaxf(a1 - a0, 0.f), l2 = fmaxf(b1 - b0, 0.f);
+        const float inv = rcp_approx(fmaf(c.fx[i], c.fx[i], c.fy[i] * c.fy[i]));
+        const float b0 = __saturatef(fmaf(c.ax[i] - Q.x[i], c.fx[i], (c.ay[i] - Q.y[i]) * c.fy[i]) * inv);
+        const float b1 = __saturatef(fmaf(c.bx[i] - Q.x[i], c.fx[i], (c.by[i] - Q.y[i]) * c.fy[i]) * inv);
+        const float l1 = fmaxf(a1 - a0, 0.f);
+        const float l2 = ((c.on2 >> i) & 1u) ? fmaxf(b1 - b0, 0.f) : 0.f;
         const float h1 = 0.5f * (a0 + a1), h2 = 0.5f * (b0 + b1);
         al1[i] = l1 - l1 * h1; be1[i] = l1 * h1;
         al2[i] = l2 - l2 * h2; be2[i] = l2 * h2;
     }
-    // dIoU/dA_i = (A_u + A_i)/A_u^2, dIoU/dA_1,2 = -A_i/A_u^2
-    const float Ai = 0.5f * c.Aix2, Au = 0.5f * Aux2;
-    const float inv = 1.f / Au;
-    const float q = Ai * inv;
-    const float ci = g * ((1.f + q) * inv);
-    const float cu = g * (-q * inv);
-    const float hu = 0.5f * cu;
+    // dIoU/dV_i = (V_u + V_i)/V_u^2, dIoU/dV_1,2 = -V_i/V_u^2; dV/dA = d
+    const float Vi = 0.5f * Vix2, Vu = 0.5f * Vux2;
+    const float inv = 1.f / Vu;
+    const float q = Vi * inv;
+    const float cvi = g * ((1.f + q) * inv);
+    const float cvu = g * (-q * inv);
+    const float ci = cvi * ex.dz;
+    const float hu1 = (0.5f * cvu) * ex.d1, hu2 = (0.5f * cvu) * ex.d2;
+    if (co) *co = VolCoef{cvi, cvu, 0.5f * c.Aix2, 0.5f * c.A1x2, 0.5f * c.A2x2};
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int km = (k + K - 1) % K;
-        const float wa1 = fmaf(ci, al1[k], hu), wb1 = fmaf(ci, be1[km], hu);
-        const float wa2 = fmaf(ci, al2[k], hu), wb2 = fmaf(ci, be2[km], hu);
+        const float wa1 = fmaf(ci, al1[k], hu1), wb1 = fmaf(ci, be1[km], hu1);
+        const float wa2 = fmaf(ci, al2[k], hu2), wb2 = fmaf(ci, be2[km], hu2);
         G1.x[k] = fmaf(wa1, c.gy[k], wb1 * c.gy[km]);
         G1.y[k] = -fmaf(wa1, c.gx[k], wb1 * c.gx[km]);
         G2.x[k] = fmaf(wa2, c.fy[k], wb2 * c.fy[km]);
@@ -487,7 +602,11 @@ __device__ __forceinline__ void bwd_crossing(const float *sPx, const float *sPy,
     const float den = ex * hy - ey * hx;                       // g_i x f_j
     const float r = rcp_approx(den);
     const float t = __saturatef((Dx * hy - Dy * hx) * r);      // along p1 edge i
-    const float s = __saturatef((Dx * ey - Dy * ex) * r);      // along p2 edge j
+    // along p2 edge j: the projection of the SAME point X = v_i + t g_i (not an
+    // independent s = D x g / den), so the two pieces meeting at X share it even
+    // when the edges are nearly parallel (t ill-conditioned, see clip_intervals)
+    const float hh = rcp_approx(fmaf(hx, hx, hy * hy));
+    const float s = __saturatef(fmaf(fmaf(t, ex, -Dx), hx, fmaf(t, ey, -Dy) * hy) * hh);
     const bool enter = den < 0.f;
     DGAL_ASSERT(i >= 0 && i < K && j >= 0 && j < K);
     scr[(enter ? i : K + i) * TILE] = t;
@@ -498,10 +617,12 @@ __device__ __forceinline__ void bwd_crossing(const float *sPx, const float *sPy,
 template <int K, int TILE>
 __device__ __forceinline__ void bwd_epilogue(const float *sPx, const float *sPy, const float *sQx,
                                              const float *sQy, float g, uint32_t V, const float *scr,
-                                             Poly<K> &G1, Poly<K> &G2)
+                                             Poly<K> &G1, Poly<K> &G2, const Extrude ex = flat(),
+                                             VolCoef *co = nullptr)
 {
 #pragma unroll
     for (int k = 0; k < K; ++k) { G1.x[k] = 0.f; G1.y[k] = 0.f; G2.x[k] = 0.f; G2.y[k] = 0.f; }
+    if (co) *co = VolCoef{0.f, 0.f, 0.f, 0.f, 0.f};
     if (V == 0) return;  // nx == 0: zero subgradient
 
     Poly<K> P, Q;
@@ -547,28 +668,87 @@ __device__ __forceinline__ void bwd_epilogue(const float *sPx, const float *sPy,
         Aix2 = fmaf(l2, C2[i], Aix2);
     }
 
-    // dIoU/dA_i = (A_u + A_i)/A_u^2, dIoU/dA_1,2 = -A_i/A_u^2
+    // dIoU/dV_i = (V_u + V_i)/V_u^2, dIoU/dV_1,2 = -V_i/V_u^2; V = A d (2D: d = 1)
     const float Ai = 0.5f * Aix2;
-    const float Au = 0.5f * ((A1x2 + A2x2) - Aix2);
-    if (!(Au > 0.f) || !(Ai > 0.f)) return;  // R10 guard
-    const float inv = 1.f / Au;
-    const float q = Ai * inv;
-    const float ci = g * ((1.f + q) * inv);
-    const float cu = g * (-q * inv);
-    const float hu = 0.5f * cu;  // area_grad of p1/p2 is (n_k + n_k-1)/2 per vertex
+    const float Vi = Ai * ex.dz;
+    const float Vu = 0.5f * ((A1x2 * ex.d1 + A2x2 * ex.d2) - Aix2 * ex.dz);
+    if (!(Vu > 0.f) || !(Vi > 0.f)) return;  // R10 guard
+    const float inv = 1.f / Vu;
+    const float q = Vi * inv;
+    const float cvi = g * ((1.f + q) * inv);
+    const float cvu = g * (-q * inv);
+    const float ci = cvi * ex.dz;
+    // area_grad of p1/p2 is (n_k + n_k-1)/2 per vertex
+    const float hu1 = (0.5f * cvu) * ex.d1, hu2 = (0.5f * cvu) * ex.d2;
+    if (co) *co = VolCoef{cvi, cvu, Ai, 0.5f * A1x2, 0.5f * A2x2};
 
     // vertex k collects edge k (as its start, alpha) and edge k-1 (as its end, beta);
     // n = perp(edge) = (e_y, -e_x)
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int km = (k + K - 1) % K;
-        const float wa1 = fmaf(ci, al1[k], hu), wb1 = fmaf(ci, be1[km], hu);
-        const float wa2 = fmaf(ci, al2[k], hu), wb2 = fmaf(ci, be2[km], hu);
+        const float wa1 = fmaf(ci, al1[k], hu1), wb1 = fmaf(ci, be1[km], hu1);
+        const float wa2 = fmaf(ci, al2[k], hu2), wb2 = fmaf(ci, be2[km], hu2);
         G1.x[k] = fmaf(wa1, gy[k], wb1 * gy[km]);
         G1.y[k] = -fmaf(wa1, gx[k], wb1 * gx[km]);
         G2.x[k] = fmaf(wa2, fy[k], wb2 * fy[km]);
         G2.y[k] = -fmaf(wa2, fx[k], wb2 * fx[km]);
     }
+}
+
+// One backward tile: thread tid owns pair tid of a tile of TILE pairs whose
+// vertices are staged in shared memory as [pair][k] planes.  Decodes the pair's
+// flag bytes into provenance bits, queues its Cross bytes in the warp's queue
+// (warp prefix sum), evaluates the warp's crossings 32 at a time (full SIMT
+// width), then runs the epilogue.  Must be called by all 32 lanes of the warp.
+template <int K, int TILE>
+__device__ __forceinline__ void bwd_tile_pair(const float *tx1, const float *ty1, const float *tx2,
+                                              const float *ty2, const Seq<K> &sq, int m, float g, bool live,
+                                              float *scr, uint16_t *queue, const FlagLut &lut,
+                                              Poly<K> &G1, Poly<K> &G2, const Extrude ex = flat(),
+                                              VolCoef *co = nullptr)
+{
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint32_t V = 0;
+    int cnt = 0;
+#pragma unroll
+    for (int p = 0; p < 2 * K; ++p) {
+        const uint32_t b = (p < m) ? seq_byte<K>(sq, p) : 0u;
+        V |= lut.v[b];
+        cnt += (b >= 0xC0u);
+    }
+    int incl = cnt;                                  // warp prefix sum of the counts
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= d) incl += v;
+    }
+    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    int at = incl - cnt;
+#pragma unroll
+    for (int p = 0; p < 2 * K; ++p) {
+        const uint32_t b = (p < m) ? seq_byte<K>(sq, p) : 0u;
+        if (b >= 0xC0u) {
+            DGAL_ASSERT(at >= 0 && at < 32 * 2 * K);
+            queue[at++] = (uint16_t)((lane << 8) | b);
+        }
+    }
+    bwd_prologue<K, TILE>(scr + tid);
+    __syncwarp();
+    for (int base = 0; base < total; base += 32) {   // warp-uniform trip count
+        const int e = base + lane;
+        if (e < total) {
+            DGAL_ASSERT(e < 32 * 2 * K);
+            const uint32_t ent = queue[e];
+            DGAL_ASSERT((int)(ent >> 8) < 32);
+            const int pt = warp * 32 + (int)(ent >> 8);
+            bwd_crossing<K, TILE>(tx1 + pt * K, ty1 + pt * K, tx2 + pt * K, ty2 + pt * K, ent & 0xFFu, scr + pt);
+        }
+    }
+    __syncwarp();
+    if (live)
+        bwd_epilogue<K, TILE>(tx1 + tid * K, ty1 + tid * K, tx2 + tid * K, ty2 + tid * K, g, V, scr + tid, G1, G2,
+                              ex, co);
 }
 
 }  // namespace dgal

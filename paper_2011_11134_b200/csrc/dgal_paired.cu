@@ -19,10 +19,10 @@ __device__ __forceinline__ void recentre(Poly<K> &P, Poly<K> &Q)
     }
 }
 
-// Forward, one pair per thread, direct streaming loads.  Used for K=4: that
-// kernel is issue-bound (ncu: not_selected / math_pipe_throttle), so the extra
-// registers of the persistent pipeline (3 instead of 4 CTAs/SM) cost more than
-// the latency it hides.
+// Forward, one pair per thread, direct streaming loads.  The kernel is
+// issue-bound (ncu: not_selected / math_pipe_throttle), so a persistent
+// bulk-copy pipeline (tried: DESIGN.md §4.1) costs more in registers than the
+// latency it hides; for K = 8 it also spills.
 template <int K>
 __global__ void __launch_bounds__(kPairedThreads)
 paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
@@ -45,90 +45,6 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
         v.x = r.seq.w[0];
         v.y = r.seq.w[Seq<K>::NW - 1];
         __stcs(reinterpret_cast<ulonglong2 *>(xflags) + k, v);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Forward: persistent CTAs fed by bulk copies (same pipeline as the backward)
-// ---------------------------------------------------------------------------
-constexpr int kFwdTile = 256;
-
-template <int K>
-struct FwdSmem {
-    struct Stage {
-        float x1[kFwdTile * K], y1[kFwdTile * K], x2[kFwdTile * K], y2[kFwdTile * K];
-    };
-    Stage st[2];
-    uint64_t bar[2];
-};
-
-template <int K>
-__global__ void __launch_bounds__(kFwdTile, 1)
-paired_fwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
-                  const float *__restrict__ x2, const float *__restrict__ y2,
-                  float *__restrict__ iou, uint8_t *__restrict__ nx, uint8_t *__restrict__ xflags)
-{
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    FwdSmem<K> &S = *reinterpret_cast<FwdSmem<K> *>(smem_raw);
-    const int tid = threadIdx.x;
-    const int64_t ntiles = (n + kFwdTile - 1) / kFwdTile;
-    const int64_t nfull = n / kFwdTile;
-    constexpr uint32_t kPlane = kFwdTile * K * 4u;
-    if (tid == 0) {
-        mbar_init(&S.bar[0], 1);
-        mbar_init(&S.bar[1], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    auto issue = [&](int64_t tile, int s) {
-        const int64_t b = tile * kFwdTile * K;
-        mbar_arrive_expect_tx(&S.bar[s], 4 * kPlane);
-        bulk_g2s(S.st[s].x1, x1 + b, kPlane, &S.bar[s]);
-        bulk_g2s(S.st[s].y1, y1 + b, kPlane, &S.bar[s]);
-        bulk_g2s(S.st[s].x2, x2 + b, kPlane, &S.bar[s]);
-        bulk_g2s(S.st[s].y2, y2 + b, kPlane, &S.bar[s]);
-    };
-    int64_t tile = blockIdx.x;
-    if (tid == 0 && tile < nfull) issue(tile, 0);
-    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-        const int s = it & 1;
-        const int64_t next = tile + gridDim.x;
-        if (tid == 0 && next < nfull) issue(next, s ^ 1);
-        const int64_t k = tile * kFwdTile + tid;
-        Poly<K> P, Q;
-        if (tile < nfull) {
-            mbar_wait(&S.bar[s], (uint32_t)(it >> 1) & 1u);
-            const typename FwdSmem<K>::Stage &T = S.st[s];
-#pragma unroll
-            for (int q = 0; q < K / 4; ++q) {
-                const float4 a = reinterpret_cast<const float4 *>(T.x1)[tid * (K / 4) + q];
-                const float4 b = reinterpret_cast<const float4 *>(T.y1)[tid * (K / 4) + q];
-                const float4 c = reinterpret_cast<const float4 *>(T.x2)[tid * (K / 4) + q];
-                const float4 d = reinterpret_cast<const float4 *>(T.y2)[tid * (K / 4) + q];
-                P.x[4 * q] = a.x; P.x[4 * q + 1] = a.y; P.x[4 * q + 2] = a.z; P.x[4 * q + 3] = a.w;
-                P.y[4 * q] = b.x; P.y[4 * q + 1] = b.y; P.y[4 * q + 2] = b.z; P.y[4 * q + 3] = b.w;
-                Q.x[4 * q] = c.x; Q.x[4 * q + 1] = c.y; Q.x[4 * q + 2] = c.z; Q.x[4 * q + 3] = c.w;
-                Q.y[4 * q] = d.x; Q.y[4 * q + 1] = d.y; Q.y[4 * q + 2] = d.z; Q.y[4 * q + 3] = d.w;
-            }
-        } else if (k < n) {
-            load_poly<K>(x1, y1, k, P);
-            load_poly<K>(x2, y2, k, Q);
-        }
-        __syncthreads();  // stage s consumed (values are in registers) before it is refilled
-        if (k < n) {
-            recentre<K>(P, Q);
-            const FwdOut<K, true> r = iou_fwd<K, true>(P, Q);
-            __stcs(iou + k, r.iou);
-            nx[k] = (uint8_t)r.nx;
-            if (K == 4) {
-                __stcs(reinterpret_cast<unsigned long long *>(xflags) + k, (unsigned long long)r.seq.w[0]);
-            } else {
-                ulonglong2 v;
-                v.x = r.seq.w[0];
-                v.y = r.seq.w[Seq<K>::NW - 1];
-                __stcs(reinterpret_cast<ulonglong2 *>(xflags) + k, v);
-            }
-        }
     }
 }
 
@@ -217,57 +133,16 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
             for (int q = 0; q < K / 4; ++q)
                 T.xf[tid * (K / 4) + q] = reinterpret_cast<const uint64_t *>(xflags)[k * (K / 4) + q];
         }
-        // ---- per pair: provenance bits, crossing bytes -> the warp's queue ----
-        const int warp = tid >> 5, lane = tid & 31;
+        // ---- per pair: provenance bits, the warp's crossings, epilogue ----
         const bool live = k < n;
         Seq<K> sq;
 #pragma unroll
         for (int q = 0; q < K / 4; ++q) sq.w[q] = live ? T.xf[tid * (K / 4) + q] : 0ull;
         const int m = live ? T.nx[tid] : 0;
-        uint32_t V = 0;
-        int cnt = 0;
-#pragma unroll
-        for (int p = 0; p < 2 * K; ++p) {
-            const uint32_t b = (p < m) ? seq_byte<K>(sq, p) : 0u;
-            V |= S.lut.v[b];
-            cnt += (b >= 0xC0u);
-        }
-        int incl = cnt;                                  // warp prefix sum of the counts
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-            if (lane >= d) incl += v;
-        }
-        const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        int at = incl - cnt;
-        uint16_t *queue = S.queue[warp];
-#pragma unroll
-        for (int p = 0; p < 2 * K; ++p) {
-            const uint32_t b = (p < m) ? seq_byte<K>(sq, p) : 0u;
-            if (b >= 0xC0u) {
-                DGAL_ASSERT(at >= 0 && at < 32 * 2 * K);
-                queue[at++] = (uint16_t)((lane << 8) | b);
-            }
-        }
-        bwd_prologue<K, kTile>(S.scr + tid);
-        __syncwarp();
-        // ---- the warp's crossings, 32 at a time (full SIMT efficiency) ----
-        for (int base = 0; base < total; base += 32) {   // warp-uniform trip count
-            const int e = base + lane;
-            if (e < total) {
-                DGAL_ASSERT(e < 32 * 2 * K);
-                const uint32_t ent = queue[e];
-                DGAL_ASSERT((int)(ent >> 8) < 32);
-                const int pt = warp * 32 + (int)(ent >> 8);
-                bwd_crossing<K, kTile>(T.x1 + pt * K, T.y1 + pt * K, T.x2 + pt * K, T.y2 + pt * K,
-                                       ent & 0xFFu, S.scr + pt);
-            }
-        }
-        __syncwarp();
+        Poly<K> G1, G2;
+        bwd_tile_pair<K, kTile>(T.x1, T.y1, T.x2, T.y2, sq, m, live ? T.g[tid] : 0.f, live, S.scr,
+                                S.queue[tid >> 5], S.lut, G1, G2);
         if (live) {
-            Poly<K> G1, G2;
-            bwd_epilogue<K, kTile>(T.x1 + tid * K, T.y1 + tid * K, T.x2 + tid * K, T.y2 + tid * K, T.g[tid], V,
-                                   S.scr + tid, G1, G2);
             store_plane<K>(gx1, k, G1.x);
             store_plane<K>(gy1, k, G1.y);
             store_plane<K>(gx2, k, G2.x);
@@ -277,42 +152,16 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
     }
 }
 
-namespace {
-template <int K>
-cudaError_t launch_fwd_k(int64_t n, const float *x1, const float *y1, const float *x2, const float *y2,
-                         float *iou, uint8_t *nx, uint8_t *xflags, cudaStream_t st)
-{
-    static int dev_cached = -1, limit = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const size_t smem = sizeof(FwdSmem<K>);
-    if (dev != dev_cached) {
-        cudaError_t e = cudaFuncSetAttribute(paired_fwd_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        int sms = 0, per = 0;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, paired_fwd_kernel<K>, kFwdTile, smem);
-        limit = sms * (per > 0 ? per : 1);
-        dev_cached = dev;
-    }
-    const int64_t ntiles = (n + kFwdTile - 1) / kFwdTile;
-    const unsigned grid = (unsigned)(ntiles < limit ? ntiles : limit);
-    paired_fwd_kernel<K><<<grid, kFwdTile, smem, st>>>(n, x1, y1, x2, y2, iou, nx, xflags);
-    return cudaGetLastError();
-}
-}  // namespace
-
 cudaError_t launch_paired_fwd(int K, int64_t n, const float *x1, const float *y1, const float *x2,
                               const float *y2, float *iou, uint8_t *nx, uint8_t *xflags,
                               cudaStream_t st)
 {
-    if (K == 4) {
-        const unsigned grid = (unsigned)((n + kPairedThreads - 1) / kPairedThreads);
+    const unsigned grid = (unsigned)((n + kPairedThreads - 1) / kPairedThreads);
+    if (K == 4)
         paired_fwd_direct_kernel<4><<<grid, kPairedThreads, 0, st>>>(n, x1, y1, x2, y2, iou, nx, xflags);
-        return cudaGetLastError();
-    }
-    return launch_fwd_k<8>(n, x1, y1, x2, y2, iou, nx, xflags, st);
+    else
+        paired_fwd_direct_kernel<8><<<grid, kPairedThreads, 0, st>>>(n, x1, y1, x2, y2, iou, nx, xflags);
+    return cudaGetLastError();
 }
 
 namespace {

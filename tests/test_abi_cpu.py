@@ -25,6 +25,7 @@ def _declared():
 def test_header_declares_the_boundary():
     names = _declared()
     assert names == sorted(["dgal_iou_paired_fwd", "dgal_iou_paired_bwd", "dgal_iou_paired_fused",
+                            "dgal_box_iou_paired_fwd", "dgal_box_iou_paired_bwd", "dgal_box_iou_paired_fused",
                             "dgal_iou_pairwise",
                             "dgal_pairwise_workspace_bytes", "dgal_nms_round", "dgal_nms_keep",
                             "dgal_status_string", "dgal_build_info"])
@@ -67,6 +68,15 @@ def test_host_side_validation_without_gpu():
     # n == 0 is a no-op
     assert L.dgal_iou_paired_fwd(4, 0, None, None, None, None, None, None, None, None) == 0
     assert L.dgal_iou_paired_bwd(4, 0, *([None] * 11), None) == 0
+    # boxes: bad dims / layout, NULL, misaligned, n == 0
+    assert L.dgal_box_iou_paired_fwd(4, 0, 8, P(a), P(a), P(a), P(a), P(a), None) == 1
+    assert L.dgal_box_iou_paired_fwd(2, 2, 8, P(a), P(a), P(a), P(a), P(a), None) == 1
+    assert L.dgal_box_iou_paired_fwd(2, 0, 8, None, P(a), P(a), P(a), P(a), None) == 1
+    assert L.dgal_box_iou_paired_fwd(3, 1, 8, P(a + 2), P(a), P(a), P(a), P(a), None) == 3
+    assert L.dgal_box_iou_paired_fwd(2, 0, 8, P(a), P(a), P(a), P(a), P(a + 4), None) == 3
+    assert L.dgal_box_iou_paired_fwd(2, 0, 0, None, None, None, None, None, None) == 0
+    assert L.dgal_box_iou_paired_bwd(3, 0, 8, P(a), P(a), None, P(a), P(a), P(a), P(a), None) == 1
+    assert L.dgal_box_iou_paired_fused(2, 0, 8, P(a), P(a), None, 1.0, None, None, P(a), None) == 1
     # pairwise: nothing requested, negative threshold with a mask, short mask rows
     args = [4, 8, P(a), P(a), 8, P(a), P(a), 0]
     assert L.dgal_iou_pairwise(*args, None, 0.5, None, 0, None, None, 0, None, 0, None) == 1
@@ -104,9 +114,11 @@ def test_sass_is_sm100a_register_resident():
     assert "sm_100a" in out
     stats = _sass_stats()
     names = " ".join(stats)
-    for k in ("paired_fwd_direct_kernelILi4", "paired_fwd_kernelILi8", "paired_bwd_kernelILi4",
+    for k in ("paired_fwd_direct_kernelILi4", "paired_fwd_direct_kernelILi8", "paired_bwd_kernelILi4",
               "paired_fused_kernelILi4", "paired_fused_kernelILi8",
-              "paired_bwd_kernelILi8", "pairwise_kernelILi4", "nms_keep_kernel", "nms_round_kernel"):
+              "paired_bwd_kernelILi8", "pairwise_kernelILi4", "nms_keep_kernel", "nms_round_kernel",
+              "box_fwd_kernelILi2", "box_fwd_kernelILi3", "box_bwd_kernelILi2", "box_bwd_kernelILi3",
+              "box_fused_kernelILi2", "box_fused_kernelILi3"):
         assert k in names, k
     for name, c in stats.items():
         assert c.get("LDL", 0) == 0 and c.get("STL", 0) == 0, (name, c.get("LDL"), c.get("STL"))

@@ -1,0 +1,195 @@
+"""GPU parity of the rotated-box front end (dgal_box_iou_paired_fwd/bwd/fused;
+SURVEY §8(f) f1 2D boxes and f3 yaw-only 3D boxes) against the oracle, through
+the C ABI.  Same tolerances as the polygon path: nx/xflags bit-exact on margin
+inputs, IoU <= 1e-5 abs, parameter gradients <= 1e-4 abs or <= 1e-3 rel."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2011_11134_b200 as dgal
+import synth
+from gpu_util import assert_flags_exact, assert_grad_close, assert_iou_close, dev
+from helpers import box_margin_batch, box_margin_ok
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_box(b, layout="planes", grad=None):
+    """BoxPairBatch -> (iou, nx, xf, gb1 [P, n], gb2 [P, n]) through fwd + bwd."""
+    if layout == "planes":
+        b1, b2 = torch.from_numpy(b.b1).to(dev()), torch.from_numpy(b.b2).to(dev())
+    else:
+        b1 = torch.from_numpy(np.ascontiguousarray(b.b1.T)).to(dev())
+        b2 = torch.from_numpy(np.ascontiguousarray(b.b2.T)).to(dev())
+    iou, nx, xf = dgal.box_iou_paired_fwd(b1, b2, layout)
+    g = torch.from_numpy(b.grad if grad is None else grad).to(dev())
+    g1, g2 = dgal.box_iou_paired_bwd(b1, b2, g, nx, xf, layout)
+    torch.cuda.synchronize()
+    g1, g2 = g1.cpu().numpy(), g2.cpu().numpy()
+    if layout == "rows":
+        g1, g2 = g1.T, g2.T
+    return iou.cpu().numpy(), nx.cpu().numpy(), xf.cpu().numpy(), g1, g2
+
+
+def check_box_against_oracle(b, flags=True, layout="planes"):
+    iou, nx, xf, g1, g2 = gpu_box(b, layout)
+    r1, r2 = b.rows64()
+    ref = oracle.box_iou_paired(r1, r2, b.grad.astype(np.float64))
+    assert_iou_close(iou, ref["iou"])
+    if flags:
+        assert_flags_exact(nx, xf, ref)
+    assert_grad_close(g1.T, ref["gb1"])
+    assert_grad_close(g2.T, ref["gb2"])
+    return iou, nx, xf, g1, g2, ref
+
+
+def _batch(rows1, rows2, grad=None):
+    r1 = np.asarray(rows1, np.float32)
+    r2 = np.asarray(rows2, np.float32)
+    g = np.ones(len(r1), np.float32) if grad is None else np.asarray(grad, np.float32)
+    return synth.BoxPairBatch(np.ascontiguousarray(r1.T), np.ascontiguousarray(r2.T), g)
+
+
+@pytest.mark.parametrize("dims", [2, 3])
+@pytest.mark.parametrize("n", [1, 31, 257, 4097, 40_000])
+def test_box_margin_inputs_full_compare(dims, n):
+    check_box_against_oracle(box_margin_batch(dims, n))
+
+
+@pytest.mark.parametrize("dims", [2, 3])
+def test_rows_layout_is_bitwise_planes(dims):
+    b = box_margin_batch(dims, 3000)
+    a = gpu_box(b, "planes")
+    r = gpu_box(b, "rows")
+    for x, y in zip(a, r):
+        assert np.array_equal(x, y)
+    check_box_against_oracle(b, layout="rows")
+
+
+def test_box_equals_polygon_path_on_its_corners():
+    """The box forward is the polygon forward on box_to_polygon's corners: IoU
+    within rounding of the two corner computations, flags identical."""
+    b = box_margin_batch(2, 5000)
+    iou, nx, xf, _, _ = gpu_box(b)
+    r1, r2 = b.rows64()
+    x1, y1 = oracle.box_corners(r1)
+    x2, y2 = oracle.box_corners(r2)
+    T = lambda a: torch.from_numpy(a.astype(np.float32)).to(dev())  # noqa: E731
+    pi, pn, pf = dgal.iou_paired_fwd(T(x1), T(y1), T(x2), T(y2))
+    assert np.max(np.abs(pi.cpu().numpy() - iou)) <= 2e-5
+    assert np.array_equal(pn.cpu().numpy(), nx) and np.array_equal(pf.cpu().numpy(), xf)
+
+
+def test_box_worked_examples():
+    """S:370-372, S:390-392 on the device."""
+    rows2 = [[0, 0, 2, 2, 0], [3, -2, 4, 1.5, 0.4], [0, 0, 2, 2, 0.3]]
+    rows2b = [[0, 0, 2, 2, math.pi / 4], [3, -2, 4, 1.5, 0.4], [10, 0, 2, 2, 1.1]]
+    iou, nx, xf, g1, g2 = gpu_box(_batch(rows2, rows2b))
+    assert abs(iou[0] - 1 / math.sqrt(2)) < 2e-6 and nx[0] == 8          # octagon
+    assert iou[1] == 1.0                                                 # identical
+    assert abs(g1[0, 1]) < 1e-5 and abs(g1[1, 1]) < 1e-5                 # stationary
+    assert iou[2] == 0.0 and nx[2] == 0 and np.all(g1[:, 2] == 0)        # disjoint
+    rows3 = [[0, 0, 0, 1, 1, 1, 0], [0, 0, 0, 1, 1, 1, 0], [0, 0, 0, 1, 1, 1, 0.2], [0, 0, 0, 1, 1, 1, 0]]
+    rows3b = [[0, 0, 0, 1, 1, 1, 0], [0.5, 0.5, 0.5, 1, 1, 1, 0], [0.1, 0, 1.0, 1, 1, 1, 0], [0, 0, 0.3, 1, 1, 1, 0]]
+    iou, nx, xf, g1, g2 = gpu_box(_batch(rows3, rows3b))
+    assert iou[0] == 1.0
+    assert abs(iou[1] - 1 / 15) < 1e-6
+    assert iou[2] == 0.0 and nx[2] == 0 and np.all(g1[:, 2] == 0) and np.all(g2[:, 2] == 0)
+    assert abs(g2[2, 3] + 2 / 1.3 ** 2) < 1e-5                           # dz closed form
+
+
+def test_3d_reduces_to_2d_on_device():
+    b3 = box_margin_batch(3, 4000)
+    b3.b2[2] = b3.b1[2]
+    b3.b2[5] = b3.b1[5]
+    i3 = gpu_box(b3)[0]
+    b2 = synth.BoxPairBatch(np.ascontiguousarray(b3.b1[[0, 1, 3, 4, 6]]),
+                            np.ascontiguousarray(b3.b2[[0, 1, 3, 4, 6]]), b3.grad)
+    i2 = gpu_box(b2)[0]
+    assert np.max(np.abs(i3 - i2)) <= 2e-6
+
+
+@pytest.mark.parametrize("dims", [2, 3])
+def test_box_fused_matches_oracle_and_split(dims):
+    b = box_margin_batch(dims, 20_000)
+    B1, B2 = torch.from_numpy(b.b1).to(dev()), torch.from_numpy(b.b2).to(dev())
+    g = torch.from_numpy(b.grad).to(dev())
+    iou, g1, g2 = dgal.box_iou_paired_fused(B1, B2, grad=g)
+    torch.cuda.synchronize()
+    r1, r2 = b.rows64()
+    ref = oracle.box_iou_paired(r1, r2, b.grad.astype(np.float64))
+    assert_iou_close(iou.cpu().numpy(), ref["iou"])
+    assert_grad_close(g1.cpu().numpy().T, ref["gb1"])
+    assert_grad_close(g2.cpu().numpy().T, ref["gb2"])
+    # scalar-gradient form == per-pair form with a constant vector, bitwise
+    _, h1, _ = dgal.box_iou_paired_fused(B1, B2, scale=-0.25, want_iou=False)
+    _, k1, _ = dgal.box_iou_paired_fused(B1, B2, grad=torch.full_like(g, -0.25))
+    assert torch.equal(h1, k1)
+
+
+def test_box_autograd_and_loss():
+    b = box_margin_batch(3, 2000)
+    B1 = torch.from_numpy(b.b1).to(dev()).requires_grad_(True)
+    B2 = torch.from_numpy(b.b2).to(dev()).requires_grad_(True)
+    iou = dgal.BoxIoU.apply(B1, B2, "planes")
+    (iou * torch.from_numpy(b.grad).to(dev())).sum().backward()
+    r1, r2 = b.rows64()
+    ref = oracle.box_iou_paired(r1, r2, b.grad.astype(np.float64))
+    assert_grad_close(B1.grad.cpu().numpy().T, ref["gb1"])
+    assert_grad_close(B2.grad.cpu().numpy().T, ref["gb2"])
+    B1.grad = None
+    B2.grad = None
+    loss = dgal.BoxIoULoss.apply(B1, B2, "planes")
+    loss.backward()
+    ref = oracle.box_iou_paired(r1, r2, np.full(b.n, -1.0 / b.n))
+    assert abs(loss.item() - (1 - ref["iou"]).mean()) < 1e-5
+    assert_grad_close(B1.grad.cpu().numpy().T, ref["gb1"])
+
+
+def test_box_empty_batch_is_noop():
+    z = torch.empty(5, 0, device=dev())
+    iou, nx, xf = dgal.box_iou_paired_fwd(z, z)
+    assert iou.numel() == 0
+
+
+@pytest.mark.parametrize("dims", [2, 3])
+def test_box_full_size_sampled(dims):
+    """bench.py's box workload (2^24 pairs, one launch each); sampled pairs vs the
+    oracle, flags / gradients on the margin-passing ones; invariants on all."""
+    b = synth.gen_box_pairs(1 << 24, dims)
+    iou, nx, xf, g1, g2 = gpu_box(b)
+    rng = np.random.default_rng(dims)
+    idx = np.sort(rng.choice(b.n, size=50_000, replace=False))
+    s = b.take(idx)
+    r1, r2 = s.rows64()
+    ref = oracle.box_iou_paired(r1, r2, s.grad.astype(np.float64))
+    assert_iou_close(iou[idx], ref["iou"])
+    ok = box_margin_ok(r1, r2)
+    assert ok.mean() > 0.8
+    assert_flags_exact(nx[idx][ok], xf[idx][ok], {"nx": ref["nx"][ok], "xflags": ref["xflags"][ok]})
+    assert_grad_close(g1[:, idx].T[ok], ref["gb1"][ok])
+    assert_grad_close(g2[:, idx].T[ok], ref["gb2"][ok])
+    assert np.all((iou >= 0) & (iou <= 1))
+    assert np.all(iou[nx == 0] == 0)
+
+
+@pytest.mark.parametrize("scale", [1e-7, 1e-6, 1e-5, 1e-4, 1e-3, 1e-2])
+def test_near_coincident_boxes_iou(scale):
+    """Prediction ~ target box pairs (nearly coincident edges): IoU within 1e-5 on
+    every pair, 2D and 3D."""
+    from test_gpu_paired import _near_coincident_boxes
+    b1, b2 = _near_coincident_boxes(100_000, scale, seed=7 + int(-math.log10(scale)))
+    g = np.ones(b1.shape[1], np.float32)
+    iou = gpu_box(synth.BoxPairBatch(b1, b2, g))[0]
+    ref = oracle.box_iou_paired(b1.T.astype(np.float64), b2.T.astype(np.float64))["iou"]
+    assert_iou_close(iou, ref)
+    rng = np.random.default_rng(3)
+    z = rng.normal(-1, 0.4, b1.shape[1]); d = rng.uniform(1.4, 1.9, b1.shape[1])
+    b13 = np.concatenate([b1[:2], z[None], b1[2:4], d[None], b1[4:]]).astype(np.float32)
+    b23 = np.concatenate([b2[:2], (z + scale * rng.normal(size=z.size))[None], b2[2:4], d[None], b2[4:]]).astype(np.float32)
+    iou3 = gpu_box(synth.BoxPairBatch(b13, b23, g))[0]
+    ref3 = oracle.box_iou_paired(b13.T.astype(np.float64), b23.T.astype(np.float64))["iou"]
+    assert_iou_close(iou3, ref3)

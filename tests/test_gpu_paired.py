@@ -232,3 +232,49 @@ def test_fused_loss_autograd():
     rg = oracle.iou_paired_bwd(b.p1, b.p2, np.full(b.n, -1.0 / b.n))
     for t, want in zip(ts, rg):
         assert_grad_close(t.grad.cpu().numpy().reshape(want.shape), want)
+
+
+def _near_coincident_boxes(n, scale, seed):
+    """Box pairs b2 = b1 + perturbation of relative size `scale` on a random subset of
+    the parameters (prediction ~ target: nearly coincident edges, shared vertices)."""
+    rng = np.random.default_rng(seed)
+    cx = rng.uniform(0, 70, n); cy = rng.uniform(-40, 40, n)
+    w = rng.uniform(0.5, 5, n); h = rng.uniform(0.5, 2, n); th = rng.uniform(-np.pi, np.pi, n)
+    b1 = np.stack([cx, cy, w, h, th]).astype(np.float32)
+    pert = rng.normal(size=(5, n)) * scale * np.array([w, w, w, h, np.ones(n)])
+    pert *= rng.uniform(size=(5, n)) < 0.6
+    b2 = (b1.astype(np.float64) + pert).astype(np.float32)
+    return b1, b2
+
+
+@pytest.mark.parametrize("scale", [1e-7, 1e-6, 1e-5, 1e-4, 1e-3, 1e-2])
+def test_near_coincident_polygons_iou(scale):
+    """The converged-training regime: IoU within 1e-5 of the oracle on every pair
+    (closure of the clip), not only on margin inputs."""
+    b1, b2 = _near_coincident_boxes(100_000, scale, seed=int(-math.log10(scale)))
+    x1, y1 = oracle.box_corners(b1.T.astype(np.float64))
+    x2, y2 = oracle.box_corners(b2.T.astype(np.float64))
+    x1, y1, x2, y2 = (a.astype(np.float32) for a in (x1, y1, x2, y2))
+    T = lambda a: torch.from_numpy(a).to(dev())  # noqa: E731
+    iou, nx, xf = dgal.iou_paired_fwd(T(x1), T(y1), T(x2), T(y2))
+    ref = oracle.iou_paired_fwd((x1, y1), (x2, y2))
+    assert_iou_close(iou.cpu().numpy(), ref["iou"])
+    nxc = nx.cpu().numpy()
+    assert np.all((nxc >= 3) & (nxc <= 8))          # always a valid record for the backward
+
+
+def test_integer_grid_rectangles_on_device():
+    """Exact shared edges / touching / containment: the axis-aligned closed form."""
+    rng = np.random.default_rng(12)
+    g = rng.integers(0, 4, size=(50_000, 8)).astype(np.float32)
+    x0, y0, a, b = g[:, 0], g[:, 1], 1 + g[:, 2], 1 + g[:, 3]
+    u0, v0, c, d = g[:, 4], g[:, 5], 1 + g[:, 6], 1 + g[:, 7]
+    P = [np.stack([x0, x0 + a, x0 + a, x0], 1), np.stack([y0, y0, y0 + b, y0 + b], 1)]
+    Q = [np.stack([u0, u0 + c, u0 + c, u0], 1), np.stack([v0, v0, v0 + d, v0 + d], 1)]
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev())  # noqa: E731
+    iou = dgal.iou_paired_fwd(T(P[0]), T(P[1]), T(Q[0]), T(Q[1]))[0].cpu().numpy()
+    ox = np.clip(np.minimum(x0 + a, u0 + c) - np.maximum(x0, u0), 0, None)
+    oy = np.clip(np.minimum(y0 + b, v0 + d) - np.maximum(y0, v0), 0, None)
+    ai = ox * oy
+    want = ai / (a * b + c * d - ai)
+    assert np.max(np.abs(iou - want)) <= 1e-6

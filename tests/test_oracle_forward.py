@@ -372,3 +372,35 @@ def test_canonical_start_convention(cfg):
             assert flags[0] == min(flags)
         a = 0.5 * np.sum(verts[:, 0] * np.roll(verts[:, 1], -1) - np.roll(verts[:, 0], -1) * verts[:, 1])
         assert a > 0
+
+
+# --- degenerate geometry pinned to closed forms (R5 boundary-inclusive) --------
+def test_nested_collinear_boxes_closed_form():
+    """Same centre, height and yaw, widths w and w(1 - delta): p2 inside p1 with two
+    collinear edge pairs; IoU = A2/A1 = 1 - delta exactly (by definition)."""
+    rng = np.random.default_rng(11)
+    n = 400
+    w = rng.uniform(0.5, 5, n); h = rng.uniform(0.5, 2, n); th = rng.uniform(-4, 4, n)
+    cx = rng.uniform(0, 70, n); cy = rng.uniform(-40, 40, n)
+    delta = rng.choice([1e-7, 1e-6, 1e-4, 1e-2, 0.3], n)
+    b1 = np.stack([cx, cy, w, h, th], 1)
+    b2 = np.stack([cx, cy, w * (1 - delta), h, th], 1)
+    r = oracle.box_iou_paired(b1, b2)
+    assert np.max(np.abs(r["iou"] - (1 - delta))) < 1e-9
+
+
+def test_integer_grid_rectangles_closed_form():
+    """Axis-aligned rectangles on an integer grid (exact shared edges, touching,
+    containment): IoU from the interval-overlap closed form."""
+    rng = np.random.default_rng(12)
+    g = rng.integers(0, 4, size=(3000, 8)).astype(float)
+    x0, y0, a, b = g[:, 0], g[:, 1], 1 + g[:, 2], 1 + g[:, 3]
+    u0, v0, c, d = g[:, 4], g[:, 5], 1 + g[:, 6], 1 + g[:, 7]
+    P = [np.stack([x0, x0 + a, x0 + a, x0], 1), np.stack([y0, y0, y0 + b, y0 + b], 1)]
+    Q = [np.stack([u0, u0 + c, u0 + c, u0], 1), np.stack([v0, v0, v0 + d, v0 + d], 1)]
+    r = oracle.iou_paired_fwd(tuple(P), tuple(Q))
+    ox = np.clip(np.minimum(x0 + a, u0 + c) - np.maximum(x0, u0), 0, None)
+    oy = np.clip(np.minimum(y0 + b, v0 + d) - np.maximum(y0, v0), 0, None)
+    ai = ox * oy
+    want = ai / (a * b + c * d - ai)
+    assert np.max(np.abs(r["iou"] - want)) < 1e-12
