@@ -8,6 +8,9 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 # DGAL_CHECKED=1 selects the bounds-checked build (device asserts), see build.py
 SO_PATH = os.path.join(HERE, "libdgal_checked.so" if os.environ.get("DGAL_CHECKED") == "1" else "libdgal.so")
+# DGAL_SO=<path>: load another build of the same library (A/B timing of build
+# variants, tools/probes/); it must be a libdgal build, there is no other path.
+SO_PATH = os.environ.get("DGAL_SO", SO_PATH)
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

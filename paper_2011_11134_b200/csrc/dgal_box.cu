@@ -5,8 +5,8 @@
 // The boxes are read as parameters (20 B per 2D box, 28 B per yaw-only 3D box
 // instead of 32 B of corners) and turned into Poly<4> in registers:
 //   box_to_polygon: corners c + R(theta)(+-w/2, +-h/2), CCW from (-w/2, -h/2),
-// taken relative to the centre of box 1 (IoU is translation invariant; corners
-// near 0 keep the decision predicates accurate).  The clip, the flags and the
+// taken relative to the centre of box 1 and then to its corner 0 (IoU is
+// translation invariant; corners near 0 keep the decision predicates accurate).  The clip, the flags and the
 // backward phases are the polygon path's (dgal_core.cuh).  3D: V = A d, V_i =
 // A_i dz with dz the overlap of the z extents.  The backward maps the
 // corner gradients to the box parameters (box_to_polygon_grad) and adds
@@ -23,6 +23,17 @@ namespace dgal {
 namespace {
 
 constexpr int kBoxTile = 256;  // backward tile = CTA size
+// CTAs per SM the box forward / fused kernels are register-budgeted for (the
+// largest without local-memory spills, tools/sass_stats.py)
+#ifndef DGAL_BOX_FWD2_MINB
+#define DGAL_BOX_FWD2_MINB 3
+#endif
+#ifndef DGAL_BOX_FWD3_MINB
+#define DGAL_BOX_FWD3_MINB 2
+#endif
+#ifndef DGAL_BOX_FUSED_MINB
+#define DGAL_BOX_FUSED_MINB 2
+#endif
 
 template <int DIMS>
 struct Box {
@@ -79,6 +90,16 @@ __device__ __forceinline__ Trig box_pair_polys(const Box<DIMS> &a, const Box<DIM
     box_sincos(b.th, t.s2, t.c2);
     box_poly(0.f, 0.f, a.w, a.h, t.c1, t.s1, P);
     box_poly(__fsub_rn(b.cx, a.cx), __fsub_rn(b.cy, a.cy), b.w, b.h, t.c2, t.s2, Q);
+    // then on p1's corner 0, as the polygon path (same floats for identical boxes;
+    // p1.v0 == 0 exactly lets the compiler fold it)
+    const float ox = P.x[0], oy = P.y[0];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        P.x[k] = __fsub_rn(P.x[k], ox); P.y[k] = __fsub_rn(P.y[k], oy);
+        Q.x[k] = __fsub_rn(Q.x[k], ox); Q.y[k] = __fsub_rn(Q.y[k], oy);
+    }
+    P.x[0] = 0.f;
+    P.y[0] = 0.f;
     return t;
 }
 
@@ -163,7 +184,7 @@ __device__ __forceinline__ void z_grads(const VolCoef &co, const ZOver &z, float
 // forward: IoU (2D) or 3D IoU, nx / xflags of the BEV intersection
 // ---------------------------------------------------------------------------
 template <int DIMS>
-__global__ void __launch_bounds__(kPairedThreads)
+__global__ void __launch_bounds__(kPairedThreads, DIMS == 2 ? DGAL_BOX_FWD2_MINB : DGAL_BOX_FWD3_MINB)
 box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict__ b2, int64_t sk, int64_t sp,
                float *__restrict__ iou, uint8_t *__restrict__ nx, uint8_t *__restrict__ xflags)
 {
@@ -251,7 +272,7 @@ box_bwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
 // fused loss forward + backward (f2 on boxes): no nx / xflags round trip
 // ---------------------------------------------------------------------------
 template <int DIMS>
-__global__ void __launch_bounds__(kPairedThreads)
+__global__ void __launch_bounds__(kPairedThreads, DGAL_BOX_FUSED_MINB)
 box_fused_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict__ b2, int64_t sk, int64_t sp,
                  const float *__restrict__ grad, float scale, float *__restrict__ iou, float *__restrict__ gb1,
                  float *__restrict__ gb2)

@@ -106,6 +106,27 @@ __device__ __forceinline__ float pick(const float (&a)[K], int i)
     return r;
 }
 
+// (x[i], y[i]) for a dynamic i in [0, K): a select tree on the bits of i (the two
+// coordinates share the predicates).
+template <int K>
+__device__ __forceinline__ void pick_xy(const float (&x)[K], const float (&y)[K], uint32_t i, float &rx, float &ry)
+{
+    const bool b0 = i & 1u, b1 = i & 2u;
+    float x2[(K + 1) / 2], y2[(K + 1) / 2];
+#pragma unroll
+    for (int k = 0; k < K / 2; ++k) { x2[k] = b0 ? x[2 * k + 1] : x[2 * k]; y2[k] = b0 ? y[2 * k + 1] : y[2 * k]; }
+    if (K == 4) {
+        rx = b1 ? x2[1] : x2[0];
+        ry = b1 ? y2[1] : y2[0];
+    } else {
+        const bool b2 = i & 4u;
+        const float x4a = b1 ? x2[1] : x2[0], x4b = b1 ? x2[3] : x2[2];
+        const float y4a = b1 ? y2[1] : y2[0], y4b = b1 ? y2[3] : y2[2];
+        rx = b2 ? x4b : x4a;
+        ry = b2 ? y4b : y4a;
+    }
+}
+
 // Streaming loads/stores of the SoA planes.
 template <int K>
 __device__ __forceinline__ void load_poly(const float *__restrict__ X, const float *__restrict__ Y,
@@ -223,7 +244,7 @@ struct Clip {
     float t0[K], t1[K];                // boundary piece [t0, t1] on p1 edge i (empty if t0 > t1)
     uint32_t jin, jout;                // line index of the entry / exit of p1 edge i (4 bits each)
     uint32_t valid, enter, leave;      // p1 edges with a piece / an entry / an exit (bit i)
-    float ax[K], ay[K], bx[K], by[K];  // boundary piece on p2 edge j: from (ax, ay) to (bx, by)
+    float ax[K], ay[K], bx[K], by[K];  // PIECES: piece on p2 edge j runs from (ax, ay) to (bx, by)
     uint32_t on2;                      // p2 edges carrying a boundary piece
     uint32_t in2;                      // p2 vertices inside p1 (consistent with the events)
     float A1x2, A2x2, Aix2;            // twice the areas
@@ -231,7 +252,10 @@ struct Clip {
 };
 
 // p1, p2 must already be recentred (coordinates near 0; p1.v0 or a box centre).
-template <int K>
+// PIECES: also materialise the end points of the p2 pieces (c.ax .. c.by; the
+// fused gradient needs them, and for K = 4 the per-edge selects are cheaper than
+// the per-event form, which serves K = 8).
+template <int K, bool PIECES = (K == 4)>
 __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &Q, Clip<K> &c)
 {
     constexpr uint32_t KMASK = (1u << K) - 1u;
@@ -250,30 +274,27 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
         A2x2 = __fadd_rn(A2x2, C2[i]);
     }
 
-    // decision values, shifted by +-tiny (below any non-degenerate value) so that
-    // "inside" is "> 0" on both sides and no value is exactly 0:
+    // decision values, shifted by +tiny (below any non-degenerate value) so that
+    // "inside" is "> 0" and no value is exactly 0:
     //   d[i][j] = f_j x (v_i - w_j) + tiny   p1 vertex i vs p2 line j, CLOSED test (d >= 0)
-    //   e[j][i] = g_i x (w_j - v_i) - tiny   p2 vertex j vs p1 line i, OPEN test (e > 0)
-    float d[K][K], e[K][K];
+    float d[K][K];
 #pragma unroll
     for (int i = 0; i < K; ++i)
 #pragma unroll
         for (int j = 0; j < K; ++j) {
             const float Dx = __fsub_rn(P.x[i], Q.x[j]), Dy = __fsub_rn(P.y[i], Q.y[j]);
             d[i][j] = __fadd_rn(cross_rn(fx[j], fy[j], Dx, Dy), kTiny);
-            e[j][i] = __fsub_rn(cross_rn(Dx, Dy, gx[i], gy[i]), kTiny);
         }
 
-    // Separating axis (closed): an edge line of either polygon with the other
-    // polygon entirely on or outside it -> the intersection has zero area.  This
-    // makes collinear, opposite-facing edges (touching boxes) exactly empty.
+    // Separating p2 edge line (closed): p1 entirely on or outside it -> the
+    // intersection has zero area (makes touching edges exactly empty).
     bool separated = false;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        float m1 = d[0][j], m2 = e[0][j];
+        float m1 = d[0][j];
 #pragma unroll
-        for (int i = 1; i < K; ++i) { m1 = fmaxf(m1, d[i][j]); m2 = fmaxf(m2, e[i][j]); }
-        separated |= (m1 <= kTiny) | (m2 <= 0.f);
+        for (int i = 1; i < K; ++i) m1 = fmaxf(m1, d[i][j]);
+        separated |= (m1 <= kTiny);
     }
 
     // p1 vertices inside p2 (closed test, d never 0)
@@ -289,26 +310,38 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     // Cyrus-Beck intervals of p1's edges.  For the edge a -> b against one line
     // (a, b = the shifted decision values of its end points, never 0): the inside
     // set is {t : a + t (b - a) > 0}; b > a bounds it below by t* = a / (a - b),
-    // b < a above, b == a keeps all (a > 0) or nothing (a < 0).  t* is formed from
-    // the end point nearer the line — a/(a-b) if |a| <= |b|, else 1 + b/(a-b) — so
-    // no cancellation, and an end point on the line gives exactly 0 or 1.
+    // b < a above, b == a keeps all (a > 0) or nothing (a < 0).  An end point that
+    // is inside pins its parameter below, so t* = a/(a-b) only has to be accurate
+    // to an ulp (identical polygons still keep [0, 1] exactly).
     // den + tiny keeps r finite (a == b: r = 1e30, t* = +-huge), so every candidate
     // is finite and carries the index j of its line.  hi starts just above 1 so a
     // candidate that rounds to 1 still wins and keeps its index.
+    // The piece exists iff an end point is inside or t0 < t1 (strictly: an edge
+    // that only touches p2 at a point from outside has none); an inside end pins
+    // its parameter, and the other one is clamped to the edge.
     float *t0 = c.t0, *t1 = c.t1;
     uint32_t jin = 0, jout = 0, valid = 0, enter = 0, leave = 0;
     const float hi0 = __int_as_float(0x3F800008);
-    // Events and the p2 pieces they delimit (same pass): an exit of p1 edge i through
-    // p2 line j_out starts the piece on p2 edge j_out at X_out = v_i + t1 g_i; an
-    // entry through line j_in ends the piece on p2 edge j_in at X_in = v_i + t0 g_i.
-    float *ax = c.ax, *ay = c.ay, *bx = c.bx, *by = c.by;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-        const int j1 = (j + 1) % K;
-        ax[j] = Q.x[j]; ay[j] = Q.y[j];
-        bx[j] = Q.x[j1]; by[j] = Q.y[j1];
-    }
+    // Events (same pass).  An exit of p1 edge i through p2 line j_out starts the p2
+    // piece on edge j_out at X_out = v_i + t1 g_i; an entry through line j_in ends
+    // the piece on edge j_in at X_in = v_i + t0 g_i.  Green's term of such a piece,
+    // X_out x w_j+1, equals C2_j + X_out x w_j up to X_out's distance from line j
+    // (an ulp of its decision values), and w_j x X_in equals C2_j + w_j+1 x X_in
+    // likewise; so the p2 side of the boundary contributes
+    //     sum_{j on boundary} C2_j + sum_exits X_out x w_jout + sum_entries w_jin+1 x X_in
+    // (a piece with both events on one edge adds the product of two vectors along
+    // that edge, which vanishes).  One vertex select per event, no per-edge state.
+    float p2e = 0.f;
     uint32_t ev_out = 0, ev_in = 0;
+    float *ax = c.ax, *ay = c.ay, *bx = c.bx, *by = c.by;
+    if (PIECES) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const int j1 = (j + 1) % K;
+            ax[j] = Q.x[j]; ay[j] = Q.y[j];
+            bx[j] = Q.x[j1]; by[j] = Q.y[j1];
+        }
+    }
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         const int i1 = (i + 1) % K;
@@ -319,15 +352,17 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
             const float den = (a - b) + kTiny;
             const float r = rcp_approx(den);
             const float m = __saturatef(-den * kBig);  // 1: bounds below
-            const float v = (fabsf(a) <= fabsf(b)) ? a * r : fmaf(b, r, 1.f);
-            lo = fmaxf(lo, enc_idx(m * v, j));
-            hi = fminf(hi, enc_idx(fmaf(m, kBig, v), j));
+            const float ve = enc_idx(a * r, j);
+            lo = fmaxf(lo, m * ve);                 // m * ve == ve (bits kept) or 0
+            hi = fminf(hi, fmaf(m, kBig, ve));      // ve (bits kept) or huge
         }
         const bool in_s = (in1 >> i) & 1u, in_e = (in1 >> i1) & 1u;
-        const float a0 = in_s ? 0.f : lo;
-        const float a1 = in_e ? 1.f : fminf(hi, 1.f);
-        // compare without the index bits (they may lift a t0 of 1 above a t1 of 1)
-        const bool ok = __int_as_float(__float_as_int(a0) & ~7) <= __int_as_float(__float_as_int(a1) & ~7);
+        const float hic = fminf(hi, 1.f);
+        const float a0 = in_s ? 0.f : (in_e ? fminf(lo, 1.f) : lo);
+        const float a1 = in_e ? 1.f : (in_s ? fmaxf(hic, 0.f) : hic);
+        // strict, without the index bits (they perturb the last 3 ulps)
+        const bool ok = in_s || in_e ||
+                        (__int_as_float(__float_as_int(a0) & ~7) < __int_as_float(__float_as_int(a1) & ~7));
         const bool has_in = ok && !in_s, has_out = ok && !in_e;
         t0[i] = a0; t1[i] = a1;
         valid |= (uint32_t)ok << i;
@@ -336,18 +371,26 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
         const uint32_t ljin = (uint32_t)dec_idx(lo), ljout = (uint32_t)dec_idx(hi);
         jin |= ljin << (4 * i);
         jout |= ljout << (4 * i);
-        const int ji = has_in ? (int)ljin : 8;   // 8: no event
-        const int jo = has_out ? (int)ljout : 8;
-        ev_in |= has_in ? (1u << ji) : 0u;
-        ev_out |= has_out ? (1u << jo) : 0u;
-        const float xix = fmaf(a0, gx[i], P.x[i]), xiy = fmaf(a0, gy[i], P.y[i]);
+        ev_in |= has_in ? (1u << ljin) : 0u;
+        ev_out |= has_out ? (1u << ljout) : 0u;
         const float xox = fmaf(a1, gx[i], P.x[i]), xoy = fmaf(a1, gy[i], P.y[i]);
+        const float xix = fmaf(a0, gx[i], P.x[i]), xiy = fmaf(a0, gy[i], P.y[i]);
+        if (PIECES) {
+            const int ji = has_in ? (int)ljin : 8;   // 8: no event
+            const int jo = has_out ? (int)ljout : 8;
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-            ax[j] = (jo == j) ? xox : ax[j];
-            ay[j] = (jo == j) ? xoy : ay[j];
-            bx[j] = (ji == j) ? xix : bx[j];
-            by[j] = (ji == j) ? xiy : by[j];
+            for (int j = 0; j < K; ++j) {
+                ax[j] = (jo == j) ? xox : ax[j];
+                ay[j] = (jo == j) ? xoy : ay[j];
+                bx[j] = (ji == j) ? xix : bx[j];
+                by[j] = (ji == j) ? xiy : by[j];
+            }
+        } else {
+            float wox, woy, wix, wiy;
+            pick_xy<K>(Q.x, Q.y, ljout, wox, woy);
+            pick_xy<K>(Q.x, Q.y, (ljin + 1u) & (K - 1u), wix, wiy);
+            p2e += has_out ? cross_rn(xox, xoy, wox, woy) : 0.f;
+            p2e += has_in ? cross_rn(wix, wiy, xix, xiy) : 0.f;
         }
     }
     c.jin = jin; c.jout = jout; c.valid = valid; c.enter = enter; c.leave = leave;
@@ -356,11 +399,20 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     // an exit without an entry after it.  Segmented scan over the doubled cycle:
     // position p carries the end state of the nearest event edge <= p.
     // With no event at all p1's boundary is entirely inside p2 or entirely
-    // outside; in the latter case p2 lies inside p1 unless they are separated.
+    // outside; in the latter case p2 lies inside p1 iff its vertex centroid does
+    // (strictly: a p2 touching p1 from outside is not inside).
     const uint32_t ev = ev_out | ev_in;
     uint32_t in2;
     if (ev == 0u) {
-        in2 = (valid == 0u && !separated) ? KMASK : 0u;
+        float mx = 0.f, my = 0.f;
+#pragma unroll
+        for (int j = 0; j < K; ++j) { mx += Q.x[j]; my += Q.y[j]; }
+        mx *= (1.f / K);
+        my *= (1.f / K);
+        bool cin = true;
+#pragma unroll
+        for (int i = 0; i < K; ++i) cin &= cross_rn(gx[i], gy[i], mx - P.x[i], my - P.y[i]) > 0.f;
+        in2 = (valid == 0u && cin) ? KMASK : 0u;
     } else {
         uint32_t evd = ev | (ev << K);
         uint32_t st = (ev_out & ~ev_in) | ((ev_out & ~ev_in) << K);
@@ -379,9 +431,10 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         Aix2 = fmaf(fmaxf(t1[k] - t0[k], 0.f), C1[k], Aix2);
-        const float c2 = cross_rn(ax[k], ay[k], bx[k], by[k]);
+        const float c2 = PIECES ? cross_rn(ax[k], ay[k], bx[k], by[k]) : C2[k];
         Aix2 = __fadd_rn(Aix2, ((on2 >> k) & 1u) ? c2 : 0.f);
     }
+    if (!PIECES) Aix2 = __fadd_rn(Aix2, p2e);
     Aix2 = fminf(Aix2, fminf(A1x2, A2x2));
     c.A1x2 = A1x2;
     c.A2x2 = A2x2;
@@ -498,7 +551,7 @@ __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, f
     for (int k = 0; k < K; ++k) { G1.x[k] = 0.f; G1.y[k] = 0.f; G2.x[k] = 0.f; G2.y[k] = 0.f; }
     if (co) *co = VolCoef{0.f, 0.f, 0.f, 0.f, 0.f};
     Clip<K> c;
-    clip_intervals<K>(P, Q, c);
+    clip_intervals<K, true>(P, Q, c);
     if (!c.nonempty) return 0.f;
     // V = A d (2D: d = 1); IoU = V_i / V_u
     const float Vix2 = c.Aix2 * ex.dz;
@@ -507,15 +560,16 @@ __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, f
     const float iou = fminf(Vix2 / Vux2, 1.f);
 
     // piece weights (saturate: dead edges carry arbitrary end points, length 0)
-    // p2 pieces: parameters of their end points along the edge (projection; exact
-    // 0 at w_j, 1 up to rounding at w_j+1)
+    // p2 pieces: parameters of their end points (the crossing points of the p1
+    // side) along the edge (projection; exact 0 at w_j)
+    const float *ax = c.ax, *ay = c.ay, *bx = c.bx, *by = c.by;
     float al1[K], be1[K], al2[K], be2[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         const float a0 = __saturatef(c.t0[i]), a1 = __saturatef(c.t1[i]);
         const float inv = rcp_approx(fmaf(c.fx[i], c.fx[i], c.fy[i] * c.fy[i]));
-        const float b0 = __saturatef(fmaf(c.ax[i] - Q.x[i], c.fx[i], (c.ay[i] - Q.y[i]) * c.fy[i]) * inv);
-        const float b1 = __saturatef(fmaf(c.bx[i] - Q.x[i], c.fx[i], (c.by[i] - Q.y[i]) * c.fy[i]) * inv);
+        const float b0 = __saturatef(fmaf(ax[i] - Q.x[i], c.fx[i], (ay[i] - Q.y[i]) * c.fy[i]) * inv);
+        const float b1 = __saturatef(fmaf(bx[i] - Q.x[i], c.fx[i], (by[i] - Q.y[i]) * c.fy[i]) * inv);
         const float l1 = fmaxf(a1 - a0, 0.f);
         const float l2 = ((c.on2 >> i) & 1u) ? fmaxf(b1 - b0, 0.f) : 0.f;
         const float h1 = 0.5f * (a0 + a1), h2 = 0.5f * (b0 + b1);
@@ -633,6 +687,8 @@ __device__ __forceinline__ void bwd_epilogue(const float *sPx, const float *sPy,
             P.x[k] = sPx[k] - ox; P.y[k] = sPy[k] - oy;
             Q.x[k] = sQx[k] - ox; Q.y[k] = sQy[k] - oy;
         }
+        P.x[0] = 0.f;   // exact for finite input; lets the compiler fold it
+        P.y[0] = 0.f;
     }
     float gx[K], gy[K], fx[K], fy[K], C1[K], C2[K];
     float A1x2 = 0.f, A2x2 = 0.f;

@@ -17,14 +17,26 @@ __device__ __forceinline__ void recentre(Poly<K> &P, Poly<K> &Q)
         P.x[k] = __fsub_rn(P.x[k], ox); P.y[k] = __fsub_rn(P.y[k], oy);
         Q.x[k] = __fsub_rn(Q.x[k], ox); Q.y[k] = __fsub_rn(Q.y[k], oy);
     }
+    // x - x == 0 for every finite x: stated as a constant so the compiler folds
+    // the products with p1.v0 (fewer instructions and registers)
+    P.x[0] = 0.f;
+    P.y[0] = 0.f;
 }
 
 // Forward, one pair per thread, direct streaming loads.  The kernel is
 // issue-bound (ncu: not_selected / math_pipe_throttle), so a persistent
 // bulk-copy pipeline (tried: DESIGN.md §4.1) costs more in registers than the
 // latency it hides; for K = 8 it also spills.
+#ifndef DGAL_FWD4_MINB
+#define DGAL_FWD4_MINB 3     // CTAs per SM the K=4 forward is register-budgeted for
+#endif
+#ifndef DGAL_FWD4_THREADS
+#define DGAL_FWD4_THREADS 256
+#endif
+constexpr int kFwd4Threads = DGAL_FWD4_THREADS;
+
 template <int K>
-__global__ void __launch_bounds__(kPairedThreads)
+__global__ void __launch_bounds__((K == 4) ? kFwd4Threads : kPairedThreads, (K == 4) ? DGAL_FWD4_MINB : 1)
 paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
                          const float *__restrict__ x2, const float *__restrict__ y2,
                          float *__restrict__ iou, uint8_t *__restrict__ nx, uint8_t *__restrict__ xflags)
@@ -156,11 +168,13 @@ cudaError_t launch_paired_fwd(int K, int64_t n, const float *x1, const float *y1
                               const float *y2, float *iou, uint8_t *nx, uint8_t *xflags,
                               cudaStream_t st)
 {
-    const unsigned grid = (unsigned)((n + kPairedThreads - 1) / kPairedThreads);
-    if (K == 4)
-        paired_fwd_direct_kernel<4><<<grid, kPairedThreads, 0, st>>>(n, x1, y1, x2, y2, iou, nx, xflags);
-    else
+    if (K == 4) {
+        const unsigned grid = (unsigned)((n + kFwd4Threads - 1) / kFwd4Threads);
+        paired_fwd_direct_kernel<4><<<grid, kFwd4Threads, 0, st>>>(n, x1, y1, x2, y2, iou, nx, xflags);
+    } else {
+        const unsigned grid = (unsigned)((n + kPairedThreads - 1) / kPairedThreads);
         paired_fwd_direct_kernel<8><<<grid, kPairedThreads, 0, st>>>(n, x1, y1, x2, y2, iou, nx, xflags);
+    }
     return cudaGetLastError();
 }
 
@@ -206,8 +220,12 @@ cudaError_t launch_paired_bwd(int K, int64_t n, const float *x1, const float *y1
 // ---------------------------------------------------------------------------
 // Fused loss forward + backward, one pair per thread
 // ---------------------------------------------------------------------------
+#ifndef DGAL_FUSED4_MINB
+#define DGAL_FUSED4_MINB 3   // CTAs per SM the K=4 fused kernel is register-budgeted for (A/B)
+#endif
+
 template <int K>
-__global__ void __launch_bounds__(kPairedThreads)
+__global__ void __launch_bounds__(kPairedThreads, (K == 4) ? DGAL_FUSED4_MINB : 1)
 paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
                     const float *__restrict__ x2, const float *__restrict__ y2,
                     const float *__restrict__ grad, float scale, float *__restrict__ iou,

@@ -113,6 +113,8 @@ pairwise_kernel(int64_t n_rows, const float *__restrict__ rxg, const float *__re
             Pc.x[k] = __fsub_rn(px[k], ox); Pc.y[k] = __fsub_rn(py[k], oy);
             Qc.x[k] = __fsub_rn(qx[k], ox); Qc.y[k] = __fsub_rn(qy[k], oy);
         }
+        Pc.x[0] = 0.f;   // exact for finite input; lets the compiler fold it
+        Pc.y[0] = 0.f;
         const float v = iou_fwd<K, false>(Pc, Qc).iou;
         const int64_t r = r0 + rl, c = c0 + cl;
         if (iou) iou[r * m + c] = v;

@@ -285,6 +285,8 @@ pw_candidates(int64_t n_rows, const float *__restrict__ rx, const float *__restr
             P.x[k] = __fsub_rn(P.x[k], ox); P.y[k] = __fsub_rn(P.y[k], oy);
             Q.x[k] = __fsub_rn(Q.x[k], ox); Q.y[k] = __fsub_rn(Q.y[k], oy);
         }
+        P.x[0] = 0.f;   // exact for finite input; lets the compiler fold it
+        P.y[0] = 0.f;
         DGAL_ASSERT(rr >= 0 && rr < n_rows && c >= 0 && c < m);
         const float v = iou_fwd<K, false>(P, Q).iou;
         if (iou && v != 0.f) iou[rr * m + c] = v;

@@ -59,7 +59,9 @@ def clip(P, Q, verbose=False):
             e[j, i] = f32(cross(Dx, Dy, g[i, 0], g[i, 1]) - TINY)
     separated = False
     for j in range(K):
-        separated |= (d[:, j].max() <= TINY) or (e[:, j].max() <= 0)
+        separated |= (d[:, j].max() <= TINY)
+    cxm = f32(sum(Q[:, 0]) * f32(1.0 / K)); cym = f32(sum(Q[:, 1]) * f32(1.0 / K))
+    cin = all(cross(g[i, 0], g[i, 1], f32(cxm - P[i, 0]), f32(cym - P[i, 1])) > 0 for i in range(K))
     emin = e.min()
     HI0 = f32(struct.unpack("<f", struct.pack("<I", 0x3F800008))[0])
     inside = [bool(np.all(d[i, :] > 0)) for i in range(K)]
@@ -72,9 +74,9 @@ def clip(P, Q, verbose=False):
             den = f32(f32(a - b) + TINY)
             r = f32(1.0 / den)
             m = sat(f32(-den * BIG))
-            v = f32(a * r) if abs(a) <= abs(b) else fma(b, r, f32(1))
-            lo = max(lo, enc(f32(m * v), j))
-            hi = min(hi, enc(fma(m, BIG, v), j))
+            ve = enc(f32(a * r), j)
+            lo = max(lo, f32(m * ve))
+            hi = min(hi, fma(m, BIG, ve))
         t0[i], t1[i] = lo, hi
     ax = Q[:, 0].copy(); ay = Q[:, 1].copy()
     bx = np.roll(Q[:, 0], -1).copy(); by = np.roll(Q[:, 1], -1).copy()
@@ -83,9 +85,9 @@ def clip(P, Q, verbose=False):
     T0 = np.zeros(K, f32); T1 = np.zeros(K, f32); VAL = [False] * K; HIN = [False] * K; HOUT = [False] * K
     for i in range(K):
         i1 = (i + 1) % K
-        a0 = f32(0) if inside[i] else t0[i]
-        a1 = f32(1) if inside[i1] else min(t1[i], f32(1))
-        valid = strip(a0) <= strip(a1)
+        a0 = f32(0) if inside[i] else (min(t0[i], f32(1)) if inside[i1] else t0[i])
+        a1 = f32(1) if inside[i1] else (max(min(t1[i], f32(1)), f32(0)) if inside[i] else min(t1[i], f32(1)))
+        valid = inside[i] or inside[i1] or (strip(a0) < strip(a1))
         has_in = valid and not inside[i]
         has_out = valid and not inside[i1]
         T0[i], T1[i], VAL[i], HIN[i], HOUT[i] = a0, a1, valid, has_in, has_out
@@ -103,7 +105,7 @@ def clip(P, Q, verbose=False):
     ev = ev_out | ev_in
     if ev == 0:
         anyvalid = any(VAL)
-        in2 = KM if (not anyvalid and not separated) else 0
+        in2 = KM if (not anyvalid and cin) else 0
     else:
         evd = ev | (ev << K)
         endin = ev_out & ~ev_in
@@ -115,11 +117,20 @@ def clip(P, Q, verbose=False):
             sh <<= 1
         in2 = (st >> (K - 1)) & KM
     on2 = ev | in2
+    p2e = f32(0)
+    for i in range(K):
+        if HOUT[i]:
+            jo = dec(t1[i]); X = (fma(T1[i], g[i, 0], P[i, 0]), fma(T1[i], g[i, 1], P[i, 1]))
+            p2e = f32(p2e + cross(X[0], X[1], Q[jo, 0], Q[jo, 1]))
+        if HIN[i]:
+            ji = dec(t0[i]); X = (fma(T0[i], g[i, 0], P[i, 0]), fma(T0[i], g[i, 1], P[i, 1]))
+            w = Q[(ji + 1) % K]
+            p2e = f32(p2e + cross(w[0], w[1], X[0], X[1]))
     Ai = f32(0)
     for k in range(K):
         Ai = fma(max(f32(T1[k] - T0[k]), f32(0)) if VAL[k] else f32(0), C1[k], Ai)
-        c2 = cross(ax[k], ay[k], bx[k], by[k])
-        Ai = f32(Ai + (c2 if (on2 >> k) & 1 else f32(0)))
+        Ai = f32(Ai + (C2[k] if (on2 >> k) & 1 else f32(0)))
+    Ai = f32(Ai + p2e)
     Ai = min(Ai, min(A1, A2))
     # flags walk
     seq = []
