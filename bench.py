@@ -326,6 +326,7 @@ def bench_fused(ctx, n, steps, warmup, peak):
     return {"workload": "cfg3 batch, fused IoU-loss fwd+bwd (dgal_iou_paired_fused, SURVEY f2)",
             "scaling": "weak", "pairs_per_s": n * ctx.world / (ms * 1e-3), "ms_per_step": ms,
             "roofline": {"bound": "hbm", "kernel": "paired_fused_kernel<4>",
+                         "traffic": ncu_traffic().get("paired_fused_k4_bytes_per_launch"),
                          "achieved": n * nbytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": n * nbytes / (ms * 1e-3) / 1e9 / peak, "algorithmic_bytes_per_pair": nbytes}}
 
@@ -379,19 +380,24 @@ def bench_box(ctx, dims, n, steps, warmup, peak):
     bb = 2 * 4 * P + 4 + 1 + 8 + 2 * 4 * P
     ub = 2 * 4 * P + 4 + 2 * 4 * P
     gbs = lambda nb, t: n * nb / (t * 1e-3) / 1e9  # noqa: E731
+    tr = ncu_traffic()
+    scale_tr = lambda key: (tr[key] * n / (1 << 24)) if key in tr else None  # noqa: E731  (captured at 2^24)
     return {"workload": f"2^{n.bit_length() - 1} KITTI {'3D yaw-only' if dims == 3 else '2D rotated'} box pairs, "
                         f"[{P}, n] planes (SURVEY {'f3' if dims == 3 else 'f1'})",
             "scaling": "weak", "pairs_per_s": n * ctx.world / (ms * 1e-3), "ms_per_step": ms,
             "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
             "fwd_roofline": {"bound": "hbm", "kernel": f"box_fwd_kernel<{dims}>", "achieved": gbs(fb, fwd_ms),
                              "peak": peak, "unit": "GB/s", "frac": gbs(fb, fwd_ms) / peak,
+                             "traffic": scale_tr(f"box_fwd_d{dims}_bytes_per_launch"),
                              "algorithmic_bytes_per_pair": fb},
             "bwd_roofline": {"bound": "hbm", "kernel": f"box_bwd_kernel<{dims}>", "achieved": gbs(bb, bwd_ms),
                              "peak": peak, "unit": "GB/s", "frac": gbs(bb, bwd_ms) / peak,
+                             "traffic": scale_tr(f"box_bwd_d{dims}_bytes_per_launch"),
                              "algorithmic_bytes_per_pair": bb},
             "fused": {"pairs_per_s": n * ctx.world / (ums * 1e-3), "ms_per_step": ums,
                       "roofline": {"bound": "hbm", "kernel": f"box_fused_kernel<{dims}>", "achieved": gbs(ub, ums),
                                    "peak": peak, "unit": "GB/s", "frac": gbs(ub, ums) / peak,
+                                   "traffic": scale_tr(f"box_fused_d{dims}_bytes_per_launch"),
                                    "algorithmic_bytes_per_pair": ub}}}
 
 
