@@ -188,12 +188,19 @@ __global__ void __launch_bounds__(kPairedThreads, DIMS == 2 ? DGAL_BOX_FWD2_MINB
 box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict__ b2, int64_t sk, int64_t sp,
                float *__restrict__ iou, uint8_t *__restrict__ nx, uint8_t *__restrict__ xflags)
 {
+    __shared__ float sq[8 * kPairedThreads];   // per-thread p2 vertex table (kP2Smem), [k][thread]
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const Box<DIMS> a = load_box<DIMS>(b1, k, sk, sp), b = load_box<DIMS>(b2, k, sk, sp);
     Poly<4> P, Q;
     box_pair_polys<DIMS>(a, b, P, Q);
-    const FwdOut<4, true> r = iou_fwd<4, true>(P, Q);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        sq[q * kPairedThreads + threadIdx.x] = Q.x[q];
+        sq[(4 + q) * kPairedThreads + threadIdx.x] = Q.y[q];
+    }
+    const FwdOut<4, true> r = iou_fwd<4, true, kP2Smem>(
+        P, Q, QTable{sq + threadIdx.x, sq + 4 * kPairedThreads + threadIdx.x, kPairedThreads});
     float v = r.iou;
     int m = r.nx;
     uint64_t seq = r.seq.w[0];

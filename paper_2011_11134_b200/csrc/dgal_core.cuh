@@ -252,12 +252,27 @@ struct Clip {
 };
 
 // p1, p2 must already be recentred (coordinates near 0; p1.v0 or a box centre).
-// PIECES: also materialise the end points of the p2 pieces (c.ax .. c.by; the
-// fused gradient needs them, and for K = 4 the per-edge selects are cheaper than
-// the per-event form, which serves K = 8).
-template <int K, bool PIECES = (K == 4)>
-__device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &Q, Clip<K> &c)
+// How the p2 side of Green's sum is formed (§4.1 of DESIGN.md):
+//   kP2Pieces  materialise the end points of the p2 pieces (c.ax .. c.by) with
+//              per-(edge, line) selects — the fused gradient needs them;
+//   kP2Regs    per-event form, the event's p2 vertex picked by a select tree;
+//   kP2Smem    per-event form, the vertex read from a per-thread shared-memory
+//              table (QTable) — one LDS instead of a select tree (the LSU pipe is
+//              idle in these kernels, the ALU pipe is the binding one).
+enum P2Mode { kP2Pieces = 0, kP2Regs = 1, kP2Smem = 2 };
+
+// Per-thread table of p2's (recentred) vertices in shared memory: vertex j at
+// x[j * stride], y[j * stride].  Written and read by the same thread only.
+struct QTable {
+    const float *x, *y;
+    int stride;
+};
+
+template <int K, int MODE>
+__device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &Q, Clip<K> &c,
+                                               QTable qt = QTable{nullptr, nullptr, 0})
 {
+    constexpr bool PIECES = (MODE == kP2Pieces);
     constexpr uint32_t KMASK = (1u << K) - 1u;
     // edge vectors g_i = v_i+1 - v_i (p1), f_j = w_j+1 - w_j (p2); shoelace terms
     float *gx = c.gx, *gy = c.gy, *fx = c.fx, *fy = c.fy, *C1 = c.C1, *C2 = c.C2;
@@ -387,8 +402,14 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
             }
         } else {
             float wox, woy, wix, wiy;
-            pick_xy<K>(Q.x, Q.y, ljout, wox, woy);
-            pick_xy<K>(Q.x, Q.y, (ljin + 1u) & (K - 1u), wix, wiy);
+            const uint32_t jn = (ljin + 1u) & (K - 1u);
+            if (MODE == kP2Smem) {
+                wox = qt.x[ljout * qt.stride]; woy = qt.y[ljout * qt.stride];
+                wix = qt.x[jn * qt.stride]; wiy = qt.y[jn * qt.stride];
+            } else {
+                pick_xy<K>(Q.x, Q.y, ljout, wox, woy);
+                pick_xy<K>(Q.x, Q.y, jn, wix, wiy);
+            }
             p2e += has_out ? cross_rn(xox, xoy, wox, woy) : 0.f;
             p2e += has_in ? cross_rn(wix, wiy, xix, xiy) : 0.f;
         }
@@ -445,12 +466,13 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
 }
 
 // p1, p2 must already be recentred on o = p1.v0 (p1.x[0] == p1.y[0] == 0).
-template <int K, bool FLAGS>
-__device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly<K> &Q)
+template <int K, bool FLAGS, int MODE = (K == 4 ? kP2Pieces : kP2Regs)>
+__device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly<K> &Q,
+                                                    QTable qt = QTable{nullptr, nullptr, 0})
 {
     constexpr uint32_t KMASK = (1u << K) - 1u;
     Clip<K> c;
-    clip_intervals<K>(P, Q, c);
+    clip_intervals<K, MODE>(P, Q, c, qt);
     const float *t0 = c.t0, *t1 = c.t1;
     const float A1x2 = c.A1x2, A2x2 = c.A2x2, Aix2 = c.Aix2;
     bool nonempty = c.nonempty;
@@ -551,7 +573,7 @@ __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, f
     for (int k = 0; k < K; ++k) { G1.x[k] = 0.f; G1.y[k] = 0.f; G2.x[k] = 0.f; G2.y[k] = 0.f; }
     if (co) *co = VolCoef{0.f, 0.f, 0.f, 0.f, 0.f};
     Clip<K> c;
-    clip_intervals<K, true>(P, Q, c);
+    clip_intervals<K, kP2Pieces>(P, Q, c);
     if (!c.nonempty) return 0.f;
     // V = A d (2D: d = 1); IoU = V_i / V_u
     const float Vix2 = c.Aix2 * ex.dz;

@@ -35,19 +35,30 @@ __device__ __forceinline__ void recentre(Poly<K> &P, Poly<K> &Q)
 #endif
 constexpr int kFwd4Threads = DGAL_FWD4_THREADS;
 
+#ifndef DGAL_FWD_P2MODE
+#define DGAL_FWD_P2MODE kP2Smem   // how the forward forms the p2 side (dgal_core.cuh P2Mode)
+#endif
+
 template <int K>
 __global__ void __launch_bounds__((K == 4) ? kFwd4Threads : kPairedThreads, (K == 4) ? DGAL_FWD4_MINB : 1)
 paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
                          const float *__restrict__ x2, const float *__restrict__ y2,
                          float *__restrict__ iou, uint8_t *__restrict__ nx, uint8_t *__restrict__ xflags)
 {
+    constexpr int T = (K == 4) ? kFwd4Threads : kPairedThreads;
+    __shared__ float sq[2 * K * T];   // per-thread p2 vertex table, [k][thread] (DGAL_FWD_P2MODE == kP2Smem)
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     Poly<K> P, Q;
     load_poly<K>(x1, y1, k, P);
     load_poly<K>(x2, y2, k, Q);
     recentre<K>(P, Q);
-    const FwdOut<K, true> r = iou_fwd<K, true>(P, Q);
+    QTable qt{sq + threadIdx.x, sq + K * T + threadIdx.x, T};
+    if (DGAL_FWD_P2MODE == kP2Smem) {
+#pragma unroll
+        for (int q = 0; q < K; ++q) { sq[q * T + threadIdx.x] = Q.x[q]; sq[(K + q) * T + threadIdx.x] = Q.y[q]; }
+    }
+    const FwdOut<K, true> r = iou_fwd<K, true, DGAL_FWD_P2MODE>(P, Q, qt);
     __stcs(iou + k, r.iou);
     nx[k] = (uint8_t)r.nx;
     if (K == 4) {
