@@ -661,11 +661,28 @@ __device__ __forceinline__ void bwd_prologue(float *scr)
     }
 }
 
-// Cross(i, j) is X = v_i + t g_i = w_j + s f_j.  If p1 edge i enters p2 there
-// (g_i x f_j < 0) the boundary piece on p1 edge i starts at t and the piece on
-// p2 edge j ends at s; otherwise the other way round.
+// Cross(i, j) is X = v_i + t g_i = w_j + s f_j.  If p1 edge i enters p2 there the
+// boundary piece on p1 edge i starts at t and the piece on p2 edge j ends at s;
+// if it exits, the other way round.  s is the projection of the same point X onto
+// p2 edge j, so the two pieces meeting at X share it.
+//
+// Precision: t is conditioned by 1/sin of the crossing angle.  bwd_crossing (float)
+// serves well-conditioned crossings — there the entry/exit role is the sign of
+// g_i x f_j, which the forward's classification agrees with — and reports the
+// others (|sin| < 2^-10).  bwd_crossing_exact recomputes those with the numerators /
+// denominators in double (differences and products of the float inputs are exact
+// there: ~1e-7 relative accuracy instead of ~6e-8/sin), and takes the role from
+// the forward's own float decision values for that (edge, line), recomputed
+// bitwise-identically (same recentring, same contraction-free expressions): for
+// nearly parallel edges the true sign and the forward's could disagree, and the
+// gradient must differentiate the boundary the forward recorded.
+constexpr float kRefineSin = 0.0009765625f;   // 2^-10: float t error ~6e-8/sin <= 6e-5 above it
+#ifndef DGAL_BWD_REFINE
+#define DGAL_BWD_REFINE 1     // exact second pass for ill-conditioned crossings
+#endif
+
 template <int K, int TILE>
-__device__ __forceinline__ void bwd_crossing(const float *sPx, const float *sPy, const float *sQx,
+__device__ __forceinline__ bool bwd_crossing(const float *sPx, const float *sPy, const float *sQx,
                                              const float *sQy, uint32_t b, float *scr)
 {
     const int i = (b >> 3) & (K - 1), j = b & (K - 1);
@@ -678,13 +695,51 @@ __device__ __forceinline__ void bwd_crossing(const float *sPx, const float *sPy,
     const float den = ex * hy - ey * hx;                       // g_i x f_j
     const float r = rcp_approx(den);
     const float t = __saturatef((Dx * hy - Dy * hx) * r);      // along p1 edge i
-    // along p2 edge j: the projection of the SAME point X = v_i + t g_i (not an
-    // independent s = D x g / den), so the two pieces meeting at X share it even
-    // when the edges are nearly parallel (t ill-conditioned, see clip_intervals)
-    const float hh = rcp_approx(fmaf(hx, hx, hy * hy));
-    const float s = __saturatef(fmaf(fmaf(t, ex, -Dx), hx, fmaf(t, ey, -Dy) * hy) * hh);
+    const float hh = fmaf(hx, hx, hy * hy);
+    const float s = __saturatef(fmaf(fmaf(t, ex, -Dx), hx, fmaf(t, ey, -Dy) * hy) * rcp_approx(hh));
     const bool enter = den < 0.f;
     DGAL_ASSERT(i >= 0 && i < K && j >= 0 && j < K);
+    // ill-conditioned (den^2 < sin^2 |e|^2 |h|^2): left to bwd_crossing_exact
+    const bool need = DGAL_BWD_REFINE && (den * den < (kRefineSin * kRefineSin) * fmaf(ex, ex, ey * ey) * hh);
+    if (!need) {
+        scr[(enter ? i : K + i) * TILE] = t;
+        scr[(enter ? 3 * K + j : 2 * K + j) * TILE] = s;
+    }
+    return need;
+}
+
+template <int K, int TILE>
+__device__ __forceinline__ void bwd_crossing_exact(const float *sPx, const float *sPy, const float *sQx,
+                                                   const float *sQy, uint32_t b, float *scr)
+{
+    const int i = (b >> 3) & (K - 1), j = b & (K - 1);
+    const int i1 = (i + 1) & (K - 1), j1 = (j + 1) & (K - 1);
+    // the forward's class of line j for edge i: the sign of d[i][j] - d[i+1][j]
+    // on the recentred coordinates (clip_intervals), bitwise the same floats
+    const float ox = sPx[0], oy = sPy[0];
+    const float pxi = __fsub_rn(sPx[i], ox), pyi = __fsub_rn(sPy[i], oy);
+    const float pxi1 = __fsub_rn(sPx[i1], ox), pyi1 = __fsub_rn(sPy[i1], oy);
+    const float qxj = __fsub_rn(sQx[j], ox), qyj = __fsub_rn(sQy[j], oy);
+    const float qxj1 = __fsub_rn(sQx[j1], ox), qyj1 = __fsub_rn(sQy[j1], oy);
+    const float fxj = qxj1 - qxj, fyj = qyj1 - qyj;
+    const float da = __fadd_rn(cross_rn(fxj, fyj, __fsub_rn(i == 0 ? 0.f : pxi, qxj),
+                                        __fsub_rn(i == 0 ? 0.f : pyi, qyj)), kTiny);
+    const float db = __fadd_rn(cross_rn(fxj, fyj, __fsub_rn(i1 == 0 ? 0.f : pxi1, qxj),
+                                        __fsub_rn(i1 == 0 ? 0.f : pyi1, qyj)), kTiny);
+    const bool enter = __saturatef(-((da - db) + kTiny) * kBig) > 0.5f;
+    // the crossing in double
+    const double vx = sPx[i], vy = sPy[i];
+    const double ex = (double)sPx[i1] - vx, ey = (double)sPy[i1] - vy;
+    const double wx = sQx[j], wy = sQy[j];
+    const double hx = (double)sQx[j1] - wx, hy = (double)sQy[j1] - wy;
+    const double Dx = wx - vx, Dy = wy - vy;
+    const double den = ex * hy - ey * hx;
+    const double tn = Dx * hy - Dy * hx;
+    const float t = __saturatef((float)tn * rcp_approx((float)den));
+    const double tt = t;
+    const double sn = (tt * ex - Dx) * hx + (tt * ey - Dy) * hy;       // (X - w_j) . f_j
+    const double hh = hx * hx + hy * hy;
+    const float s = __saturatef((float)sn * rcp_approx((float)hh));
     scr[(enter ? i : K + i) * TILE] = t;
     scr[(enter ? 3 * K + j : 2 * K + j) * TILE] = s;
 }
@@ -795,6 +850,7 @@ __device__ __forceinline__ void bwd_tile_pair(const float *tx1, const float *ty1
         V |= lut.v[b];
         cnt += (b >= 0xC0u);
     }
+
     int incl = cnt;                                  // warp prefix sum of the counts
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -813,14 +869,38 @@ __device__ __forceinline__ void bwd_tile_pair(const float *tx1, const float *ty1
     }
     bwd_prologue<K, TILE>(scr + tid);
     __syncwarp();
+    // pass 1 (float) over all crossings; the ill-conditioned ones are compacted in
+    // place to the front of the queue (each write lands at or before the writer's
+    // own, already consumed, slot)
+    int nref = 0;
     for (int base = 0; base < total; base += 32) {   // warp-uniform trip count
         const int e = base + lane;
+        bool need = false;
+        uint32_t ent = 0;
         if (e < total) {
             DGAL_ASSERT(e < 32 * 2 * K);
-            const uint32_t ent = queue[e];
+            ent = queue[e];
             DGAL_ASSERT((int)(ent >> 8) < 32);
             const int pt = warp * 32 + (int)(ent >> 8);
-            bwd_crossing<K, TILE>(tx1 + pt * K, ty1 + pt * K, tx2 + pt * K, ty2 + pt * K, ent & 0xFFu, scr + pt);
+            need = bwd_crossing<K, TILE>(tx1 + pt * K, ty1 + pt * K, tx2 + pt * K, ty2 + pt * K, ent & 0xFFu,
+                                         scr + pt);
+        }
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, need);
+        if (bal) {
+            __syncwarp();
+            if (need) queue[nref + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)ent;
+            nref += __popc(bal);
+            __syncwarp();
+        }
+    }
+    // pass 2: exact recomputation of the compacted ones, 32 at a time
+    for (int base = 0; base < nref; base += 32) {
+        const int e = base + lane;
+        if (e < nref) {
+            const uint32_t ent = queue[e];
+            const int pt = warp * 32 + (int)(ent >> 8);
+            bwd_crossing_exact<K, TILE>(tx1 + pt * K, ty1 + pt * K, tx2 + pt * K, ty2 + pt * K, ent & 0xFFu,
+                                        scr + pt);
         }
     }
     __syncwarp();

@@ -278,3 +278,27 @@ def test_integer_grid_rectangles_on_device():
     ai = ox * oy
     want = ai / (a * b + c * d - ai)
     assert np.max(np.abs(iou - want)) <= 1e-6
+
+
+@pytest.mark.parametrize("scale", [1e-6, 1e-5, 1e-4, 1e-3, 1e-2])
+def test_near_coincident_gradients(scale):
+    """Backward on prediction ~ target pairs: wherever the device's nx/xflags equal the
+    oracle's (same piece of the piecewise-smooth IoU), the vertex gradients match the
+    oracle at the north_star tolerance — the crossing parameters of nearly parallel
+    edges are refined in double.  Pairs whose flags differ sit within
+    rounding of a flag change, where the gradient is discontinuous."""
+    b1, b2 = _near_coincident_boxes(50_000, scale, seed=20 + int(-math.log10(scale)))
+    x1, y1 = oracle.box_corners(b1.T.astype(np.float64))
+    x2, y2 = oracle.box_corners(b2.T.astype(np.float64))
+    x1, y1, x2, y2 = (a.astype(np.float32) for a in (x1, y1, x2, y2))
+    g = np.random.default_rng(5).uniform(-1, 1, x1.shape[0]).astype(np.float32)
+    T = lambda a: torch.from_numpy(a).to(dev())  # noqa: E731
+    X = (T(x1), T(y1), T(x2), T(y2))
+    iou, nx, xf = dgal.iou_paired_fwd(*X)
+    gr = dgal.iou_paired_bwd(*X, T(g), nx, xf)
+    rf = oracle.iou_paired_fwd((x1, y1), (x2, y2))
+    same = (nx.cpu().numpy() == rf["nx"]) & np.all(xf.cpu().numpy() == rf["xflags"], 1)
+    assert same.mean() > 0.8
+    ref = oracle.iou_paired_bwd((x1, y1), (x2, y2), g)
+    for got, want in zip(gr, ref):
+        assert_grad_close(got.cpu().numpy()[same], want[same])
