@@ -221,8 +221,39 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
 // ---------------------------------------------------------------------------
 // backward through the recorded nx / xflags (the polygon path's phases)
 // ---------------------------------------------------------------------------
+// Exact corners for the refinement of ill-conditioned crossings (bwd_crossing_exact):
+// the float corners carry ~6e-8 relative rounding, which a crossing of nearly
+// parallel edges amplifies ~1/sin, so they are rebuilt in double from the (float)
+// box parameters, as the oracle does: cos / sin by sincospi (exact
+// reduction, no local memory), frame = box 1's centre.
+struct BoxGeometry {
+    const float *p;   // staged parameters [param][pair]: cx1, cy1, w1, h1, th1, cx2, cy2, w2, h2, th2
+    __device__ __forceinline__ static void corner(double dcx, double dcy, double w, double h, double th, int k,
+                                                  double &x, double &y)
+    {
+        double s, c;
+        sincospi(th * 0.318309886183790671537767526745, &s, &c);
+        const double lx = ((k == 1 || k == 2) ? 0.5 : -0.5) * w, ly = ((k >= 2) ? 0.5 : -0.5) * h;
+        x = dcx + (c * lx - s * ly);
+        y = dcy + (s * lx + c * ly);
+    }
+    __device__ __forceinline__ void get(int pt, int i, int i1, int j, int j1, double &vx, double &vy, double &v1x,
+                                        double &v1y, double &wx, double &wy, double &w1x, double &w1y) const
+    {
+        const double dcx = (double)p[5 * kBoxTile + pt] - (double)p[pt];
+        const double dcy = (double)p[6 * kBoxTile + pt] - (double)p[kBoxTile + pt];
+        const double w1 = p[2 * kBoxTile + pt], h1 = p[3 * kBoxTile + pt], t1 = p[4 * kBoxTile + pt];
+        const double w2 = p[7 * kBoxTile + pt], h2 = p[8 * kBoxTile + pt], t2 = p[9 * kBoxTile + pt];
+        corner(0.0, 0.0, w1, h1, t1, i, vx, vy);
+        corner(0.0, 0.0, w1, h1, t1, i1, v1x, v1y);
+        corner(dcx, dcy, w2, h2, t2, j, wx, wy);
+        corner(dcx, dcy, w2, h2, t2, j1, w1x, w1y);
+    }
+};
+
 struct BoxBwdSmem {
     float x1[kBoxTile * 4], y1[kBoxTile * 4], x2[kBoxTile * 4], y2[kBoxTile * 4];  // corners, [pair][k]
+    float bp[10 * kBoxTile];                                                     // BEV params, [param][pair]
     float scr[4 * 4 * kBoxTile];                                                 // [slot][pair]
     uint16_t queue[kBoxTile / 32][32 * 8];
     FlagLut lut;
@@ -263,11 +294,17 @@ box_bwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
         S.x2[tid * 4 + q] = Q.x[q]; S.y2[tid * 4 + q] = Q.y[q];
     }
     const ZOver z = z_overlap<DIMS>(a, b);
-    __syncthreads();  // flag table and corner tile
+    {
+        const float bv[10] = {a.cx, a.cy, a.w, a.h, a.th, b.cx, b.cy, b.w, b.h, b.th};
+#pragma unroll
+        for (int q = 0; q < 10; ++q) S.bp[q * kBoxTile + tid] = bv[q];
+    }
+    __syncthreads();  // flag table, corner tile, parameters
     Poly<4> G1, G2;
     VolCoef co;
-    bwd_tile_pair<4, kBoxTile>(S.x1, S.y1, S.x2, S.y2, sq, m, g, live, S.scr, S.queue[tid >> 5], S.lut, G1, G2,
-                               Extrude{z.dz, a.d, b.d}, &co);
+    const BoxGeometry geo{S.bp};
+    bwd_tile_pair<4, kBoxTile, BoxGeometry>(S.x1, S.y1, S.x2, S.y2, sq, m, g, live, S.scr, S.queue[tid >> 5], S.lut,
+                                            G1, G2, Extrude{z.dz, a.d, b.d}, &co, &geo);
     if (!live) return;
     float gcz1, gd1, gcz2, gd2;
     z_grads<DIMS>(co, z, gcz1, gd1, gcz2, gd2);

@@ -708,9 +708,25 @@ __device__ __forceinline__ bool bwd_crossing(const float *sPx, const float *sPy,
     return need;
 }
 
-template <int K, int TILE>
+// Exact geometry for bwd_crossing_exact: vertices i, i+1 of p1 and j, j+1 of p2 of
+// the pair at tile slot pt, in double.  Polygon path: the staged float tile IS
+// the input, so its values are exact.
+template <int K>
+struct TileGeometry {
+    const float *x1, *y1, *x2, *y2;   // tile bases, [pair][k]
+    __device__ __forceinline__ void get(int pt, int i, int i1, int j, int j1, double &vx, double &vy,
+                                        double &v1x, double &v1y, double &wx, double &wy, double &w1x,
+                                        double &w1y) const
+    {
+        vx = x1[pt * K + i]; vy = y1[pt * K + i]; v1x = x1[pt * K + i1]; v1y = y1[pt * K + i1];
+        wx = x2[pt * K + j]; wy = y2[pt * K + j]; w1x = x2[pt * K + j1]; w1y = y2[pt * K + j1];
+    }
+};
+
+template <int K, int TILE, class GEO>
 __device__ __forceinline__ void bwd_crossing_exact(const float *sPx, const float *sPy, const float *sQx,
-                                                   const float *sQy, uint32_t b, float *scr)
+                                                   const float *sQy, uint32_t b, float *scr, const GEO &geo,
+                                                   int pt)
 {
     const int i = (b >> 3) & (K - 1), j = b & (K - 1);
     const int i1 = (i + 1) & (K - 1), j1 = (j + 1) & (K - 1);
@@ -727,11 +743,11 @@ __device__ __forceinline__ void bwd_crossing_exact(const float *sPx, const float
     const float db = __fadd_rn(cross_rn(fxj, fyj, __fsub_rn(i1 == 0 ? 0.f : pxi1, qxj),
                                         __fsub_rn(i1 == 0 ? 0.f : pyi1, qyj)), kTiny);
     const bool enter = __saturatef(-((da - db) + kTiny) * kBig) > 0.5f;
-    // the crossing in double
-    const double vx = sPx[i], vy = sPy[i];
-    const double ex = (double)sPx[i1] - vx, ey = (double)sPy[i1] - vy;
-    const double wx = sQx[j], wy = sQy[j];
-    const double hx = (double)sQx[j1] - wx, hy = (double)sQy[j1] - wy;
+    // the crossing in double on the exact geometry
+    double vx, vy, v1x, v1y, wx, wy, w1x, w1y;
+    geo.get(pt, i, i1, j, j1, vx, vy, v1x, v1y, wx, wy, w1x, w1y);
+    const double ex = v1x - vx, ey = v1y - vy;
+    const double hx = w1x - wx, hy = w1y - wy;
     const double Dx = wx - vx, Dy = wy - vy;
     const double den = ex * hy - ey * hx;
     const double tn = Dx * hy - Dy * hx;
@@ -834,12 +850,12 @@ __device__ __forceinline__ void bwd_epilogue(const float *sPx, const float *sPy,
 // flag bytes into provenance bits, queues its Cross bytes in the warp's queue
 // (warp prefix sum), evaluates the warp's crossings 32 at a time (full SIMT
 // width), then runs the epilogue.  Must be called by all 32 lanes of the warp.
-template <int K, int TILE>
+template <int K, int TILE, class GEO = TileGeometry<K>>
 __device__ __forceinline__ void bwd_tile_pair(const float *tx1, const float *ty1, const float *tx2,
                                               const float *ty2, const Seq<K> &sq, int m, float g, bool live,
                                               float *scr, uint16_t *queue, const FlagLut &lut,
                                               Poly<K> &G1, Poly<K> &G2, const Extrude ex = flat(),
-                                              VolCoef *co = nullptr)
+                                              VolCoef *co = nullptr, const GEO *geo = nullptr)
 {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     uint32_t V = 0;
@@ -899,8 +915,13 @@ __device__ __forceinline__ void bwd_tile_pair(const float *tx1, const float *ty1
         if (e < nref) {
             const uint32_t ent = queue[e];
             const int pt = warp * 32 + (int)(ent >> 8);
-            bwd_crossing_exact<K, TILE>(tx1 + pt * K, ty1 + pt * K, tx2 + pt * K, ty2 + pt * K, ent & 0xFFu,
-                                        scr + pt);
+            if (geo)
+                bwd_crossing_exact<K, TILE, GEO>(tx1 + pt * K, ty1 + pt * K, tx2 + pt * K, ty2 + pt * K,
+                                                 ent & 0xFFu, scr + pt, *geo, pt);
+            else
+                bwd_crossing_exact<K, TILE, TileGeometry<K>>(tx1 + pt * K, ty1 + pt * K, tx2 + pt * K,
+                                                             ty2 + pt * K, ent & 0xFFu, scr + pt,
+                                                             TileGeometry<K>{tx1, ty1, tx2, ty2}, pt);
         }
     }
     __syncwarp();
