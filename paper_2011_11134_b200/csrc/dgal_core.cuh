@@ -524,16 +524,16 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
                 s.w[0] |= valid ? shl64(seg, 8u * (uint32_t)pos) : 0ull;
                 pos += c;
             } else {
-                if (valid) {
-                    if (pos < 2 * K) seq_or<K>(s, b0, pos);
-                    ++pos;
-                    if (has_out) {
-                        if (pos < 2 * K) seq_or<K>(s, b1, pos);
-                        ++pos;
-                        if (pos < 2 * K) seq_or<K>(s, run, pos);
-                        pos += (int)L;
-                    }
-                }
+                // group = b0 | b1 << 8 | run << 16 (up to 9 bytes: lo word + byte 8),
+                // OR-ed in at byte pos of the 16-byte sequence, branch-free
+                const uint64_t glo = has_out ? ((uint64_t)b0 | ((uint64_t)b1 << 8) | (run << 16)) : (uint64_t)b0;
+                const uint64_t ghi = has_out ? (run >> 48) : 0ull;
+                const uint32_t sh = 8u * (uint32_t)pos;
+                const uint64_t olo = shl64(glo, sh);
+                const uint64_t ohi = (sh >= 64u) ? shl64(glo, sh - 64u) : (shr64(glo, 64u - sh) | shl64(ghi, sh));
+                s.w[0] |= valid ? olo : 0ull;
+                s.w[Seq<K>::NW - 1] |= valid ? ohi : 0ull;
+                pos += valid ? (has_out ? 2 + (int)L : 1) : 0;
             }
         }
         if (pos == 0 && in2 == KMASK) {  // p2 inside p1: all FromP2, in order
