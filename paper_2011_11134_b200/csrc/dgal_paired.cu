@@ -79,6 +79,9 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
 // other stage of a 2-deep shared-memory ring while every thread computes tile
 // it from shared memory, so the 141 B/pair of HBM traffic overlaps the math at
 // any occupancy.  The tail tile (or misaligned inputs) is loaded directly.
+// Warps are independent within a tile (own pairs, own crossing queue), so a
+// stage is released per warp on an "empty" mbarrier instead of a CTA barrier:
+// only the producer waits for all warps before refilling it; the others run on.
 constexpr int kTile = 256;
 
 template <int K>
@@ -93,7 +96,8 @@ struct BwdSmem {
     float scr[4 * K * kTile];                       // interval end points, [slot][pair]
     uint16_t queue[kTile / 32][32 * 2 * K];         // per-warp crossing queue: lane << 8 | byte
     FlagLut lut;
-    uint64_t bar[2];
+    uint64_t bar[2];     // full: the stage's bulk copies landed
+    uint64_t empty[2];   // empty: every warp is done with the stage
 };
 
 template <int K>
@@ -116,6 +120,8 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
     if (tid == 0) {
         mbar_init(&S.bar[0], 1);
         mbar_init(&S.bar[1], 1);
+        mbar_init(&S.empty[0], kTile / 32);
+        mbar_init(&S.empty[1], kTile / 32);
         fence_mbar_init();
     }
     __syncthreads();
@@ -138,7 +144,11 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
     for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
         const int s = it & 1;
         const int64_t next = tile + gridDim.x;
-        if (tid == 0 && next < nfull) issue(next, s ^ 1);
+        if (tid == 0 && next < nfull) {
+            // stage s^1 last held tile it-1: wait until every warp released it
+            if (it >= 1) mbar_wait(&S.empty[s ^ 1], (uint32_t)((it - 1) >> 1) & 1u);
+            issue(next, s ^ 1);
+        }
         typename BwdSmem<K>::Stage &T = S.st[s];
         const int64_t k = tile * kTile + tid;
         DGAL_ASSERT(tile < ntiles && (tile >= nfull || (tile + 1) * kTile <= n));
@@ -171,7 +181,8 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
             store_plane<K>(gx2, k, G2.x);
             store_plane<K>(gy2, k, G2.y);
         }
-        __syncthreads();  // stage s fully consumed before it is refilled
+        __syncwarp();                                      // the warp is done with stage s
+        if ((tid & 31) == 0) mbar_arrive(&S.empty[s]);
     }
 }
 
