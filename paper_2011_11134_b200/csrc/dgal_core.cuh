@@ -858,14 +858,21 @@ __device__ __forceinline__ void bwd_tile_pair(const float *tx1, const float *ty1
                                               VolCoef *co = nullptr, const GEO *geo = nullptr)
 {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    uint32_t V = 0;
+    // the recorded bytes, masked to the first m once (the padding is 0x00 already;
+    // the mask keeps a malformed record from reading past nx)
+    Seq<K> w;
     int cnt = 0;
 #pragma unroll
-    for (int p = 0; p < 2 * K; ++p) {
-        const uint32_t b = (p < m) ? seq_byte<K>(sq, p) : 0u;
-        V |= lut.v[b];
-        cnt += (b >= 0xC0u);
+    for (int q = 0; q < Seq<K>::NW; ++q) {
+        const int rem = m - 8 * q;
+        const uint64_t keep = (rem >= 8) ? ~0ull : ((rem <= 0) ? 0ull : (shl64(1ull, 8u * (uint32_t)rem) - 1ull));
+        w.w[q] = sq.w[q] & keep;
+        // Cross bytes: tag bits 7 and 6 both set
+        cnt += __popcll(w.w[q] & (w.w[q] << 1) & 0x8080808080808080ull);
     }
+    uint32_t V = 0;
+#pragma unroll
+    for (int p = 0; p < 2 * K; ++p) V |= lut.v[seq_byte<K>(w, p)];
 
     int incl = cnt;                                  // warp prefix sum of the counts
 #pragma unroll
@@ -877,7 +884,7 @@ __device__ __forceinline__ void bwd_tile_pair(const float *tx1, const float *ty1
     int at = incl - cnt;
 #pragma unroll
     for (int p = 0; p < 2 * K; ++p) {
-        const uint32_t b = (p < m) ? seq_byte<K>(sq, p) : 0u;
+        const uint32_t b = seq_byte<K>(w, p);
         if (b >= 0xC0u) {
             DGAL_ASSERT(at >= 0 && at < 32 * 2 * K);
             queue[at++] = (uint16_t)((lane << 8) | b);
