@@ -100,8 +100,16 @@ struct BwdSmem {
     uint64_t empty[2];   // empty: every warp is done with the stage
 };
 
+// Warp-specialised: warps 0..7 consume (one pair per thread), warp 8 produces —
+// its lane 0 refills a stage with the next tile as soon as all consumer warps have
+// released it, so no consumer ever waits on the producer's own bookkeeping.
+constexpr int kBwdThreads = kTile + 32;
+
+#ifndef DGAL_BWD4_MINB
+#define DGAL_BWD4_MINB 3
+#endif
 template <int K>
-__global__ void __launch_bounds__(kTile, (K == 4) ? 3 : 1)
+__global__ void __launch_bounds__(kBwdThreads, (K == 4) ? DGAL_BWD4_MINB : 1)
 paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
                   const float *__restrict__ x2, const float *__restrict__ y2,
                   const float *__restrict__ grad, const uint8_t *__restrict__ nx,
@@ -116,7 +124,7 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
     const int64_t nfull = use_bulk ? n / kTile : 0;  // tiles fed by bulk copies
     constexpr uint32_t kStageBytes = 4u * kTile * K * 4u + kTile * 4u + kTile * 2u * K + kTile;
 
-    fill_flag_lut(S.lut, tid, kTile);
+    fill_flag_lut(S.lut, tid, kBwdThreads);
     if (tid == 0) {
         mbar_init(&S.bar[0], 1);
         mbar_init(&S.bar[1], 1);
@@ -126,35 +134,39 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
     }
     __syncthreads();
 
-    auto issue = [&](int64_t tile, int s) {
-        const int64_t b = tile * kTile;
-        typename BwdSmem<K>::Stage &T = S.st[s];
-        mbar_arrive_expect_tx(&S.bar[s], kStageBytes);
-        bulk_g2s(T.x1, x1 + b * K, kTile * K * 4, &S.bar[s]);
-        bulk_g2s(T.y1, y1 + b * K, kTile * K * 4, &S.bar[s]);
-        bulk_g2s(T.x2, x2 + b * K, kTile * K * 4, &S.bar[s]);
-        bulk_g2s(T.y2, y2 + b * K, kTile * K * 4, &S.bar[s]);
-        bulk_g2s(T.g, grad + b, kTile * 4, &S.bar[s]);
-        bulk_g2s(T.xf, xflags + b * 2 * K, kTile * 2 * K, &S.bar[s]);
-        bulk_g2s(T.nx, nx + b, kTile, &S.bar[s]);
-    };
+    if (tid >= kTile) {   // ---- producer warp ----
+        if (tid == kTile) {
+            int it = 0;
+#pragma unroll 1
+            for (int64_t tile = blockIdx.x; tile < nfull; ++it, tile += gridDim.x) {
+                const int s = it & 1;
+                // stage s last held tile it-2: wait until every consumer warp released it
+                if (it >= 2) mbar_wait(&S.empty[s], (uint32_t)((it - 2) >> 1) & 1u);
+                const int64_t b = tile * kTile;
+                typename BwdSmem<K>::Stage &T = S.st[s];
+                mbar_arrive_expect_tx(&S.bar[s], kStageBytes);
+                bulk_g2s(T.x1, x1 + b * K, kTile * K * 4, &S.bar[s]);
+                bulk_g2s(T.y1, y1 + b * K, kTile * K * 4, &S.bar[s]);
+                bulk_g2s(T.x2, x2 + b * K, kTile * K * 4, &S.bar[s]);
+                bulk_g2s(T.y2, y2 + b * K, kTile * K * 4, &S.bar[s]);
+                bulk_g2s(T.g, grad + b, kTile * 4, &S.bar[s]);
+                bulk_g2s(T.xf, xflags + b * 2 * K, kTile * 2 * K, &S.bar[s]);
+                bulk_g2s(T.nx, nx + b, kTile, &S.bar[s]);
+            }
+        }
+        return;
+    }
 
     int64_t tile = blockIdx.x;
-    if (tid == 0 && tile < nfull) issue(tile, 0);
+#pragma unroll 1
     for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
         const int s = it & 1;
-        const int64_t next = tile + gridDim.x;
-        if (tid == 0 && next < nfull) {
-            // stage s^1 last held tile it-1: wait until every warp released it
-            if (it >= 1) mbar_wait(&S.empty[s ^ 1], (uint32_t)((it - 1) >> 1) & 1u);
-            issue(next, s ^ 1);
-        }
         typename BwdSmem<K>::Stage &T = S.st[s];
         const int64_t k = tile * kTile + tid;
         DGAL_ASSERT(tile < ntiles && (tile >= nfull || (tile + 1) * kTile <= n));
         if (tile < nfull) {
             mbar_wait(&S.bar[s], (uint32_t)(it >> 1) & 1u);
-        } else if (k < n) {  // direct path: this thread stages its own pair
+        } else if (k < n) {  // direct path: this thread stages its own pair (own slots only)
 #pragma unroll
             for (int q = 0; q < K; ++q) {
                 T.x1[tid * K + q] = x1[k * K + q]; T.y1[tid * K + q] = y1[k * K + q];
@@ -216,7 +228,7 @@ cudaError_t launch_bwd_k(int64_t n, const float *x1, const float *y1, const floa
         if (e != cudaSuccess) return e;
         int sms = 0, per = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, paired_bwd_kernel<K>, kTile, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, paired_bwd_kernel<K>, kBwdThreads, smem);
         limit = sms * (per > 0 ? per : 1);
         dev_cached = dev;
     }
@@ -224,8 +236,8 @@ cudaError_t launch_bwd_k(int64_t n, const float *x1, const float *y1, const floa
     const unsigned grid = (unsigned)(ntiles < limit ? ntiles : limit);
     auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
     const int use_bulk = al16(grad) && al16(nx) && al16(xflags);   // planes are 16 B aligned (ABI)
-    paired_bwd_kernel<K><<<grid, kTile, smem, st>>>(n, x1, y1, x2, y2, grad, nx, xflags, gx1, gy1, gx2, gy2,
-                                                     use_bulk);
+    paired_bwd_kernel<K><<<grid, kBwdThreads, smem, st>>>(n, x1, y1, x2, y2, grad, nx, xflags, gx1, gy1, gx2,
+                                                           gy2, use_bulk);
     return cudaGetLastError();
 }
 }  // namespace
