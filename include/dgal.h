@@ -203,8 +203,11 @@ dgal_status dgal_iou_pairwise(int K, int64_t n_rows,
  *   undecided to *undecided (device int32; the caller zeroes it).  Uses nbr lists
  *   when nbr_count[r] <= nbr_cap, else scans the lower part of mask row r.
  * dgal_nms_keep: all rounds for a single-GPU problem (rows = all n boxes,
- *   row_offset = 0), in one persistent single-CTA kernel (no host round trips);
- *   writes keep[i] in {0,1}.  status [n] is caller-provided scratch.
+ *   row_offset = 0) in one kernel (no host round trips); writes keep[i] in {0,1}.
+ *   status [n] is caller-provided scratch.  scratch (nullable, >= 2 int32, 4-byte
+ *   aligned, device): with it the rounds run grid-wide (a cooperative launch, one
+ *   box per thread, grid-wide barriers between rounds); without it, in a single
+ *   1024-thread CTA (same result).
  * mask / nbr_* are exactly the outputs of dgal_iou_pairwise with the same thr.
  */
 dgal_status dgal_nms_round(int64_t n_total, int64_t n_rows, int64_t row_offset,
@@ -216,7 +219,7 @@ dgal_status dgal_nms_round(int64_t n_total, int64_t n_rows, int64_t row_offset,
 dgal_status dgal_nms_keep(int64_t n,
                           const uint64_t *mask, int64_t mask_words,
                           const int32_t *nbr_count, const int32_t *nbr_idx, int32_t nbr_cap,
-                          uint8_t *status, uint8_t *keep,
+                          uint8_t *status, uint8_t *keep, int32_t *scratch,
                           dgal_stream stream);
 
 /* Human-readable name of a status code (static storage). */

@@ -269,15 +269,17 @@ def nms_round(n_total: int, row_offset: int, mask, nbr_count, nbr_idx, status, u
          _ptr(nbr_idx), cap, _ptr(status), _ptr(undecided), _stream(mask.device))
 
 
-def nms_keep(mask, nbr_count=None, nbr_idx=None, status=None, keep=None):
-    """Greedy NMS keep vector u8[n] from a single-GPU pairwise mask (dgal_nms_keep)."""
+def nms_keep(mask, nbr_count=None, nbr_idx=None, status=None, keep=None, grid: bool = True):
+    """Greedy NMS keep vector u8[n] from a single-GPU pairwise mask (dgal_nms_keep).
+    grid=True runs the rounds grid-wide (cooperative launch); False in one CTA."""
     n = mask.shape[0]
     dev = mask.device
     cap = nbr_idx.shape[1] if nbr_idx is not None else 0
     status = torch.empty(n, dtype=torch.uint8, device=dev) if status is None else status
     keep = torch.empty(n, dtype=torch.uint8, device=dev) if keep is None else keep
+    scratch = torch.empty(2, dtype=torch.int32, device=dev) if grid else None
     call("dgal_nms_keep", n, _ptr(mask), mask.shape[1], _ptr(nbr_count), _ptr(nbr_idx), cap, _ptr(status),
-         _ptr(keep), _stream(dev))
+         _ptr(keep), _ptr(scratch), _stream(dev))
     return keep
 
 

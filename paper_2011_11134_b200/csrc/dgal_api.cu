@@ -175,15 +175,15 @@ dgal_status dgal_nms_round(int64_t n_total, int64_t n_rows, int64_t row_offset, 
 
 dgal_status dgal_nms_keep(int64_t n, const uint64_t *mask, int64_t mask_words, const int32_t *nbr_count,
                           const int32_t *nbr_idx, int32_t nbr_cap, uint8_t *status, uint8_t *keep,
-                          dgal_stream stream)
+                          int32_t *scratch, dgal_stream stream)
 {
     if (n < 0) return DGAL_ERR_INVALID_ARG;
     if (n == 0) return DGAL_OK;
     if (!mask || !status || !keep || mask_words < (n + 63) / 64) return DGAL_ERR_INVALID_ARG;
     if ((nbr_count == nullptr) != (nbr_idx == nullptr) || nbr_cap < 0) return DGAL_ERR_INVALID_ARG;
-    if (!aligned(mask, 8)) return DGAL_ERR_MISALIGNED;
+    if (!aligned(mask, 8) || (scratch && !aligned(scratch, 4))) return DGAL_ERR_MISALIGNED;
     return from_cuda(dgal::launch_nms_keep(n, mask, mask_words, nbr_count, nbr_idx, nbr_cap, status, keep,
-                                           as_cuda(stream)));
+                                           scratch, as_cuda(stream)));
 }
 
 const char *dgal_status_string(dgal_status s)

@@ -8,6 +8,8 @@
 // rounds terminate with exactly the greedy result; in practice the number of
 // rounds is the length of the longest suppression chain (a handful).
 // Status bytes: 0 undecided, 1 kept, 2 removed.
+#include <cooperative_groups.h>
+
 #include "dgal_internal.h"
 
 namespace dgal {
@@ -107,10 +109,73 @@ cudaError_t launch_nms_round(int64_t n_total, int64_t n_rows, int64_t row_offset
     return cudaGetLastError();
 }
 
+// All rounds grid-wide: a cooperative launch (every CTA resident), one box per
+// thread per round, grid barriers between rounds.  The undecided count of round r
+// goes to cnt[r & 1]; cnt[(r + 1) & 1] is cleared during round r, before anyone
+// can add to it (round r + 1 starts after the barrier).
+__global__ void __launch_bounds__(kNmsRoundThreads)
+nms_keep_grid_kernel(int64_t n, const uint64_t *__restrict__ mask, int64_t mask_words,
+                     const int32_t *__restrict__ nbr_count, const int32_t *__restrict__ nbr_idx, int32_t cap,
+                     uint8_t *status, uint8_t *__restrict__ keep, int32_t *cnt)
+{
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    volatile uint8_t *vs = status;
+    for (int64_t i = t0; i < n; i += stride) vs[i] = 0;
+    if (t0 == 0) { cnt[0] = 0; cnt[1] = 0; }
+    grid.sync();
+    for (int r = 0;; ++r) {
+        volatile int32_t *c = cnt + (r & 1);
+        if (t0 == 0) cnt[(r + 1) & 1] = 0;
+        int still = 0;
+        for (int64_t i = t0; i < n; i += stride) {
+            if (vs[i] != 0) continue;
+            const int d = decide(i, i, mask, mask_words, nbr_count, nbr_idx, cap, vs);
+            if (d) vs[i] = (uint8_t)d;
+            else ++still;
+        }
+        const unsigned b = __ballot_sync(0xFFFFFFFFu, still != 0);
+        if (b) {
+            // warp sum of the (small) counts
+            int v = still;
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, d);
+            if ((threadIdx.x & 31) == 0) atomicAdd((int32_t *)c, v);
+        }
+        grid.sync();
+        if (*c == 0) break;      // the same value for every thread (read after the barrier)
+        grid.sync();             // everyone has read c before it is cleared again (round r + 2)
+    }
+    for (int64_t i = t0; i < n; i += stride) keep[i] = (vs[i] == 1) ? 1 : 0;
+}
+
 cudaError_t launch_nms_keep(int64_t n, const uint64_t *mask, int64_t mask_words,
                             const int32_t *nbr_count, const int32_t *nbr_idx, int32_t cap,
-                            uint8_t *status, uint8_t *keep, cudaStream_t st)
+                            uint8_t *status, uint8_t *keep, int32_t *scratch, cudaStream_t st)
 {
+    if (scratch) {
+        static int dev_cached = -1, limit = 0;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev != dev_cached) {
+            int sms = 0, per = 0, coop = 0;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, nms_keep_grid_kernel, kNmsRoundThreads, 0);
+            limit = coop ? sms * (per > 0 ? per : 1) : 0;
+            dev_cached = dev;
+        }
+        if (limit > 0) {
+            const int64_t need = (n + kNmsRoundThreads - 1) / kNmsRoundThreads;
+            unsigned grid = (unsigned)(need < limit ? need : limit);
+            void *args[] = {&n, (void *)&mask, &mask_words, (void *)&nbr_count, (void *)&nbr_idx, &cap, &status,
+                            &keep, &scratch};
+            return cudaLaunchCooperativeKernel((const void *)nms_keep_grid_kernel, dim3(grid),
+                                               dim3(kNmsRoundThreads), args, 0, st);
+        }
+    }
     nms_keep_kernel<<<1, kNmsKeepThreads, 0, st>>>(n, mask, mask_words, nbr_count, nbr_idx, cap, status,
                                                    keep);
     return cudaGetLastError();

@@ -200,3 +200,20 @@ def test_indexed_and_tiled_paths_agree():
     v = dgal.iou_pairwise(xs, ys, xs, ys, thr=0.5, indexed=False)
     assert torch.equal(u[0], v[0]) and torch.equal(u[1], v[1])
     assert bool((u[0] == 1.0).all())
+
+
+def test_keep_grid_equals_single_cta_and_oracle():
+    """The grid-wide rounds (cooperative launch) and the single-CTA rounds reach the same
+    unique fixed point, which is the oracle's greedy scan of the same mask."""
+    sc = synth.gen_cfg5_scene(n_objects=400, per_object=50)
+    n = sc.polys.n
+    x = torch.from_numpy(sc.polys.x.reshape(n, 4)).to(dev())
+    y = torch.from_numpy(sc.polys.y.reshape(n, 4)).to(dev())
+    _, mask, cnt, idx = dgal.iou_pairwise(x, y, x, y, thr=sc.thr, want_iou=False, nbr_cap=64)
+    kg = dgal.nms_keep(mask, cnt, idx, grid=True)
+    kc = dgal.nms_keep(mask, cnt, idx, grid=False)
+    kl = dgal.nms_keep(mask, grid=True)                       # mask rows only (no lists)
+    torch.cuda.synchronize()
+    assert torch.equal(kg, kc) and torch.equal(kg, kl)
+    ref = oracle.nms_scan_mask(mask.cpu().numpy().view(np.uint64))
+    assert np.array_equal(kg.cpu().numpy(), ref)
