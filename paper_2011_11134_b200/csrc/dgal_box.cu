@@ -321,6 +321,8 @@ box_fused_kernel(int64_t n, const float *__restrict__ b1, const float *__restric
                  const float *__restrict__ grad, float scale, float *__restrict__ iou, float *__restrict__ gb1,
                  float *__restrict__ gb2)
 {
+    constexpr int T = kPairedThreads;
+    __shared__ float pt[16 * T];   // per-thread piece table (kP2PiecesSmem), [slot][thread]
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const Box<DIMS> a = load_box<DIMS>(b1, k, sk, sp), b = load_box<DIMS>(b2, k, sk, sp);
@@ -329,7 +331,8 @@ box_fused_kernel(int64_t n, const float *__restrict__ b1, const float *__restric
     const Trig t = box_pair_polys<DIMS>(a, b, P, Q);
     const ZOver z = z_overlap<DIMS>(a, b);
     VolCoef co;
-    const float v = iou_fused<4>(P, Q, g, G1, G2, Extrude{z.dz, a.d, b.d}, &co);
+    const float v = iou_fused<4, kP2PiecesSmem>(P, Q, g, G1, G2, Extrude{z.dz, a.d, b.d}, &co,
+                                                QTable{pt + threadIdx.x, pt + 8 * T + threadIdx.x, T});
     if (iou) __stcs(iou + k, v);
     float gcz1, gd1, gcz2, gd2;
     z_grads<DIMS>(co, z, gcz1, gd1, gcz2, gd2);

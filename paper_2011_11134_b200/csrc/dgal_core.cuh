@@ -259,7 +259,10 @@ struct Clip {
 //   kP2Smem    per-event form, the vertex read from a per-thread shared-memory
 //              table (QTable) — one LDS instead of a select tree (the LSU pipe is
 //              idle in these kernels, the ALU pipe is the binding one).
-enum P2Mode { kP2Pieces = 0, kP2Regs = 1, kP2Smem = 2 };
+enum P2Mode { kP2Pieces = 0, kP2Regs = 1, kP2Smem = 2, kP2PiecesSmem = 3 };
+// kP2PiecesSmem: the piece end points of kP2Pieces, scattered by event into a
+//              per-thread shared-memory table (QTable x/y = a, stride; b at +2K)
+//              instead of per-(edge, line) selects, then read back.
 
 // Per-thread table of p2's (recentred) vertices in shared memory: vertex j at
 // x[j * stride], y[j * stride].  Written and read by the same thread only.
@@ -272,7 +275,8 @@ template <int K, int MODE>
 __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &Q, Clip<K> &c,
                                                QTable qt = QTable{nullptr, nullptr, 0})
 {
-    constexpr bool PIECES = (MODE == kP2Pieces);
+    constexpr bool PIECES = (MODE == kP2Pieces || MODE == kP2PiecesSmem);
+    constexpr bool PSMEM = (MODE == kP2PiecesSmem);
     constexpr uint32_t KMASK = (1u << K) - 1u;
     // edge vectors g_i = v_i+1 - v_i (p1), f_j = w_j+1 - w_j (p2); shoelace terms
     float *gx = c.gx, *gy = c.gy, *fx = c.fx, *fy = c.fy, *C1 = c.C1, *C2 = c.C2;
@@ -349,12 +353,20 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     float p2e = 0.f;
     uint32_t ev_out = 0, ev_in = 0;
     float *ax = c.ax, *ay = c.ay, *bx = c.bx, *by = c.by;
+    // kP2PiecesSmem table: a_j at (qt.x, qt.y)[j * st], b_j at (qt.x, qt.y)[(K + j) * st]
+    float *tx = const_cast<float *>(qt.x), *ty = const_cast<float *>(qt.y);
+    const int tst = qt.stride;
     if (PIECES) {
 #pragma unroll
         for (int j = 0; j < K; ++j) {
             const int j1 = (j + 1) % K;
-            ax[j] = Q.x[j]; ay[j] = Q.y[j];
-            bx[j] = Q.x[j1]; by[j] = Q.y[j1];
+            if (PSMEM) {
+                tx[j * tst] = Q.x[j]; ty[j * tst] = Q.y[j];
+                tx[(K + j) * tst] = Q.x[j1]; ty[(K + j) * tst] = Q.y[j1];
+            } else {
+                ax[j] = Q.x[j]; ay[j] = Q.y[j];
+                bx[j] = Q.x[j1]; by[j] = Q.y[j1];
+            }
         }
     }
 #pragma unroll
@@ -390,7 +402,10 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
         ev_out |= has_out ? (1u << ljout) : 0u;
         const float xox = fmaf(a1, gx[i], P.x[i]), xoy = fmaf(a1, gy[i], P.y[i]);
         const float xix = fmaf(a0, gx[i], P.x[i]), xiy = fmaf(a0, gy[i], P.y[i]);
-        if (PIECES) {
+        if (PSMEM) {
+            if (has_out) { tx[ljout * tst] = xox; ty[ljout * tst] = xoy; }
+            if (has_in) { tx[(K + ljin) * tst] = xix; ty[(K + ljin) * tst] = xiy; }
+        } else if (PIECES) {
             const int ji = has_in ? (int)ljin : 8;   // 8: no event
             const int jo = has_out ? (int)ljout : 8;
 #pragma unroll
@@ -415,6 +430,13 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
         }
     }
     c.jin = jin; c.jout = jout; c.valid = valid; c.enter = enter; c.leave = leave;
+    if (PSMEM) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            ax[j] = tx[j * tst]; ay[j] = ty[j * tst];
+            bx[j] = tx[(K + j) * tst]; by[j] = ty[(K + j) * tst];
+        }
+    }
 
     // p2 vertex j inside p1 <=> the last event on p2 edges j-1, j-2, ... (cyclic) is
     // an exit without an entry after it.  Segmented scan over the doubled cycle:
@@ -565,15 +587,16 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
 // trip, no crossing recomputation): dA_i/dv_i += n_i ∫(1-t)dt, dA_i/dv_i+1 +=
 // n_i ∫t dt over each boundary piece, then the S:303 chain.
 // p1, p2 recentred on p1.v0.  Returns IoU (identical to the pairwise path).
-template <int K>
+template <int K, int MODE = kP2Pieces>
 __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, float g, Poly<K> &G1,
-                                           Poly<K> &G2, const Extrude ex = flat(), VolCoef *co = nullptr)
+                                           Poly<K> &G2, const Extrude ex = flat(), VolCoef *co = nullptr,
+                                           QTable qt = QTable{nullptr, nullptr, 0})
 {
 #pragma unroll
     for (int k = 0; k < K; ++k) { G1.x[k] = 0.f; G1.y[k] = 0.f; G2.x[k] = 0.f; G2.y[k] = 0.f; }
     if (co) *co = VolCoef{0.f, 0.f, 0.f, 0.f, 0.f};
     Clip<K> c;
-    clip_intervals<K, kP2Pieces>(P, Q, c);
+    clip_intervals<K, MODE>(P, Q, c, qt);
     if (!c.nonempty) return 0.f;
     // V = A d (2D: d = 1); IoU = V_i / V_u
     const float Vix2 = c.Aix2 * ex.dz;
