@@ -302,3 +302,29 @@ def test_near_coincident_gradients(scale):
     ref = oracle.iou_paired_bwd((x1, y1), (x2, y2), g)
     for got, want in zip(gr, ref):
         assert_grad_close(got.cpu().numpy()[same], want[same])
+
+
+@pytest.mark.parametrize("scale", [1e-7, 1e-5, 1e-3, 1e-2])
+def test_near_coincident_octagons_iou(scale):
+    """K = 8: convex octagons (ellipse-inscribed, as cfg4) and a copy with every vertex
+    moved by ~scale x size (still convex at these scales): IoU within 1e-5 on every pair,
+    and a valid record (3 <= nx <= 16)."""
+    rng = np.random.default_rng(30 + int(-math.log10(scale)))
+    n = 50_000
+    c = rng.uniform(-10, 10, (n, 2))
+    a = rng.uniform(1, 3, n)
+    b = a * rng.uniform(0.6, 1.0, n)
+    phi = rng.uniform(-np.pi, np.pi, n)
+    ang = (np.arange(8)[None, :] + rng.uniform(-0.3, 0.3, (n, 8))) * np.pi / 4
+    ex, ey = a[:, None] * np.cos(ang), b[:, None] * np.sin(ang)
+    x1 = c[:, :1] + np.cos(phi)[:, None] * ex - np.sin(phi)[:, None] * ey
+    y1 = c[:, 1:] + np.sin(phi)[:, None] * ex + np.cos(phi)[:, None] * ey
+    x2 = x1 + rng.normal(size=x1.shape) * scale * a[:, None] * (rng.uniform(size=x1.shape) < 0.6)
+    y2 = y1 + rng.normal(size=y1.shape) * scale * a[:, None] * (rng.uniform(size=y1.shape) < 0.6)
+    x1, y1, x2, y2 = (v.astype(np.float32) for v in (x1, y1, x2, y2))
+    T = lambda v: torch.from_numpy(np.ascontiguousarray(v)).to(dev())  # noqa: E731
+    iou, nx, xf = dgal.iou_paired_fwd(T(x1), T(y1), T(x2), T(y2))
+    ref = oracle.iou_paired_fwd((x1, y1), (x2, y2))
+    assert_iou_close(iou.cpu().numpy(), ref["iou"])
+    nxc = nx.cpu().numpy()
+    assert np.all((nxc >= 3) & (nxc <= 16))
