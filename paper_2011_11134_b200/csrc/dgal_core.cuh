@@ -97,15 +97,6 @@ __device__ __forceinline__ uint64_t shr64(uint64_t x, uint32_t s)
     return r;
 }
 
-template <int K>
-__device__ __forceinline__ float pick(const float (&a)[K], int i)
-{
-    float r = a[0];
-#pragma unroll
-    for (int k = 1; k < K; ++k) r = (i == k) ? a[k] : r;
-    return r;
-}
-
 // (x[i], y[i]) for a dynamic i in [0, K): a select tree on the bits of i (the two
 // coordinates share the predicates).
 template <int K>
@@ -159,19 +150,6 @@ struct Seq {
     static constexpr int NW = K / 4;  // 64-bit words
     uint64_t w[NW];
 };
-
-// OR the (<= 8 byte) value r into the byte string at byte offset pos (0..2K-1).
-template <int K>
-__device__ __forceinline__ void seq_or(Seq<K> &s, uint64_t r, int pos)
-{
-    if (K == 4) {
-        s.w[0] |= shl64(r, 8u * (uint32_t)pos);
-    } else {
-        const uint32_t sh = 8u * (uint32_t)pos;
-        s.w[0] |= shl64(r, sh);
-        s.w[Seq<K>::NW - 1] |= (sh >= 64u) ? shl64(r, sh - 64u) : shr64(r, 64u - sh);
-    }
-}
 
 template <int K>
 __device__ __forceinline__ uint32_t seq_byte(const Seq<K> &s, int p)  // p static
