@@ -566,7 +566,15 @@ def main(argv=None):
                      "paired_fwd": {"ms": fwd_ms, "GB/s": fwd_gbs, "frac": fwd_gbs / peak},
                      "paired_bwd": {"ms": bwd_ms, "GB/s": bwd_gbs, "frac": bwd_gbs / peak},
                      "step_GB/s": n * (fb + bb) / (ms / args.steps * 1e-3) / 1e9,
-                     "step_frac": n * (fb + bb) / (ms / args.steps * 1e-3) / 1e9 / peak},
+                     "step_frac": n * (fb + bb) / (ms / args.steps * 1e-3) / 1e9 / peak,
+                     # the same step against the nominal 8 TB/s, and the
+                     # algorithmic FP32 fraction beside it (SH-method flops: 184 fwd + 195 bwd
+                     # per K=4 pair; FP32 peak 148 SMs x 128 lanes x 2 x SM clock)
+                     "step_frac_nominal_hbm": n * (fb + bb) / (ms / args.steps * 1e-3) / 1e9 / 8000.0,
+                     "fp32_algorithmic_tflops": n * 379 / (ms / args.steps * 1e-3) / 1e12,
+                     "fp32_algorithmic_frac": (n * 379 / (ms / args.steps * 1e-3) / 1e12)
+                                              / (148 * 128 * 2 * 1965e6 / 1e12),
+                     "binding_units": "ALU pipe / issue slots (ncu, profiles/README.md): not FP32, not HBM"},
         "clocks": sampler.summary(t0, t1),
         "gpu_launches": 2 * args.steps,
         "e2e": e2e,
