@@ -19,7 +19,7 @@ import torch
 
 from ._lib import DgalError, call, lib  # noqa: F401
 
-__all__ = ["iou_paired_fwd", "iou_paired_bwd", "iou_paired_fused", "PolyIoULoss",
+__all__ = ["iou_paired_fwd", "iou_paired_bwd", "iou_paired_fused", "iou_paired", "iou_paired_backward", "PolyIoULoss",
            "box_iou_paired_fwd", "box_iou_paired_bwd", "box_iou_paired_fused", "BoxIoU", "BoxIoULoss", "iou_pairwise", "pairwise_workspace", "nms_round", "nms_keep",
            "nms", "PolyIoU", "DgalError", "build_info"]
 
@@ -305,3 +305,8 @@ class PolyIoU(torch.autograd.Function):
     def backward(ctx, g):
         x1, y1, x2, y2, nx, xf = ctx.saved_tensors
         return iou_paired_bwd(x1, y1, x2, y2, g.contiguous().float(), nx, xf)
+
+
+# SURVEY §8(b) shim names (same functions)
+iou_paired = iou_paired_fwd
+iou_paired_backward = iou_paired_bwd

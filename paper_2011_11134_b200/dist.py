@@ -41,6 +41,9 @@ def iou_paired_shard(x1, y1, x2, y2, grad, world: int, rank: int):
     return lo, hi, iou, nx, xf, g
 
 
+iou_paired_sharded = iou_paired_shard   # SURVEY §8(b) name
+
+
 def nms_rounds(n: int, lo: int, hi: int, round_fn: Callable[[torch.Tensor], None],
                status: torch.Tensor, group=None, max_rounds: Optional[int] = None) -> int:
     """Run NMS rounds to convergence.
