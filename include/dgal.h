@@ -62,6 +62,10 @@ typedef struct CUstream_st *dgal_stream;
  *   iou    [n]       float, overwritten
  *   nx     [n]       uint8, overwritten (0 or 3..2K)
  *   xflags [n * 2K]  uint8, overwritten (see flag bytes above)
+ *
+ * Polygons with m < K vertices (triangles in K = 4, 5..7-gons in K = 8): repeat the
+ * last vertex K - m times; the result is the IoU of the m-gon, and the gradient of
+ * that vertex is the SUM over its copies (tests/test_gpu_paired.py::test_padded_polygons).
  */
 dgal_status dgal_iou_paired_fwd(int K, int64_t n,
                                 const float *x1, const float *y1,

@@ -283,15 +283,17 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
             d[i][j] = __fadd_rn(cross_rn(fx[j], fy[j], Dx, Dy), kTiny);
         }
 
-    // Separating p2 edge line (closed): p1 entirely on or outside it -> the
-    // intersection has zero area (makes touching edges exactly empty).
+    // Separating p2 edge line: p1 strictly outside it -> empty.  Strict, so a
+    // zero-length edge (a repeated vertex: polygons with fewer than K vertices are
+    // padded that way), whose d are all exactly tiny, separates nothing; p1
+    // touching a line from outside reaches zero area through the closed boundary.
     bool separated = false;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         float m1 = d[0][j];
 #pragma unroll
         for (int i = 1; i < K; ++i) m1 = fmaxf(m1, d[i][j]);
-        separated |= (m1 <= kTiny);
+        separated |= (m1 < kTiny);
     }
 
     // p1 vertices inside p2 (closed test, d never 0)
@@ -432,7 +434,8 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
         my *= (1.f / K);
         bool cin = true;
 #pragma unroll
-        for (int i = 0; i < K; ++i) cin &= cross_rn(gx[i], gy[i], mx - P.x[i], my - P.y[i]) > 0.f;
+        for (int i = 0; i < K; ++i)   // (a zero-length edge of a padded p1 is no constraint)
+            cin &= (cross_rn(gx[i], gy[i], mx - P.x[i], my - P.y[i]) > 0.f) | (fabsf(gx[i]) + fabsf(gy[i]) == 0.f);
         in2 = (valid == 0u && cin) ? KMASK : 0u;
     } else {
         uint32_t evd = ev | (ev << K);

@@ -328,3 +328,43 @@ def test_near_coincident_octagons_iou(scale):
     assert_iou_close(iou.cpu().numpy(), ref["iou"])
     nxc = nx.cpu().numpy()
     assert np.all((nxc >= 3) & (nxc <= 16))
+
+
+@pytest.mark.parametrize("m,K", [(3, 4), (5, 8), (6, 8), (7, 8)])
+def test_padded_polygons(m, K):
+    """Polygons with m < K vertices, padded by repeating the last vertex (include/dgal.h):
+    IoU and the gradient of each real vertex (summed over its copies) equal the oracle on
+    the unpadded polygons (margin inputs)."""
+    rng = np.random.default_rng(50 + m)
+    n = 20000
+    def convex():
+        c = rng.uniform(-5, 5, (n, 2)); a = rng.uniform(1, 3, n); b = a * rng.uniform(0.5, 1, n)
+        # vertex angles at least 0.6 rad apart: no sliver polygons (a sliver intersection far
+        # from p1.v0 is conditioned by the origin distance, DESIGN.md §4.1)
+        gaps = rng.uniform(0.6, 1.0, (n, m))
+        gaps = gaps / gaps.sum(1, keepdims=True) * (2 * np.pi - 0.6 * m) + 0.6
+        ang = rng.uniform(0, 2 * np.pi, (n, 1)) + np.cumsum(gaps, 1) - gaps[:, :1]
+        phi = rng.uniform(-np.pi, np.pi, n)
+        ex, ey = a[:, None] * np.cos(ang), b[:, None] * np.sin(ang)
+        return ((c[:, :1] + np.cos(phi)[:, None] * ex - np.sin(phi)[:, None] * ey).astype(np.float32),
+                (c[:, 1:] + np.sin(phi)[:, None] * ex + np.cos(phi)[:, None] * ey).astype(np.float32))
+    x1, y1 = convex()
+    x2, y2 = convex()
+    x2 += (x1.mean(1, keepdims=True) - x2.mean(1, keepdims=True)) * 0.8
+    y2 += (y1.mean(1, keepdims=True) - y2.mean(1, keepdims=True)) * 0.8
+    ok = oracle.margin_ok((x1, y1), (x2, y2))
+    x1, y1, x2, y2 = (v[ok] for v in (x1, y1, x2, y2))
+    pad = lambda v: np.ascontiguousarray(np.concatenate([v, np.repeat(v[:, -1:], K - m, 1)], 1))  # noqa: E731
+    T = lambda v: torch.from_numpy(pad(v)).to(dev())  # noqa: E731
+    X = (T(x1), T(y1), T(x2), T(y2))
+    g = np.random.default_rng(1).uniform(-1, 1, x1.shape[0]).astype(np.float32)
+    iou, nx, xf = dgal.iou_paired_fwd(*X)
+    gr = dgal.iou_paired_bwd(*X, torch.from_numpy(g).to(dev()), nx, xf)
+    ref = oracle.iou_paired_fwd((x1, y1), (x2, y2))
+    assert_iou_close(iou.cpu().numpy(), ref["iou"])
+    rg = oracle.iou_paired_bwd((x1, y1), (x2, y2), g)
+    for got, want in zip(gr, rg):
+        got = got.cpu().numpy()
+        folded = got[:, :m].copy()
+        folded[:, m - 1] += got[:, m:].sum(1)
+        assert_grad_close(folded, want)

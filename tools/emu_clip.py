@@ -59,7 +59,7 @@ def clip(P, Q, verbose=False):
             e[j, i] = f32(cross(Dx, Dy, g[i, 0], g[i, 1]) - TINY)
     separated = False
     for j in range(K):
-        separated |= (d[:, j].max() <= TINY)
+        separated |= (d[:, j].max() < TINY)
     cxm = f32(sum(Q[:, 0]) * f32(1.0 / K)); cym = f32(sum(Q[:, 1]) * f32(1.0 / K))
     cin = all(cross(g[i, 0], g[i, 1], f32(cxm - P[i, 0]), f32(cym - P[i, 1])) > 0 for i in range(K))
     emin = e.min()
