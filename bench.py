@@ -401,6 +401,72 @@ def bench_box(ctx, dims, n, steps, warmup, peak):
                                    "algorithmic_bytes_per_pair": ub}}}
 
 
+def bench_cfg2(ctx, steps, warmup):
+    """cfg2: pairwise 2000 x 2000 KITTI-scale scene (40 objects x 50 proposals), IoU matrix +
+    NMS mask + suppressor lists + greedy keep, one GPU (a latency-bound small problem:
+    reported, no roofline claim)."""
+    import paper_2011_11134_b200 as dgal
+    import synth
+    torch = ctx.torch
+    sc = synth.gen_cfg2_scene()
+    n = sc.polys.n
+    x = torch.from_numpy(sc.polys.x.reshape(n, 4)).to(ctx.dev)
+    y = torch.from_numpy(sc.polys.y.reshape(n, 4)).to(ctx.dev)
+    ws = dgal.pairwise_workspace(n, ctx.dev)
+    cap = 64
+    out = (torch.empty((n, n), dtype=torch.float32, device=ctx.dev),
+           torch.empty((n, (n + 63) // 64), dtype=torch.int64, device=ctx.dev),
+           torch.empty(n, dtype=torch.int32, device=ctx.dev),
+           torch.empty((n, cap), dtype=torch.int32, device=ctx.dev))
+    status = torch.empty(n, dtype=torch.uint8, device=ctx.dev)
+    keep = torch.empty(n, dtype=torch.uint8, device=ctx.dev)
+
+    def step():
+        dgal.iou_pairwise(x, y, x, y, thr=sc.thr, nbr_cap=cap, out=out, workspace=ws)
+        dgal.nms_keep(out[1], out[2], out[3], status=status, keep=keep)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(ctx.dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    kept = int(keep.sum().item())
+    # the same step captured once in a CUDA graph (the library never allocates or
+    # synchronises, so its launches are capturable) and replayed: launch-bound work
+    graph_ms = None
+    try:
+        g = torch.cuda.CUDAGraph()
+        sstream = torch.cuda.Stream(ctx.dev)
+        sstream.wait_stream(stream)
+        with torch.cuda.stream(sstream):
+            step()                      # warm the allocator on the capture stream
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=sstream):
+                step()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        assert int(keep.sum().item()) == kept
+        a.record(stream)
+        for _ in range(steps):
+            g.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+        graph_ms = a.elapsed_time(b) / steps
+    except Exception as exc:  # noqa: BLE001 — reported, the eager number stands
+        graph_ms = f"capture failed: {type(exc).__name__}: {exc}"[:200]
+    return {"workload": "cfg2: pairwise 2000 x 2000 KITTI-scale scene, IoU matrix + NMS mask + lists + keep",
+            "ms_per_step": ms, "pairs_per_s": n * n / (ms * 1e-3), "kept": kept,
+            "cuda_graph_ms_per_step": graph_ms,
+            "note": "latency-bound (16 MB output); one GPU; no roofline claim (SURVEY 8(d))"}
+
+
 def bench_cfg5(ctx, steps, warmup, peak):
     """Pairwise 100k x 100k IoU matrix + NMS mask/lists + greedy keep; rows sharded."""
     import paper_2011_11134_b200 as dgal
@@ -534,6 +600,8 @@ def main(argv=None):
         secondary["cfg3_fused"] = bench_fused(ctx, n, max(10, args.steps // 4), args.warmup, peak)
         secondary["box2d"] = bench_box(ctx, 2, n, max(10, args.steps // 4), args.warmup, peak)
         secondary["box3d"] = bench_box(ctx, 3, n, max(10, args.steps // 4), args.warmup, peak)
+        if world == 1:
+            secondary["cfg2"] = bench_cfg2(ctx, steps=50, warmup=5)
         secondary["cfg5"] = bench_cfg5(ctx, steps=5, warmup=2, peak=peak)
 
     if ctx.dist:
