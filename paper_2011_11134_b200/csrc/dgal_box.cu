@@ -240,6 +240,7 @@ struct BoxGeometry {
     __device__ __forceinline__ void get(int pt, int i, int i1, int j, int j1, double &vx, double &vy, double &v1x,
                                         double &v1y, double &wx, double &wy, double &w1x, double &w1y) const
     {
+        DGAL_ASSERT(pt >= 0 && pt < kBoxTile && i >= 0 && i < 4 && i1 >= 0 && i1 < 4 && j >= 0 && j < 4 && j1 >= 0 && j1 < 4);
         const double dcx = (double)p[5 * kBoxTile + pt] - (double)p[pt];
         const double dcy = (double)p[6 * kBoxTile + pt] - (double)p[kBoxTile + pt];
         const double w1 = p[2 * kBoxTile + pt], h1 = p[3 * kBoxTile + pt], t1 = p[4 * kBoxTile + pt];

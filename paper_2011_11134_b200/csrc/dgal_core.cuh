@@ -382,6 +382,7 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
         ev_out |= has_out ? (1u << ljout) : 0u;
         const float xox = fmaf(a1, gx[i], P.x[i]), xoy = fmaf(a1, gy[i], P.y[i]);
         const float xix = fmaf(a0, gx[i], P.x[i]), xiy = fmaf(a0, gy[i], P.y[i]);
+        DGAL_ASSERT(ljin < (uint32_t)K && ljout < (uint32_t)K);
         if (PSMEM) {
             if (has_out) { tx[ljout * tst] = xox; ty[ljout * tst] = xoy; }
             if (has_in) { tx[(K + ljin) * tst] = xix; ty[(K + ljin) * tst] = xiy; }

@@ -131,6 +131,7 @@ nms_keep_grid_kernel(int64_t n, const uint64_t *__restrict__ mask, int64_t mask_
         if (t0 == 0) cnt[(r + 1) & 1] = 0;
         int still = 0;
         for (int64_t i = t0; i < n; i += stride) {
+            DGAL_ASSERT(i >= 0 && i < n);
             if (vs[i] != 0) continue;
             const int d = decide(i, i, mask, mask_words, nbr_count, nbr_idx, cap, vs);
             if (d) vs[i] = (uint8_t)d;
