@@ -26,11 +26,20 @@ constexpr int kBoxTile = 256;  // backward tile = CTA size
 // CTAs per SM the box forward / fused kernels are register-budgeted for (the
 // largest without local-memory spills, tools/sass_stats.py)
 #ifndef DGAL_BOX_FWD2_MINB
-#define DGAL_BOX_FWD2_MINB 3
+#define DGAL_BOX_FWD2_MINB 6
 #endif
 #ifndef DGAL_BOX_FWD3_MINB
-#define DGAL_BOX_FWD3_MINB 2
+#define DGAL_BOX_FWD3_MINB 4
 #endif
+// forward CTA shape (as the K = 4 polygon forward: 128 threads, 8 tiles per CTA so
+// the walk-table fill is amortised)
+#ifndef DGAL_BOX_FWD_T
+#define DGAL_BOX_FWD_T 128
+#endif
+#ifndef DGAL_BOX_FWD_NT
+#define DGAL_BOX_FWD_NT 8
+#endif
+constexpr int kBoxFwdT = DGAL_BOX_FWD_T, kBoxFwdNT = DGAL_BOX_FWD_NT;
 #ifndef DGAL_BOX_FUSED_MINB
 #define DGAL_BOX_FUSED_MINB 2
 #endif
@@ -184,38 +193,54 @@ __device__ __forceinline__ void z_grads(const VolCoef &co, const ZOver &z, float
 // forward: IoU (2D) or 3D IoU, nx / xflags of the BEV intersection
 // ---------------------------------------------------------------------------
 template <int DIMS>
-__global__ void __launch_bounds__(kPairedThreads, DIMS == 2 ? DGAL_BOX_FWD2_MINB : DGAL_BOX_FWD3_MINB)
+__global__ void __launch_bounds__(kBoxFwdT, DIMS == 2 ? DGAL_BOX_FWD2_MINB : DGAL_BOX_FWD3_MINB)
 box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict__ b2, int64_t sk, int64_t sp,
                float *__restrict__ iou, uint8_t *__restrict__ nx, uint8_t *__restrict__ xflags)
 {
-    __shared__ float sq[8 * kPairedThreads];   // per-thread p2 vertex table (kP2Smem), [k][thread]
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    const Box<DIMS> a = load_box<DIMS>(b1, k, sk, sp), b = load_box<DIMS>(b2, k, sk, sp);
-    Poly<4> P, Q;
-    box_pair_polys<DIMS>(a, b, P, Q);
+    constexpr int T = kBoxFwdT;
+    __shared__ float sq[8 * T];   // per-thread p2 vertex table (kP2Smem), [k][thread]
+    __shared__ WalkLut4 wlut;     // flag-walk tables
+    const int64_t k0 = (int64_t)blockIdx.x * (kBoxFwdNT * T) + threadIdx.x;
+    Box<DIMS> a, b;
+    if (k0 < n) {   // the first tile's loads go out before the table fill
+        a = load_box<DIMS>(b1, k0, sk, sp);
+        b = load_box<DIMS>(b2, k0, sk, sp);
+    }
+    load_walk_lut4(wlut, threadIdx.x, T);
+    __syncthreads();
+#pragma unroll 1
+    for (int t = 0; t < kBoxFwdNT; ++t) {
+        const int64_t k = k0 + (int64_t)t * T;
+        if (k >= n) break;
+        if (t > 0) {
+            a = load_box<DIMS>(b1, k, sk, sp);
+            b = load_box<DIMS>(b2, k, sk, sp);
+        }
+        Poly<4> P, Q;
+        box_pair_polys<DIMS>(a, b, P, Q);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        sq[q * kPairedThreads + threadIdx.x] = Q.x[q];
-        sq[(4 + q) * kPairedThreads + threadIdx.x] = Q.y[q];
+        for (int q = 0; q < 4; ++q) {
+            sq[q * T + threadIdx.x] = Q.x[q];
+            sq[(4 + q) * T + threadIdx.x] = Q.y[q];
+        }
+        const FwdOut<4, true> r = iou_fwd<4, true, kP2Smem>(P, Q, QTable{sq + threadIdx.x, sq + 4 * T + threadIdx.x, T},
+                                                            &wlut);
+        float v = r.iou;
+        int m = r.nx;
+        uint64_t seq = r.seq.w[0];
+        if (DIMS == 3) {
+            const ZOver z = z_overlap<DIMS>(a, b);
+            const float Vix2 = r.Aix2 * z.dz;
+            const float Vux2 = (r.A1x2 * a.d + r.A2x2 * b.d) - Vix2;
+            const bool ok = m > 0 && Vix2 > 0.f && Vux2 > 0.f;
+            v = ok ? fminf(Vix2 / Vux2, 1.f) : 0.f;
+            m = ok ? m : 0;
+            seq = ok ? seq : 0ull;
+        }
+        __stcs(iou + k, v);
+        nx[k] = (uint8_t)m;
+        __stcs(reinterpret_cast<unsigned long long *>(xflags) + k, (unsigned long long)seq);
     }
-    const FwdOut<4, true> r = iou_fwd<4, true, kP2Smem>(
-        P, Q, QTable{sq + threadIdx.x, sq + 4 * kPairedThreads + threadIdx.x, kPairedThreads});
-    float v = r.iou;
-    int m = r.nx;
-    uint64_t seq = r.seq.w[0];
-    if (DIMS == 3) {
-        const ZOver z = z_overlap<DIMS>(a, b);
-        const float Vix2 = r.Aix2 * z.dz;
-        const float Vux2 = (r.A1x2 * a.d + r.A2x2 * b.d) - Vix2;
-        const bool ok = m > 0 && Vix2 > 0.f && Vux2 > 0.f;
-        v = ok ? fminf(Vix2 / Vux2, 1.f) : 0.f;
-        m = ok ? m : 0;
-        seq = ok ? seq : 0ull;
-    }
-    __stcs(iou + k, v);
-    nx[k] = (uint8_t)m;
-    __stcs(reinterpret_cast<unsigned long long *>(xflags) + k, (unsigned long long)seq);
 }
 
 // ---------------------------------------------------------------------------
@@ -358,11 +383,11 @@ cudaError_t launch_box_fwd(int dims, int layout, int64_t n, const float *b1, con
 {
     int64_t sk, sp;
     box_strides(dims, layout, n, sk, sp);
-    const unsigned grid = (unsigned)((n + kPairedThreads - 1) / kPairedThreads);
+    const unsigned grid = (unsigned)((n + kBoxFwdNT * kBoxFwdT - 1) / (kBoxFwdNT * kBoxFwdT));
     if (dims == 3)
-        box_fwd_kernel<3><<<grid, kPairedThreads, 0, st>>>(n, b1, b2, sk, sp, iou, nx, xflags);
+        box_fwd_kernel<3><<<grid, kBoxFwdT, 0, st>>>(n, b1, b2, sk, sp, iou, nx, xflags);
     else
-        box_fwd_kernel<2><<<grid, kPairedThreads, 0, st>>>(n, b1, b2, sk, sp, iou, nx, xflags);
+        box_fwd_kernel<2><<<grid, kBoxFwdT, 0, st>>>(n, b1, b2, sk, sp, iou, nx, xflags);
     return cudaGetLastError();
 }
 

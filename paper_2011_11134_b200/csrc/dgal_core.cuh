@@ -183,6 +183,85 @@ struct VolCoef {
     float cvi, cvu, ai, a1, a2;
 };
 
+// ---------------------------------------------------------------------------
+// Walk tables for K = 4 (the flag walk of iou_fwd and the p2 inside mask of
+// clip_intervals as table lookups: the forward is bound by the ALU pipe, and the
+// bit-serial walk was its largest ALU consumer — DESIGN.md §4.1).  Generated at
+// compile time from the same rules the bit-serial code implements; staged in
+// shared memory by the kernels that use them (load_walk_lut4).
+//
+//   e[st << 6 | jo << 4 | in2]: the flag bytes p1 edge i contributes, for edge
+//     state st = valid | has_in << 1 | has_out << 2, exit line jo and p2 inside
+//     mask in2, as {bytes lo, bytes hi, M, count}:
+//       byte 0   FromP1(i) = 0x40 | i, or the entry Cross(i, j_in) = 0xC0 | i << 3 | j_in
+//       byte 1   the exit Cross(i, jo) = 0xC0 | i << 3 | jo          (has_out)
+//       byte 2.. FromP2(jo+1), FromP2(jo+2), ... while inside p1    (has_out)
+//     without the terms in i and j_in: bytes + M * i is the group of edge i (M
+//     puts i in bits 0-2 of a FromP1 byte, bits 3-5 of a Cross byte), j_in is
+//     OR-ed in by the caller.  An invalid edge contributes nothing (all 0).
+//   in2[ev_in | ev_out << 4]: p2 vertices inside p1 given the p2 lines carrying
+//     an entry / an exit (the segmented scan of clip_intervals; 0 without events).
+// ---------------------------------------------------------------------------
+struct alignas(16) WalkLut4 {
+    uint32_t e[512][4];
+    uint8_t in2[256];
+};
+
+constexpr uint32_t walk4_in2(uint32_t ev_in, uint32_t ev_out)
+{
+    const uint32_t ev = ev_in | ev_out;
+    if (ev == 0u) return 0u;
+    uint32_t evd = ev | (ev << 4);
+    uint32_t st = (ev_out & ~ev_in) | ((ev_out & ~ev_in) << 4);
+    for (int sh = 1; sh < 8; sh <<= 1) {
+        st = (st & evd) | ((st << sh) & ~evd);
+        evd |= evd << sh;
+    }
+    return (st >> 3) & 0xFu;
+}
+
+constexpr WalkLut4 make_walk_lut4()
+{
+    WalkLut4 L{};
+    for (uint32_t idx = 0; idx < 512; ++idx) {
+        const uint32_t st = idx >> 6, jo = (idx >> 4) & 3u, in2 = idx & 15u;
+        const bool valid = st & 1u, has_in = st & 2u, has_out = st & 4u;
+        uint64_t g = 0;
+        uint32_t M = 0, c = 0;
+        if (valid) {
+            g = has_in ? 0xC0u : 0x40u;
+            M = has_in ? 8u : 1u;
+            c = 1;
+            if (has_out) {
+                g |= (uint64_t)(0xC0u | jo) << 8;
+                M |= 8u << 8;
+                c += 1;
+                const uint32_t p0 = (jo + 1u) & 3u;
+                const uint32_t rot = ((in2 | (in2 << 4)) >> p0) & 15u;
+                for (uint32_t r = 0; r < 4 && ((rot >> r) & 1u); ++r, ++c)
+                    g |= (uint64_t)(0x80u | ((p0 + r) & 3u)) << (16 + 8 * r);
+            }
+        }
+        L.e[idx][0] = (uint32_t)g;
+        L.e[idx][1] = (uint32_t)(g >> 32);
+        L.e[idx][2] = M;
+        L.e[idx][3] = c;
+    }
+    for (uint32_t v = 0; v < 256; ++v) L.in2[v] = (uint8_t)walk4_in2(v & 15u, v >> 4);
+    return L;
+}
+
+static __device__ const WalkLut4 kWalkLut4 = make_walk_lut4();
+
+// Stage the tables in shared memory (all threads of the CTA; the caller
+// synchronises before use).
+__device__ __forceinline__ void load_walk_lut4(WalkLut4 &dst, int tid, int nthreads)
+{
+    const uint4 *s = reinterpret_cast<const uint4 *>(&kWalkLut4);
+    uint4 *d = reinterpret_cast<uint4 *>(&dst);
+    for (int q = tid; q < (int)(sizeof(WalkLut4) / 16); q += nthreads) d[q] = __ldg(s + q);
+}
+
 // The edge-interval clip shared by the paired forward, the pairwise path and the
 // fused loss kernel.
 //
@@ -223,6 +302,7 @@ struct Clip {
     uint32_t jin, jout;                // line index of the entry / exit of p1 edge i (4 bits each)
     uint32_t valid, enter, leave;      // p1 edges with a piece / an entry / an exit (bit i)
     float ax[K], ay[K], bx[K], by[K];  // PIECES: piece on p2 edge j runs from (ax, ay) to (bx, by)
+    uint32_t key[K];                   // walk-table key of p1 edge i: st << 6 | jo << 4 | j_in << 16 (WalkLut4)
     uint32_t on2;                      // p2 edges carrying a boundary piece
     uint32_t in2;                      // p2 vertices inside p1 (consistent with the events)
     float A1x2, A2x2, Aix2;            // twice the areas
@@ -251,8 +331,10 @@ struct QTable {
 
 template <int K, int MODE>
 __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &Q, Clip<K> &c,
-                                               QTable qt = QTable{nullptr, nullptr, 0})
+                                               QTable qt = QTable{nullptr, nullptr, 0},
+                                               const WalkLut4 *wl = nullptr)
 {
+    const bool LUT = (K == 4) && wl != nullptr;   // in2 from the table (wl in shared memory)
     constexpr bool PIECES = (MODE == kP2Pieces || MODE == kP2PiecesSmem);
     constexpr bool PSMEM = (MODE == kP2PiecesSmem);
     constexpr uint32_t KMASK = (1u << K) - 1u;
@@ -331,6 +413,7 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     // (a piece with both events on one edge adds the product of two vectors along
     // that edge, which vanishes).  One vertex select per event, no per-edge state.
     float p2e = 0.f;
+    float Aix2 = 0.f;   // twice the area of p1 ∩ p2 (Green over the closed boundary)
     uint32_t ev_out = 0, ev_in = 0;
     float *ax = c.ax, *ay = c.ay, *bx = c.bx, *by = c.by;
     // kP2PiecesSmem table: a_j at (qt.x, qt.y)[j * st], b_j at (qt.x, qt.y)[(K + j) * st]
@@ -372,6 +455,10 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
                         (__int_as_float(__float_as_int(a0) & ~7) < __int_as_float(__float_as_int(a1) & ~7));
         const bool has_in = ok && !in_s, has_out = ok && !in_e;
         t0[i] = a0; t1[i] = a1;
+        // p1 side of Green's sum (same order as A1x2: identical polygons reproduce
+        // it).  Per-event modes: here, so t0 / t1 / C1 die early (registers); the
+        // piece modes keep the interleaved order below (A/B: fused kernel faster).
+        if (!PIECES) Aix2 = fmaf(fmaxf(a1 - a0, 0.f), C1[i], Aix2);
         valid |= (uint32_t)ok << i;
         enter |= (uint32_t)has_in << i;
         leave |= (uint32_t)has_out << i;
@@ -380,6 +467,8 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
         jout |= ljout << (4 * i);
         ev_in |= has_in ? (1u << ljin) : 0u;
         ev_out |= has_out ? (1u << ljout) : 0u;
+        c.key[i] = (ok ? 0x40u : 0u) | (has_in ? 0x80u : 0u) | (has_out ? 0x100u : 0u) | (ljout << 4) |
+                   ((has_in ? ljin : 0u) << 16);
         const float xox = fmaf(a1, gx[i], P.x[i]), xoy = fmaf(a1, gy[i], P.y[i]);
         const float xix = fmaf(a0, gx[i], P.x[i]), xiy = fmaf(a0, gy[i], P.y[i]);
         DGAL_ASSERT(ljin < (uint32_t)K && ljout < (uint32_t)K);
@@ -438,6 +527,8 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
         for (int i = 0; i < K; ++i)   // (a zero-length edge of a padded p1 is no constraint)
             cin &= (cross_rn(gx[i], gy[i], mx - P.x[i], my - P.y[i]) > 0.f) | (fabsf(gx[i]) + fabsf(gy[i]) == 0.f);
         in2 = (valid == 0u && cin) ? KMASK : 0u;
+    } else if (LUT) {
+        in2 = wl->in2[ev_in | (ev_out << 4)];
     } else {
         uint32_t evd = ev | (ev << K);
         uint32_t st = (ev_out & ~ev_in) | ((ev_out & ~ev_in) << K);
@@ -450,12 +541,11 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     }
     const uint32_t on2 = ev | in2;
 
-    // area of p1 ∩ p2 (Green over the closed boundary), interleaved so identical
-    // polygons (no events, no p2 piece) reproduce A1x2 bitwise
-    float Aix2 = 0.f;
+    // p2 side of Green's sum (identical polygons: no events, no p2 piece, so Aix2
+    // keeps the p1 side, which reproduces A1x2 bitwise); piece modes interleave
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        Aix2 = fmaf(fmaxf(t1[k] - t0[k], 0.f), C1[k], Aix2);
+        if (PIECES) Aix2 = fmaf(fmaxf(t1[k] - t0[k], 0.f), C1[k], Aix2);
         const float c2 = PIECES ? cross_rn(ax[k], ay[k], bx[k], by[k]) : C2[k];
         Aix2 = __fadd_rn(Aix2, ((on2 >> k) & 1u) ? c2 : 0.f);
     }
@@ -472,11 +562,12 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
 // p1, p2 must already be recentred on o = p1.v0 (p1.x[0] == p1.y[0] == 0).
 template <int K, bool FLAGS, int MODE = (K == 4 ? kP2Pieces : kP2Regs)>
 __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly<K> &Q,
-                                                    QTable qt = QTable{nullptr, nullptr, 0})
+                                                    QTable qt = QTable{nullptr, nullptr, 0},
+                                                    const WalkLut4 *wl = nullptr)
 {
     constexpr uint32_t KMASK = (1u << K) - 1u;
     Clip<K> c;
-    clip_intervals<K, MODE>(P, Q, c, qt);
+    clip_intervals<K, MODE>(P, Q, c, qt, wl);
     const float *t0 = c.t0, *t1 = c.t1;
     const float A1x2 = c.A1x2, A2x2 = c.A2x2, Aix2 = c.Aix2;
     bool nonempty = c.nonempty;
@@ -500,6 +591,26 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
 #pragma unroll
         for (int k = 0; k < Seq<K>::NW; ++k) s.w[k] = 0;
         int pos = 0;
+        if (K == 4 && wl != nullptr) {
+            // table walk: edge i's group = table bytes + M i | j_in, at the byte offset
+            // given by the prefix sum of the counts (all four in one multiply)
+            uint32_t glo[4], ghi[4], cnt = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t key = c.key[i];
+                const uint4 e = *reinterpret_cast<const uint4 *>(wl->e[(key & 0x1F0u) | in2]);
+                glo[i] = (e.x + e.z * (uint32_t)i) | (key >> 16);
+                ghi[i] = e.y;
+                cnt += e.w << (8 * i);
+            }
+            const uint32_t off = cnt * 0x08080800u;   // byte i: 8 x (count of edges < i)
+            uint64_t w = (uint64_t)ghi[0] << 32 | glo[0];
+#pragma unroll
+            for (int i = 1; i < 4; ++i)
+                w |= shl64((uint64_t)ghi[i] << 32 | glo[i], (off >> (8 * i)) & 0xFFu);
+            s.w[0] = w;
+            pos = (int)((cnt * 0x01010101u) >> 24);
+        } else {
 #pragma unroll
         for (int i = 0; i < K; ++i) {
             const bool valid = (c.valid >> i) & 1u;
@@ -539,6 +650,7 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
                 s.w[Seq<K>::NW - 1] |= valid ? ohi : 0ull;
                 pos += valid ? (has_out ? 2 + (int)L : 1) : 0;
             }
+        }
         }
         if (pos == 0 && in2 == KMASK) {  // p2 inside p1: all FromP2, in order
             if (K == 4) s.w[0] = 0x83828180ull;

@@ -28,15 +28,23 @@ __device__ __forceinline__ void recentre(Poly<K> &P, Poly<K> &Q)
 // bulk-copy pipeline (tried: DESIGN.md §4.1) costs more in registers than the
 // latency it hides; for K = 8 it also spills.
 #ifndef DGAL_FWD4_MINB
-#define DGAL_FWD4_MINB 3     // CTAs per SM the K=4 forward is register-budgeted for
+#define DGAL_FWD4_MINB 6     // CTAs per SM the K=4 forward is register-budgeted for
 #endif
 #ifndef DGAL_FWD4_THREADS
-#define DGAL_FWD4_THREADS 256
+#define DGAL_FWD4_THREADS 128
 #endif
 constexpr int kFwd4Threads = DGAL_FWD4_THREADS;
 
+#ifndef DGAL_FWD4_WALKLUT
+#define DGAL_FWD4_WALKLUT 1   // K = 4 flag walk + p2 inside mask from shared-memory tables
+#endif
+
 #ifndef DGAL_FWD_P2MODE
 #define DGAL_FWD_P2MODE kP2Smem   // how the forward forms the p2 side (dgal_core.cuh P2Mode)
+#endif
+
+#ifndef DGAL_FWD4_NT
+#define DGAL_FWD4_NT 8        // K = 4: consecutive tiles of T pairs per CTA (amortises the table fill)
 #endif
 
 template <int K>
@@ -46,28 +54,45 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
                          float *__restrict__ iou, uint8_t *__restrict__ nx, uint8_t *__restrict__ xflags)
 {
     constexpr int T = (K == 4) ? kFwd4Threads : kPairedThreads;
+    constexpr bool WL = (K == 4) && DGAL_FWD4_WALKLUT;
+    constexpr int NT = (K == 4) ? DGAL_FWD4_NT : 1;
     __shared__ float sq[2 * K * T];   // per-thread p2 vertex table, [k][thread] (DGAL_FWD_P2MODE == kP2Smem)
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
+    __shared__ WalkLut4 wlut[1];      // K = 4: the walk tables (DGAL_FWD4_WALKLUT; unused otherwise)
+    const int64_t k0 = (int64_t)blockIdx.x * (NT * T) + threadIdx.x;
     Poly<K> P, Q;
-    load_poly<K>(x1, y1, k, P);
-    load_poly<K>(x2, y2, k, Q);
-    recentre<K>(P, Q);
-    QTable qt{sq + threadIdx.x, sq + K * T + threadIdx.x, T};
-    if (DGAL_FWD_P2MODE == kP2Smem) {
-#pragma unroll
-        for (int q = 0; q < K; ++q) { sq[q * T + threadIdx.x] = Q.x[q]; sq[(K + q) * T + threadIdx.x] = Q.y[q]; }
+    if (k0 < n) {   // the first tile's loads go out before the table fill
+        load_poly<K>(x1, y1, k0, P);
+        load_poly<K>(x2, y2, k0, Q);
     }
-    const FwdOut<K, true> r = iou_fwd<K, true, DGAL_FWD_P2MODE>(P, Q, qt);
-    __stcs(iou + k, r.iou);
-    nx[k] = (uint8_t)r.nx;
-    if (K == 4) {
-        __stcs(reinterpret_cast<unsigned long long *>(xflags) + k, (unsigned long long)r.seq.w[0]);
-    } else {
-        ulonglong2 v;
-        v.x = r.seq.w[0];
-        v.y = r.seq.w[Seq<K>::NW - 1];
-        __stcs(reinterpret_cast<ulonglong2 *>(xflags) + k, v);
+    if (WL) {
+        load_walk_lut4(wlut[0], threadIdx.x, T);
+        __syncthreads();
+    }
+    QTable qt{sq + threadIdx.x, sq + K * T + threadIdx.x, T};
+#pragma unroll 1
+    for (int t = 0; t < NT; ++t) {
+        const int64_t k = k0 + (int64_t)t * T;
+        if (k >= n) break;
+        if (t > 0) {
+            load_poly<K>(x1, y1, k, P);
+            load_poly<K>(x2, y2, k, Q);
+        }
+        recentre<K>(P, Q);
+        if (DGAL_FWD_P2MODE == kP2Smem) {
+#pragma unroll
+            for (int q = 0; q < K; ++q) { sq[q * T + threadIdx.x] = Q.x[q]; sq[(K + q) * T + threadIdx.x] = Q.y[q]; }
+        }
+        const FwdOut<K, true> r = iou_fwd<K, true, DGAL_FWD_P2MODE>(P, Q, qt, WL ? &wlut[0] : nullptr);
+        __stcs(iou + k, r.iou);
+        nx[k] = (uint8_t)r.nx;
+        if (K == 4) {
+            __stcs(reinterpret_cast<unsigned long long *>(xflags) + k, (unsigned long long)r.seq.w[0]);
+        } else {
+            ulonglong2 v;
+            v.x = r.seq.w[0];
+            v.y = r.seq.w[Seq<K>::NW - 1];
+            __stcs(reinterpret_cast<ulonglong2 *>(xflags) + k, v);
+        }
     }
 }
 
@@ -203,7 +228,7 @@ cudaError_t launch_paired_fwd(int K, int64_t n, const float *x1, const float *y1
                               cudaStream_t st)
 {
     if (K == 4) {
-        const unsigned grid = (unsigned)((n + kFwd4Threads - 1) / kFwd4Threads);
+        const unsigned grid = (unsigned)((n + DGAL_FWD4_NT * kFwd4Threads - 1) / (DGAL_FWD4_NT * kFwd4Threads));
         paired_fwd_direct_kernel<4><<<grid, kFwd4Threads, 0, st>>>(n, x1, y1, x2, y2, iou, nx, xflags);
     } else {
         const unsigned grid = (unsigned)((n + kPairedThreads - 1) / kPairedThreads);
