@@ -46,6 +46,9 @@ constexpr int kFwd4Threads = DGAL_FWD4_THREADS;
 #ifndef DGAL_FWD4_NT
 #define DGAL_FWD4_NT 8        // K = 4: consecutive tiles of T pairs per CTA (amortises the table fill)
 #endif
+#ifndef DGAL_FWD4_PREFETCH
+#define DGAL_FWD4_PREFETCH 1  // K = 4: tile t+1 copied to shared memory (cp.async) while tile t computes
+#endif
 
 template <int K>
 __global__ void __launch_bounds__((K == 4) ? kFwd4Threads : kPairedThreads, (K == 4) ? DGAL_FWD4_MINB : 1)
@@ -58,9 +61,27 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
     constexpr int NT = (K == 4) ? DGAL_FWD4_NT : 1;
     __shared__ float sq[2 * K * T];   // per-thread p2 vertex table, [k][thread] (DGAL_FWD_P2MODE == kP2Smem)
     __shared__ WalkLut4 wlut[1];      // K = 4: the walk tables (DGAL_FWD4_WALKLUT; unused otherwise)
+    constexpr bool PF = (K == 4) && DGAL_FWD4_PREFETCH;
+    // PF: 2-stage per-thread ring [stage][plane][thread][K] (each thread copies and
+    // reads only its own 64 bytes: no CTA barrier, cp.async groups order it)
+    __shared__ __align__(16) float ring[PF ? 2 * 4 * T * K : 4];
     const int64_t k0 = (int64_t)blockIdx.x * (NT * T) + threadIdx.x;
+    const int tid = threadIdx.x;
+    auto prefetch = [&](int stage, int64_t k) {
+        float *r = ring + stage * (4 * T * K) + tid * K;
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q) {
+            cp_async16(r + 4 * q, x1 + k * K + 4 * q);
+            cp_async16(r + T * K + 4 * q, y1 + k * K + 4 * q);
+            cp_async16(r + 2 * T * K + 4 * q, x2 + k * K + 4 * q);
+            cp_async16(r + 3 * T * K + 4 * q, y2 + k * K + 4 * q);
+        }
+    };
     Poly<K> P, Q;
-    if (k0 < n) {   // the first tile's loads go out before the table fill
+    if (PF) {
+        if (k0 < n) prefetch(0, k0);
+        cp_async_commit();
+    } else if (k0 < n) {   // the first tile's loads go out before the table fill
         load_poly<K>(x1, y1, k0, P);
         load_poly<K>(x2, y2, k0, Q);
     }
@@ -73,7 +94,23 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
     for (int t = 0; t < NT; ++t) {
         const int64_t k = k0 + (int64_t)t * T;
         if (k >= n) break;
-        if (t > 0) {
+        if (PF) {
+            if (t + 1 < NT && k + T < n) prefetch((t + 1) & 1, k + T);
+            cp_async_commit();
+            cp_async_wait<1>();   // this thread's copies of tile t have landed
+            const float *r = ring + (t & 1) * (4 * T * K) + tid * K;
+#pragma unroll
+            for (int q = 0; q < K / 4; ++q) {
+                const float4 u = *reinterpret_cast<const float4 *>(r + 4 * q);
+                const float4 v = *reinterpret_cast<const float4 *>(r + T * K + 4 * q);
+                const float4 w = *reinterpret_cast<const float4 *>(r + 2 * T * K + 4 * q);
+                const float4 z = *reinterpret_cast<const float4 *>(r + 3 * T * K + 4 * q);
+                P.x[4 * q] = u.x; P.x[4 * q + 1] = u.y; P.x[4 * q + 2] = u.z; P.x[4 * q + 3] = u.w;
+                P.y[4 * q] = v.x; P.y[4 * q + 1] = v.y; P.y[4 * q + 2] = v.z; P.y[4 * q + 3] = v.w;
+                Q.x[4 * q] = w.x; Q.x[4 * q + 1] = w.y; Q.x[4 * q + 2] = w.z; Q.x[4 * q + 3] = w.w;
+                Q.y[4 * q] = z.x; Q.y[4 * q + 1] = z.y; Q.y[4 * q + 2] = z.z; Q.y[4 * q + 3] = z.w;
+            }
+        } else if (t > 0) {
             load_poly<K>(x1, y1, k, P);
             load_poly<K>(x2, y2, k, Q);
         }

@@ -28,6 +28,7 @@ def main(argv=None):
     ap.add_argument("--cubin", default="dgal_paired")
     ap.add_argument("--kernel", required=True)
     ap.add_argument("--top", type=int, default=45)
+    ap.add_argument("--block", default=".", help="regex on the ncu 'Kernel Name' row (several kernels in one csv)")
     a = ap.parse_args(argv)
     with tempfile.TemporaryDirectory() as d:
         subprocess.run(["cuobjdump", "-xelf", "all", a.so], cwd=d, capture_output=True, check=True)
@@ -49,9 +50,12 @@ def main(argv=None):
         if mi:
             seq.append((loc, mi.group(1)))
     rows = list(csv.reader(open(a.csv)))
+    starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+    blk = next(i for i in range(len(starts) - 1) if re.search(a.block, rows[starts[i]][1]))
+    rows = rows[starts[blk]:starts[blk + 1]]
     hdr = rows[1]
     ie, ss = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
-    data = rows[2:]
+    data = [r for r in rows[2:] if len(r) > ie]
     if len(data) != len(seq):
         print(f"warning: {len(data)} ncu rows vs {len(seq)} nvdisasm instructions", file=sys.stderr)
     per = collections.defaultdict(collections.Counter)
@@ -61,7 +65,7 @@ def main(argv=None):
         pipe = "alu" if op in ALU else "fma" if op in FMA else "other"
         per[loc][pipe] += n; per[loc]["samples"] += s; per[loc]["op:" + op] += n
         tot[pipe] += n; tot["samples"] += s
-    warps = max(int(r[ie]) for r in data)
+    warps = int(data[0][ie])   # the entry instruction runs once per warp
     print(f"warps {warps}; per warp: alu {tot['alu']/warps:.0f} fma {tot['fma']/warps:.0f} other {tot['other']/warps:.0f}"
           f"  (issue {(tot['alu']+tot['fma']+tot['other'])/warps:.0f}, alu-cycles {2*tot['alu']/warps:.0f})")
     for loc, c in sorted(per.items(), key=lambda kv: -kv[1]["samples"])[: a.top]:
