@@ -356,37 +356,27 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     // decision values, shifted by +tiny (below any non-degenerate value) so that
     // "inside" is "> 0" and no value is exactly 0:
     //   d[i][j] = f_j x (v_i - w_j) + tiny   p1 vertex i vs p2 line j, CLOSED test (d >= 0)
-    float d[K][K];
-#pragma unroll
-    for (int i = 0; i < K; ++i)
+    // Computed row by row inside the edge loop below (row i+1 when edge i is
+    // clipped), so only rows 0, i, i+1 are live: K = 8 needs 64 registers for all.
+    auto drow = [&](int i, float (&r)[K]) {
 #pragma unroll
         for (int j = 0; j < K; ++j) {
             const float Dx = __fsub_rn(P.x[i], Q.x[j]), Dy = __fsub_rn(P.y[i], Q.y[j]);
-            d[i][j] = __fadd_rn(cross_rn(fx[j], fy[j], Dx, Dy), kTiny);
+            r[j] = __fadd_rn(cross_rn(fx[j], fy[j], Dx, Dy), kTiny);
         }
-
-    // Separating p2 edge line: p1 strictly outside it -> empty.  Strict, so a
-    // zero-length edge (a repeated vertex: polygons with fewer than K vertices are
-    // padded that way), whose d are all exactly tiny, separates nothing; p1
-    // touching a line from outside reaches zero area through the closed boundary.
-    bool separated = false;
+    };
+    // p1 vertex i inside p2 (closed test, d never 0): bit i of in1, with its row
+    auto inside = [&](const float (&r)[K]) {
+        float mn = r[0];
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-        float m1 = d[0][j];
+        for (int j = 1; j < K; ++j) mn = fminf(mn, r[j]);
+        return (uint32_t)(mn > 0.f);
+    };
+    float d0[K], dc[K], m1[K];
+    drow(0, d0);
+    uint32_t in1 = inside(d0);
 #pragma unroll
-        for (int i = 1; i < K; ++i) m1 = fmaxf(m1, d[i][j]);
-        separated |= (m1 < kTiny);
-    }
-
-    // p1 vertices inside p2 (closed test, d never 0)
-    uint32_t in1 = 0;
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-        float mn = d[i][0];
-#pragma unroll
-        for (int j = 1; j < K; ++j) mn = fminf(mn, d[i][j]);
-        in1 |= (uint32_t)(mn > 0.f) << i;
-    }
+    for (int j = 0; j < K; ++j) { dc[j] = d0[j]; m1[j] = d0[j]; }
 
     // Cyrus-Beck intervals of p1's edges.  For the edge a -> b against one line
     // (a, b = the shifted decision values of its end points, never 0): the inside
@@ -435,10 +425,20 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         const int i1 = (i + 1) % K;
+        float dn[K];   // row i+1 (row 0 for the closing edge)
+        if (i1 != 0) {
+            drow(i1, dn);
+            in1 |= inside(dn) << i1;
+#pragma unroll
+            for (int j = 0; j < K; ++j) m1[j] = fmaxf(m1[j], dn[j]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < K; ++j) dn[j] = d0[j];
+        }
         float lo = 0.f, hi = hi0;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-            const float a = d[i][j], b = d[i1][j];
+            const float a = dc[j], b = dn[j];
             const float den = (a - b) + kTiny;
             const float r = rcp_approx(den);
             const float m = __saturatef(-den * kBig);  // 1: bounds below
@@ -498,7 +498,16 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
             p2e += has_out ? cross_rn(xox, xoy, wox, woy) : 0.f;
             p2e += has_in ? cross_rn(wix, wiy, xix, xiy) : 0.f;
         }
+#pragma unroll
+        for (int j = 0; j < K; ++j) dc[j] = dn[j];
     }
+    // Separating p2 edge line: p1 strictly outside it -> empty.  Strict, so a
+    // zero-length edge (a repeated vertex: polygons with fewer than K vertices are
+    // padded that way), whose d are all exactly tiny, separates nothing; p1
+    // touching a line from outside reaches zero area through the closed boundary.
+    bool separated = false;
+#pragma unroll
+    for (int j = 0; j < K; ++j) separated |= (m1[j] < kTiny);
     c.jin = jin; c.jout = jout; c.valid = valid; c.enter = enter; c.leave = leave;
     if (PSMEM) {
 #pragma unroll

@@ -46,22 +46,35 @@ constexpr int kFwd4Threads = DGAL_FWD4_THREADS;
 #ifndef DGAL_FWD4_NT
 #define DGAL_FWD4_NT 8        // K = 4: consecutive tiles of T pairs per CTA (amortises the table fill)
 #endif
+#ifndef DGAL_FWD8_THREADS
+#define DGAL_FWD8_THREADS 128   // K = 8: 165 registers, 3 CTAs/SM (A/B: 256 x 1 CTA 0.50 ms, 128 x 3 0.38 ms)
+#endif
+#ifndef DGAL_FWD8_MINB
+#define DGAL_FWD8_MINB 3
+#endif
+#ifndef DGAL_FWD8_NT
+#define DGAL_FWD8_NT 1
+#endif
+#ifndef DGAL_FWD8_PREFETCH
+#define DGAL_FWD8_PREFETCH 0
+#endif
+constexpr int kFwd8Threads = DGAL_FWD8_THREADS;
 #ifndef DGAL_FWD4_PREFETCH
 #define DGAL_FWD4_PREFETCH 1  // K = 4: tile t+1 copied to shared memory (cp.async) while tile t computes
 #endif
 
 template <int K>
-__global__ void __launch_bounds__((K == 4) ? kFwd4Threads : kPairedThreads, (K == 4) ? DGAL_FWD4_MINB : 1)
+__global__ void __launch_bounds__((K == 4) ? kFwd4Threads : kFwd8Threads, (K == 4) ? DGAL_FWD4_MINB : DGAL_FWD8_MINB)
 paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
                          const float *__restrict__ x2, const float *__restrict__ y2,
                          float *__restrict__ iou, uint8_t *__restrict__ nx, uint8_t *__restrict__ xflags)
 {
-    constexpr int T = (K == 4) ? kFwd4Threads : kPairedThreads;
+    constexpr int T = (K == 4) ? kFwd4Threads : kFwd8Threads;
     constexpr bool WL = (K == 4) && DGAL_FWD4_WALKLUT;
-    constexpr int NT = (K == 4) ? DGAL_FWD4_NT : 1;
+    constexpr int NT = (K == 4) ? DGAL_FWD4_NT : DGAL_FWD8_NT;
     __shared__ float sq[2 * K * T];   // per-thread p2 vertex table, [k][thread] (DGAL_FWD_P2MODE == kP2Smem)
     __shared__ WalkLut4 wlut[1];      // K = 4: the walk tables (DGAL_FWD4_WALKLUT; unused otherwise)
-    constexpr bool PF = (K == 4) && DGAL_FWD4_PREFETCH;
+    constexpr bool PF = (K == 4) ? DGAL_FWD4_PREFETCH : DGAL_FWD8_PREFETCH;
     // PF: 2-stage per-thread ring [stage][plane][thread][K] (each thread copies and
     // reads only its own 64 bytes: no CTA barrier, cp.async groups order it)
     __shared__ __align__(16) float ring[PF ? 2 * 4 * T * K : 4];
@@ -144,10 +157,28 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
 // Warps are independent within a tile (own pairs, own crossing queue), so a
 // stage is released per warp on an "empty" mbarrier instead of a CTA barrier:
 // only the producer waits for all warps before refilling it; the others run on.
-constexpr int kTile = 256;
+#ifndef DGAL_BWD4_TILE
+#define DGAL_BWD4_TILE 256
+#endif
+#ifndef DGAL_BWD8_TILE
+#define DGAL_BWD8_TILE 128   // K = 8: smaller tiles so 2+ CTAs fit the shared memory
+#endif
+#ifndef DGAL_BWD4_MINB
+#define DGAL_BWD4_MINB 3
+#endif
+#ifndef DGAL_BWD8_MINB
+#define DGAL_BWD8_MINB 3   // A/B (K = 8): 256 x 1 CTA 0.263 ms, 128 x 2 0.262, 128 x 3 0.235
+#endif
+template <int K>
+struct BwdCfg {
+    static constexpr int tile = (K == 4) ? DGAL_BWD4_TILE : DGAL_BWD8_TILE;
+    static constexpr int threads = tile + 32;   // + the producer warp
+    static constexpr int minb = (K == 4) ? DGAL_BWD4_MINB : DGAL_BWD8_MINB;
+};
 
 template <int K>
 struct BwdSmem {
+    static constexpr int kTile = BwdCfg<K>::tile;
     struct Stage {
         float x1[kTile * K], y1[kTile * K], x2[kTile * K], y2[kTile * K];
         float g[kTile];
@@ -165,13 +196,8 @@ struct BwdSmem {
 // Warp-specialised: warps 0..7 consume (one pair per thread), warp 8 produces —
 // its lane 0 refills a stage with the next tile as soon as all consumer warps have
 // released it, so no consumer ever waits on the producer's own bookkeeping.
-constexpr int kBwdThreads = kTile + 32;
-
-#ifndef DGAL_BWD4_MINB
-#define DGAL_BWD4_MINB 3
-#endif
 template <int K>
-__global__ void __launch_bounds__(kBwdThreads, (K == 4) ? DGAL_BWD4_MINB : 1)
+__global__ void __launch_bounds__(BwdCfg<K>::threads, BwdCfg<K>::minb)
 paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
                   const float *__restrict__ x2, const float *__restrict__ y2,
                   const float *__restrict__ grad, const uint8_t *__restrict__ nx,
@@ -181,6 +207,7 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     BwdSmem<K> &S = *reinterpret_cast<BwdSmem<K> *>(smem_raw);
+    constexpr int kTile = BwdCfg<K>::tile, kBwdThreads = BwdCfg<K>::threads;
     const int tid = threadIdx.x;
     const int64_t ntiles = (n + kTile - 1) / kTile;
     const int64_t nfull = use_bulk ? n / kTile : 0;  // tiles fed by bulk copies
@@ -268,8 +295,8 @@ cudaError_t launch_paired_fwd(int K, int64_t n, const float *x1, const float *y1
         const unsigned grid = (unsigned)((n + DGAL_FWD4_NT * kFwd4Threads - 1) / (DGAL_FWD4_NT * kFwd4Threads));
         paired_fwd_direct_kernel<4><<<grid, kFwd4Threads, 0, st>>>(n, x1, y1, x2, y2, iou, nx, xflags);
     } else {
-        const unsigned grid = (unsigned)((n + kPairedThreads - 1) / kPairedThreads);
-        paired_fwd_direct_kernel<8><<<grid, kPairedThreads, 0, st>>>(n, x1, y1, x2, y2, iou, nx, xflags);
+        const unsigned grid = (unsigned)((n + DGAL_FWD8_NT * kFwd8Threads - 1) / (DGAL_FWD8_NT * kFwd8Threads));
+        paired_fwd_direct_kernel<8><<<grid, kFwd8Threads, 0, st>>>(n, x1, y1, x2, y2, iou, nx, xflags);
     }
     return cudaGetLastError();
 }
@@ -290,15 +317,16 @@ cudaError_t launch_bwd_k(int64_t n, const float *x1, const float *y1, const floa
         if (e != cudaSuccess) return e;
         int sms = 0, per = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, paired_bwd_kernel<K>, kBwdThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, paired_bwd_kernel<K>, BwdCfg<K>::threads, smem);
         limit = sms * (per > 0 ? per : 1);
         dev_cached = dev;
     }
+    constexpr int kTile = BwdCfg<K>::tile;
     const int64_t ntiles = (n + kTile - 1) / kTile;
     const unsigned grid = (unsigned)(ntiles < limit ? ntiles : limit);
     auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
     const int use_bulk = al16(grad) && al16(nx) && al16(xflags);   // planes are 16 B aligned (ABI)
-    paired_bwd_kernel<K><<<grid, kBwdThreads, smem, st>>>(n, x1, y1, x2, y2, grad, nx, xflags, gx1, gy1, gx2,
+    paired_bwd_kernel<K><<<grid, BwdCfg<K>::threads, smem, st>>>(n, x1, y1, x2, y2, grad, nx, xflags, gx1, gy1, gx2,
                                                            gy2, use_bulk);
     return cudaGetLastError();
 }
@@ -316,12 +344,26 @@ cudaError_t launch_paired_bwd(int K, int64_t n, const float *x1, const float *y1
 // ---------------------------------------------------------------------------
 // Fused loss forward + backward, one pair per thread
 // ---------------------------------------------------------------------------
+// CTA shape and CTAs per SM the fused kernels are register-budgeted for (A/B on
+// B200: K = 4 256 x 3 0.519 ms, 128 x 6 0.505 ms; K = 8 256 x 1 0.523 ms, 128 x 3
+// 0.361 ms, 128 x 2 0.443 ms)
 #ifndef DGAL_FUSED4_MINB
-#define DGAL_FUSED4_MINB 3   // CTAs per SM the K=4 fused kernel is register-budgeted for (A/B)
+#define DGAL_FUSED4_MINB 6
 #endif
+#ifndef DGAL_FUSED4_THREADS
+#define DGAL_FUSED4_THREADS 128
+#endif
+#ifndef DGAL_FUSED8_MINB
+#define DGAL_FUSED8_MINB 3
+#endif
+#ifndef DGAL_FUSED8_THREADS
+#define DGAL_FUSED8_THREADS 128
+#endif
+constexpr int kFused4Threads = DGAL_FUSED4_THREADS, kFused8Threads = DGAL_FUSED8_THREADS;
 
 template <int K>
-__global__ void __launch_bounds__(kPairedThreads, (K == 4) ? DGAL_FUSED4_MINB : 1)
+__global__ void __launch_bounds__((K == 4) ? kFused4Threads : kFused8Threads,
+                                  (K == 4) ? DGAL_FUSED4_MINB : DGAL_FUSED8_MINB)
 paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
                     const float *__restrict__ x2, const float *__restrict__ y2,
                     const float *__restrict__ grad, float scale, float *__restrict__ iou,
@@ -331,7 +373,7 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
 #ifndef DGAL_FUSED_P2MODE
 #define DGAL_FUSED_P2MODE kP2PiecesSmem   // A/B: kP2Pieces 0.571 ms, kP2PiecesSmem 0.526 ms (cfg3)
 #endif
-    constexpr int T = kPairedThreads;
+    constexpr int T = (K == 4) ? kFused4Threads : kFused8Threads;
     __shared__ float pt[(DGAL_FUSED_P2MODE == kP2PiecesSmem) ? 4 * K * T : 1];   // piece table, [slot][thread]
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
@@ -353,13 +395,12 @@ cudaError_t launch_paired_fused(int K, int64_t n, const float *x1, const float *
                                 const float *y2, const float *grad, float scale, float *iou, float *gx1,
                                 float *gy1, float *gx2, float *gy2, cudaStream_t st)
 {
-    const unsigned grid = (unsigned)((n + kPairedThreads - 1) / kPairedThreads);
     if (K == 4)
-        paired_fused_kernel<4><<<grid, kPairedThreads, 0, st>>>(n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1,
-                                                                gx2, gy2);
+        paired_fused_kernel<4><<<(unsigned)((n + kFused4Threads - 1) / kFused4Threads), kFused4Threads, 0, st>>>(
+            n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2);
     else
-        paired_fused_kernel<8><<<grid, kPairedThreads, 0, st>>>(n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1,
-                                                                gx2, gy2);
+        paired_fused_kernel<8><<<(unsigned)((n + kFused8Threads - 1) / kFused8Threads), kFused8Threads, 0, st>>>(
+            n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2);
     return cudaGetLastError();
 }
 
