@@ -22,7 +22,23 @@ namespace dgal {
 
 namespace {
 
-constexpr int kBoxTile = 256;  // backward tile = CTA size
+// backward / fused CTA shapes (A/B on B200, 2^24 KITTI pairs: backward 256 x 3 CTAs
+// 0.62 / 0.68 ms (2D / 3D) -> 128 x 7 / 128 x 6 0.59 / 0.65; fused 256 x 2 0.64 /
+// 0.78 -> 128 x 4 0.59 / 0.74; the largest CTA counts without spills)
+#ifndef DGAL_BOX_BWD_TILE
+#define DGAL_BOX_BWD_TILE 128
+#endif
+#ifndef DGAL_BOX_BWD2_MINB
+#define DGAL_BOX_BWD2_MINB 7
+#endif
+#ifndef DGAL_BOX_BWD3_MINB
+#define DGAL_BOX_BWD3_MINB 6
+#endif
+#ifndef DGAL_BOX_FUSED_T
+#define DGAL_BOX_FUSED_T 128
+#endif
+constexpr int kBoxTile = DGAL_BOX_BWD_TILE;  // backward tile = CTA size
+constexpr int kBoxFusedT = DGAL_BOX_FUSED_T;
 // CTAs per SM the box forward / fused kernels are register-budgeted for (the
 // largest without local-memory spills, tools/sass_stats.py)
 #ifndef DGAL_BOX_FWD2_MINB
@@ -40,8 +56,11 @@ constexpr int kBoxTile = 256;  // backward tile = CTA size
 #define DGAL_BOX_FWD_NT 8
 #endif
 constexpr int kBoxFwdT = DGAL_BOX_FWD_T, kBoxFwdNT = DGAL_BOX_FWD_NT;
-#ifndef DGAL_BOX_FUSED_MINB
-#define DGAL_BOX_FUSED_MINB 2
+#ifndef DGAL_BOX_FUSED2_MINB
+#define DGAL_BOX_FUSED2_MINB 4
+#endif
+#ifndef DGAL_BOX_FUSED3_MINB
+#define DGAL_BOX_FUSED3_MINB 4
 #endif
 
 template <int DIMS>
@@ -286,7 +305,7 @@ struct BoxBwdSmem {
 };
 
 template <int DIMS>
-__global__ void __launch_bounds__(kBoxTile)
+__global__ void __launch_bounds__(kBoxTile, DIMS == 2 ? DGAL_BOX_BWD2_MINB : DGAL_BOX_BWD3_MINB)
 box_bwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict__ b2, int64_t sk, int64_t sp,
                const float *__restrict__ grad, const uint8_t *__restrict__ nx, const uint8_t *__restrict__ xflags,
                float *__restrict__ gb1, float *__restrict__ gb2)
@@ -342,12 +361,12 @@ box_bwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
 // fused loss forward + backward (f2 on boxes): no nx / xflags round trip
 // ---------------------------------------------------------------------------
 template <int DIMS>
-__global__ void __launch_bounds__(kPairedThreads, DGAL_BOX_FUSED_MINB)
+__global__ void __launch_bounds__(kBoxFusedT, DIMS == 2 ? DGAL_BOX_FUSED2_MINB : DGAL_BOX_FUSED3_MINB)
 box_fused_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict__ b2, int64_t sk, int64_t sp,
                  const float *__restrict__ grad, float scale, float *__restrict__ iou, float *__restrict__ gb1,
                  float *__restrict__ gb2)
 {
-    constexpr int T = kPairedThreads;
+    constexpr int T = kBoxFusedT;
     __shared__ float pt[16 * T];   // per-thread piece table (kP2PiecesSmem), [slot][thread]
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
@@ -409,11 +428,11 @@ cudaError_t launch_box_fused(int dims, int layout, int64_t n, const float *b1, c
 {
     int64_t sk, sp;
     box_strides(dims, layout, n, sk, sp);
-    const unsigned grid = (unsigned)((n + kPairedThreads - 1) / kPairedThreads);
+    const unsigned grid = (unsigned)((n + kBoxFusedT - 1) / kBoxFusedT);
     if (dims == 3)
-        box_fused_kernel<3><<<grid, kPairedThreads, 0, st>>>(n, b1, b2, sk, sp, grad, scale, iou, gb1, gb2);
+        box_fused_kernel<3><<<grid, kBoxFusedT, 0, st>>>(n, b1, b2, sk, sp, grad, scale, iou, gb1, gb2);
     else
-        box_fused_kernel<2><<<grid, kPairedThreads, 0, st>>>(n, b1, b2, sk, sp, grad, scale, iou, gb1, gb2);
+        box_fused_kernel<2><<<grid, kBoxFusedT, 0, st>>>(n, b1, b2, sk, sp, grad, scale, iou, gb1, gb2);
     return cudaGetLastError();
 }
 

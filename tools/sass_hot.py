@@ -28,6 +28,8 @@ def main(argv=None):
     ap.add_argument("--cubin", default="dgal_paired")
     ap.add_argument("--kernel", required=True)
     ap.add_argument("--top", type=int, default=45)
+    ap.add_argument("--units", type=float, default=0,
+                    help="normalise per unit (e.g. warps of 32 pairs) instead of per launched warp")
     ap.add_argument("--block", default=".", help="regex on the ncu 'Kernel Name' row (several kernels in one csv)")
     a = ap.parse_args(argv)
     with tempfile.TemporaryDirectory() as d:
@@ -65,7 +67,7 @@ def main(argv=None):
         pipe = "alu" if op in ALU else "fma" if op in FMA else "other"
         per[loc][pipe] += n; per[loc]["samples"] += s; per[loc]["op:" + op] += n
         tot[pipe] += n; tot["samples"] += s
-    warps = int(data[0][ie])   # the entry instruction runs once per warp
+    warps = a.units or int(data[0][ie])   # the entry instruction runs once per launched warp
     print(f"warps {warps}; per warp: alu {tot['alu']/warps:.0f} fma {tot['fma']/warps:.0f} other {tot['other']/warps:.0f}"
           f"  (issue {(tot['alu']+tot['fma']+tot['other'])/warps:.0f}, alu-cycles {2*tot['alu']/warps:.0f})")
     for loc, c in sorted(per.items(), key=lambda kv: -kv[1]["samples"])[: a.top]:
