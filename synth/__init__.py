@@ -18,5 +18,6 @@ from .generators import (  # noqa: F401
     gen_cfg4_pairs,
     gen_cfg5_scene,
     gen_config,
+    gen_quad_pairs,
     seed_for,
 )

@@ -349,6 +349,56 @@ def gen_cfg4_pairs(n: int = 1 << 22, seed: int | None = None) -> PairBatch:
 
 
 # ----------------------------------------------------------------------------
+# general convex quadrilaterals (test workload: every K=4 walk-table state)
+# ----------------------------------------------------------------------------
+def _ellipse_quad(rng, m, c, a, b):
+    phi = rng.uniform(-math.pi, math.pi, size=m)
+    phi0 = rng.uniform(0, 2 * math.pi, size=m)
+    k = np.arange(4)[None, :]
+    alpha = (k + rng.uniform(-0.35, 0.35, size=(m, 4))) * (math.pi / 2) + phi0[:, None]
+    ex, ey = a[:, None] * np.cos(alpha), b[:, None] * np.sin(alpha)
+    cp, sp = np.cos(phi)[:, None], np.sin(phi)[:, None]
+    return c[:, :1] + cp * ex - sp * ey, c[:, 1:] + sp * ex + cp * ey
+
+
+def _quad_chunk(rng, m):
+    """Non-rectangular convex quads on ellipses (points in angular order on an ellipse
+    are in convex position, CCW).  Mix: 60 % partner shifted by N(0, 1.5^2) with an
+    independent shape; 20 % partner inside-ish (scaled 0.2-0.6 about a point near the
+    centre: containment both ways, runs of up to 3 FromP2 bytes); 20 % same ellipse,
+    partner rotated ~pi/4 (up to 8 crossings)."""
+    c = rng.uniform(-10, 10, size=(m, 2))
+    a = rng.uniform(1, 3, size=m)
+    b = a * rng.uniform(0.3, 1.0, size=m)
+    x1, y1 = _ellipse_quad(rng, m, c, a, b)
+    kind = rng.uniform(size=m)
+    c2 = c + rng.normal(0, 1.5, size=(m, 2))
+    a2 = rng.uniform(1, 3, size=m)
+    b2 = a2 * rng.uniform(0.3, 1.0, size=m)
+    small = (kind >= 0.6) & (kind < 0.8)
+    sc = np.where(small, rng.uniform(0.2, 0.6, size=m), 1.0)
+    c2 = np.where(small[:, None], c + rng.normal(0, 0.3, size=(m, 2)), c2)
+    a2, b2 = np.where(small, a * sc, a2), np.where(small, b * sc, b2)
+    rot = kind >= 0.8
+    c2 = np.where(rot[:, None], c, c2)
+    a2, b2 = np.where(rot, a * rng.uniform(0.9, 1.1, size=m), a2), np.where(rot, b, b2)
+    x2, y2 = _ellipse_quad(rng, m, c2, a2, b2)
+    swap = rng.uniform(size=m) < 0.5                        # containment both ways
+    x1, x2 = np.where(swap[:, None], x2, x1), np.where(swap[:, None], x1, x2)
+    y1, y2 = np.where(swap[:, None], y2, y1), np.where(swap[:, None], y1, y2)
+    g = rng.uniform(-1, 1, size=m)
+    return x1, y1, x2, y2, g
+
+
+def gen_quad_pairs(n: int = 4096, seed: int | None = None) -> PairBatch:
+    """General convex quadrilateral pairs Poly2<float,4> (tests only; seed 1134000 + 41)."""
+    seed = BASE_SEED + 41 if seed is None else seed
+    x1, y1, x2, y2, g = _chunked(n, seed, _quad_chunk)
+    f = lambda a: np.ascontiguousarray(a.astype(np.float32).reshape(-1))  # noqa: E731
+    return PairBatch(Polys(f(x1), f(y1), 4), Polys(f(x2), f(y2), 4), g.astype(np.float32))
+
+
+# ----------------------------------------------------------------------------
 # cfg5: nuScenes-like clustered proposals
 # ----------------------------------------------------------------------------
 # (share, length, width)

@@ -24,6 +24,24 @@ def test_paired_margin_inputs_full_compare(cfg, n):
     check_paired_against_oracle(margin_batch(cfg, n))
 
 
+def test_general_quads_all_walk_states():
+    """Non-rectangular convex quads (synth.gen_quad_pairs): containment both ways,
+    runs of up to 3 FromP2 bytes after an exit, up to 8 crossings — the states of
+    the K=4 forward's walk tables beyond what box pairs reach.
+    Full compare on margin inputs, and the workload must actually reach them."""
+    from helpers import margin_filter
+    b = margin_filter(synth.gen_quad_pairs(12_000), 8192)
+    ref = oracle.iou_paired_fwd(b.p1, b.p2)
+    nx, xf = ref["nx"], ref["xflags"].reshape(b.n, 8)
+    assert set(np.unique(nx)) >= {0, 3, 4, 5, 6, 7, 8}
+    tags = xf >> 6
+    runs3 = ((tags[:, :-2] == 2) & (tags[:, 1:-1] == 2) & (tags[:, 2:] == 2)).any(1)
+    assert runs3.sum() > 10                                    # 3 FromP2 in a row
+    assert ((tags[:, :4] == 2).all(1) & (nx == 4)).sum() > 10  # p2 inside p1
+    assert ((tags[:, :4] == 1).all(1) & (nx == 4)).sum() > 10  # p1 inside p2
+    check_paired_against_oracle(b)
+
+
 @pytest.mark.parametrize("n", [1, 2, 31, 255, 257, 1000, 4097])
 def test_ragged_sizes(n):
     check_paired_against_oracle(margin_batch(1, n))

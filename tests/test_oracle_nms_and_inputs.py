@@ -88,6 +88,13 @@ def test_generators_valid_and_deterministic(cfg):
         assert a.p1.x.dtype == np.float32 and a.n == n
 
 
+def test_quad_generator_valid():
+    """General convex quads (tests' walk-state workload) are convex, CCW, float32."""
+    a, b = synth.gen_quad_pairs(20000), synth.gen_quad_pairs(20000)
+    assert np.array_equal(a.p1.x, b.p1.x) and _convex_ccw(a.p1) and _convex_ccw(a.p2)
+    assert a.p1.K == 4 and a.p1.x.dtype == np.float32
+
+
 def test_generators_prefix_stable():
     a = synth.gen_cfg3_pairs(70000)
     b = synth.gen_cfg3_pairs(1000)
