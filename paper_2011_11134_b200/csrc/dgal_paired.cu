@@ -287,6 +287,123 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
     }
 }
 
+// ---------------------------------------------------------------------------
+// Backward, per-thread prefetch: no producer warp, no stage barriers.  Every
+// thread copies its own pair of the NEXT tile (vertices, g, flag bytes) into a
+// 2-stage ring with cp.async while the warp works on the current tile; a warp
+// only reads its own 32 pairs (crossing queue), so a __syncwarp after the
+// copies complete is the only ordering needed.  CTAs own NT consecutive tiles.
+// (The producer-warp kernel above spends ~20 % of its issue slots polling its
+// full / empty barriers: ncu source counters.)
+#ifndef DGAL_BWD4_PT
+#define DGAL_BWD4_PT 1        // K = 4 backward: per-thread prefetch kernel (0: producer-warp kernel)
+#endif
+#ifndef DGAL_BWDPT_THREADS
+#define DGAL_BWDPT_THREADS 128
+#endif
+#ifndef DGAL_BWDPT_MINB
+#define DGAL_BWDPT_MINB 7     // K = 4: 70 registers, 30 KB shared memory per CTA
+#endif
+#ifndef DGAL_BWD8_PT
+#define DGAL_BWD8_PT 0
+#endif
+#ifndef DGAL_BWDPT8_MINB
+#define DGAL_BWDPT8_MINB 3
+#endif
+#ifndef DGAL_BWDPT_NT
+#define DGAL_BWDPT_NT 8
+#endif
+constexpr int kBwdPtThreads = DGAL_BWDPT_THREADS;
+
+template <int K>
+struct BwdPtSmem {
+    static constexpr int T = kBwdPtThreads;
+    struct Stage {
+        float x1[T * K], y1[T * K], x2[T * K], y2[T * K];
+        float g[T];
+        uint64_t xf[T * (K / 4)];
+    };
+    Stage st[2];
+    float scr[4 * K * T];
+    uint16_t queue[T / 32][32 * 2 * K];
+    FlagLut lut;
+};
+
+__device__ __forceinline__ void cp_async4(void *dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+template <int K>
+__global__ void __launch_bounds__(kBwdPtThreads, (K == 4) ? DGAL_BWDPT_MINB : DGAL_BWDPT8_MINB)
+paired_bwd_pt_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
+                     const float *__restrict__ x2, const float *__restrict__ y2,
+                     const float *__restrict__ grad, const uint8_t *__restrict__ nx,
+                     const uint8_t *__restrict__ xflags,
+                     float *__restrict__ gx1, float *__restrict__ gy1,
+                     float *__restrict__ gx2, float *__restrict__ gy2)
+{
+    constexpr int T = kBwdPtThreads, NT = DGAL_BWDPT_NT;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    BwdPtSmem<K> &S = *reinterpret_cast<BwdPtSmem<K> *>(smem_raw);
+    const int tid = threadIdx.x;
+    const int64_t base = (int64_t)blockIdx.x * (NT * T);
+    auto prefetch = [&](int stage, int64_t k) {
+        typename BwdPtSmem<K>::Stage &D = S.st[stage];
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q) {
+            cp_async16(D.x1 + tid * K + 4 * q, x1 + k * K + 4 * q);
+            cp_async16(D.y1 + tid * K + 4 * q, y1 + k * K + 4 * q);
+            cp_async16(D.x2 + tid * K + 4 * q, x2 + k * K + 4 * q);
+            cp_async16(D.y2 + tid * K + 4 * q, y2 + k * K + 4 * q);
+        }
+        cp_async4(D.g + tid, grad + k);
+        if (K == 4) cp_async8(D.xf + tid, xflags + k * 8);
+        else cp_async16(D.xf + 2 * tid, xflags + k * 16);
+    };
+    int m_next = 0;
+    if (base + tid < n) {
+        prefetch(0, base + tid);
+        m_next = nx[base + tid];
+    }
+    cp_async_commit();
+    fill_flag_lut(S.lut, tid, T);
+    __syncthreads();
+#pragma unroll 1
+    for (int t = 0; t < NT; ++t) {
+        const int64_t kb = base + (int64_t)t * T;
+        if (kb >= n) break;                      // CTA-uniform
+        const int64_t k = kb + tid;
+        const bool live = k < n;
+        const int m = live ? m_next : 0;
+        if (t + 1 < NT && k + T < n) {
+            prefetch((t + 1) & 1, k + T);
+            m_next = nx[k + T];
+        }
+        cp_async_commit();
+        cp_async_wait<1>();                      // this thread's copies of tile t landed
+        __syncwarp();                            // ... and the other lanes' (crossing queue)
+        typename BwdPtSmem<K>::Stage &D = S.st[t & 1];
+        Seq<K> sq;
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q) sq.w[q] = live ? D.xf[tid * (K / 4) + q] : 0ull;
+        Poly<K> G1, G2;
+        bwd_tile_pair<K, T>(D.x1, D.y1, D.x2, D.y2, sq, m, live ? D.g[tid] : 0.f, live, S.scr,
+                            S.queue[tid >> 5], S.lut, G1, G2);
+        if (live) {
+            store_plane<K>(gx1, k, G1.x);
+            store_plane<K>(gy1, k, G1.y);
+            store_plane<K>(gx2, k, G2.x);
+            store_plane<K>(gy2, k, G2.y);
+        }
+        __syncwarp();                            // stage t & 1 is refilled next iteration
+    }
+}
+
 cudaError_t launch_paired_fwd(int K, int64_t n, const float *x1, const float *y1, const float *x2,
                               const float *y2, float *iou, uint8_t *nx, uint8_t *xflags,
                               cudaStream_t st)
@@ -330,6 +447,26 @@ cudaError_t launch_bwd_k(int64_t n, const float *x1, const float *y1, const floa
                                                            gy2, use_bulk);
     return cudaGetLastError();
 }
+template <int K>
+cudaError_t launch_bwd_pt(int64_t n, const float *x1, const float *y1, const float *x2, const float *y2,
+                          const float *grad, const uint8_t *nx, const uint8_t *xflags, float *gx1, float *gy1,
+                          float *gx2, float *gy2, cudaStream_t st)
+{
+    static int dev_cached = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t smem = sizeof(BwdPtSmem<K>);
+    if (dev != dev_cached) {
+        cudaError_t e = cudaFuncSetAttribute(paired_bwd_pt_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        dev_cached = dev;
+    }
+    constexpr int64_t per = (int64_t)DGAL_BWDPT_NT * kBwdPtThreads;
+    paired_bwd_pt_kernel<K><<<(unsigned)((n + per - 1) / per), kBwdPtThreads, smem, st>>>(
+        n, x1, y1, x2, y2, grad, nx, xflags, gx1, gy1, gx2, gy2);
+    return cudaGetLastError();
+}
 }  // namespace
 
 cudaError_t launch_paired_bwd(int K, int64_t n, const float *x1, const float *y1, const float *x2,
@@ -337,6 +474,11 @@ cudaError_t launch_paired_bwd(int K, int64_t n, const float *x1, const float *y1
                               const uint8_t *xflags, float *gx1, float *gy1, float *gx2, float *gy2,
                               cudaStream_t st)
 {
+    auto al = [](const void *p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; };
+    if (K == 4 && DGAL_BWD4_PT && al(grad, 4) && al(xflags, 8))
+        return launch_bwd_pt<4>(n, x1, y1, x2, y2, grad, nx, xflags, gx1, gy1, gx2, gy2, st);
+    if (K == 8 && DGAL_BWD8_PT && al(grad, 4) && al(xflags, 16))
+        return launch_bwd_pt<8>(n, x1, y1, x2, y2, grad, nx, xflags, gx1, gy1, gx2, gy2, st);
     if (K == 4) return launch_bwd_k<4>(n, x1, y1, x2, y2, grad, nx, xflags, gx1, gy1, gx2, gy2, st);
     return launch_bwd_k<8>(n, x1, y1, x2, y2, grad, nx, xflags, gx1, gy1, gx2, gy2, st);
 }
