@@ -259,7 +259,7 @@ inline void launch_zero(void *p, size_t bytes, cudaStream_t st)
 // them with coalesced 16 B loads, ballot the circle-overlapping columns into the
 // warp's queue, and the queue is evaluated 32 entries at a time.
 template <int K>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, K == 4 ? 2 : 1)   // K = 8: the whole register file (no spill)
 pw_candidates(int64_t n_rows, const float *__restrict__ rx, const float *__restrict__ ry, int64_t m,
               const float *__restrict__ cxg, const float *__restrict__ cyg, int64_t row_offset,
               float *__restrict__ iou, float thr, uint64_t *__restrict__ mask, int64_t mask_words,
