@@ -925,13 +925,17 @@ __device__ __forceinline__ void bwd_epilogue(const float *sPx, const float *sPy,
     // boundary pieces -> A_i and the edge weights
     //   alpha = ∫ (1-t) dt = l (1 - h),  beta = ∫ t dt = l h,  l = t1 - t0, h = (t0 + t1)/2
     // p1 edge i is on the boundary iff v_i or v_i+1 is a vertex of p1 ∩ p2 or it is crossed
+    // (edge i on the boundary, as masks: vertex i, vertex i+1 (rotated) or a crossing)
+    constexpr uint32_t KMASK = (1u << K) - 1u;
+    const uint32_t v1 = V & KMASK, v2 = (V >> 8) & KMASK;
+    const uint32_t on1m = v1 | ((v1 >> 1) | (v1 << (K - 1))) | (V >> 16);
+    const uint32_t on2m = v2 | ((v2 >> 1) | (v2 << (K - 1))) | (V >> 24);
     float al1[K], be1[K], al2[K], be2[K];
     float Aix2 = 0.f;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-        const int i1 = (i + 1) % K;
-        const bool on1 = (((V >> i) | (V >> i1) | (V >> (16 + i))) & 1u) != 0;
-        const bool on2 = (((V >> (8 + i)) | (V >> (8 + i1)) | (V >> (24 + i))) & 1u) != 0;
+        const bool on1 = (on1m >> i) & 1u;
+        const bool on2 = (on2m >> i) & 1u;
         const float a0 = scr[i * TILE], a1 = scr[(K + i) * TILE];
         const float b0 = scr[(2 * K + i) * TILE], b1 = scr[(3 * K + i) * TILE];
         const float l1 = on1 ? fmaxf(a1 - a0, 0.f) : 0.f;
