@@ -447,9 +447,12 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
             hi = fminf(hi, fmaf(m, kBig, ve));      // ve (bits kept) or huge
         }
         const bool in_s = (in1 >> i) & 1u, in_e = (in1 >> i1) & 1u;
+        // per-event modes: clamped to the edge (an invalid piece keeps a0 >= a1 without
+        // the index bits either way, a valid one lies in [0, 1]; saturate keeps the
+        // bits) — fewer selects; the piece modes keep the unclamped form (registers)
         const float hic = fminf(hi, 1.f);
-        const float a0 = in_s ? 0.f : (in_e ? fminf(lo, 1.f) : lo);
-        const float a1 = in_e ? 1.f : (in_s ? fmaxf(hic, 0.f) : hic);
+        const float a0 = in_s ? 0.f : ((in_e || !PIECES) ? fminf(lo, 1.f) : lo);
+        const float a1 = in_e ? 1.f : (!PIECES ? __saturatef(hi) : (in_s ? fmaxf(hic, 0.f) : hic));
         // strict, without the index bits (they perturb the last 3 ulps)
         const bool ok = in_s || in_e ||
                         (__int_as_float(__float_as_int(a0) & ~7) < __int_as_float(__float_as_int(a1) & ~7));
