@@ -498,8 +498,9 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
                 pick_xy<K>(Q.x, Q.y, ljout, wox, woy);
                 pick_xy<K>(Q.x, Q.y, jn, wix, wiy);
             }
-            p2e += has_out ? cross_rn(xox, xoy, wox, woy) : 0.f;
-            p2e += has_in ? cross_rn(wix, wiy, xix, xiy) : 0.f;
+            // (area terms, not decisions: contracted, one rounding fewer)
+            p2e += has_out ? fmaf(xox, woy, -(xoy * wox)) : 0.f;
+            p2e += has_in ? fmaf(wix, xiy, -(wiy * xix)) : 0.f;
         }
 #pragma unroll
         for (int j = 0; j < K; ++j) dc[j] = dn[j];
