@@ -73,6 +73,54 @@ __device__ __forceinline__ float rcp_approx(float x)
     return r;
 }
 
+// Paired FP32 (sm_100: FADD2 / FMUL2 / FFMA2 — two IEEE RN operations in one
+// instruction on a 64-bit register pair; no contraction across the asm).  The
+// kernels are issue-bound, so pairing the decision values and the Cyrus-Beck
+// candidates of two p2 lines halves their FMA-pipe instruction count with
+// bitwise the same results.
+#ifndef DGAL_F32X2
+#define DGAL_F32X2 3   // bit 0: decision rows, bit 1: Cyrus-Beck candidates
+#endif
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi)
+{
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float &lo, float &hi)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b)
+{
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2sub(uint64_t a, uint64_t b)
+{
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2mul(uint64_t a, uint64_t b)
+{
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c)
+{
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+// a * b rounded, as a product ptxas cannot contract into a following add: it
+// fuses mul.rn.f32x2 + sub.rn.f32x2 into FFMA2 despite the rounding modifiers
+// (measured: 26 % of decision values 1 ulp off).  fma(a, b, +0) is the rounded
+// product (up to the sign of a zero, which the + tiny of every use absorbs).
+__device__ __forceinline__ uint64_t f2mul_nc(uint64_t a, uint64_t b) { return f2fma(a, b, 0ull); }
+
 // carry a line index 0..7 in the 3 low mantissa bits of a finite value:
 // one LOP3 (v & ~7) | j with j in a register
 __device__ __forceinline__ float enc_idx(float v, int j)
@@ -359,10 +407,22 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     // Computed row by row inside the edge loop below (row i+1 when edge i is
     // clipped), so only rows 0, i, i+1 are live: K = 8 needs 64 registers for all.
     auto drow = [&](int i, float (&r)[K]) {
+        if (DGAL_F32X2 & 1) {   // lines 2q, 2q+1 in one register pair
+            const uint64_t px = f2pack(P.x[i], P.x[i]), py = f2pack(P.y[i], P.y[i]);
+            const uint64_t tiny2 = f2pack(kTiny, kTiny);
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const float Dx = __fsub_rn(P.x[i], Q.x[j]), Dy = __fsub_rn(P.y[i], Q.y[j]);
-            r[j] = __fadd_rn(cross_rn(fx[j], fy[j], Dx, Dy), kTiny);
+            for (int q = 0; q < K / 2; ++q) {
+                const uint64_t Dx = f2sub(px, f2pack(Q.x[2 * q], Q.x[2 * q + 1]));
+                const uint64_t Dy = f2sub(py, f2pack(Q.y[2 * q], Q.y[2 * q + 1]));
+                const uint64_t fx2 = f2pack(fx[2 * q], fx[2 * q + 1]), fy2 = f2pack(fy[2 * q], fy[2 * q + 1]);
+                f2unpack(f2add(f2sub(f2mul_nc(fx2, Dy), f2mul_nc(fy2, Dx)), tiny2), r[2 * q], r[2 * q + 1]);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const float Dx = __fsub_rn(P.x[i], Q.x[j]), Dy = __fsub_rn(P.y[i], Q.y[j]);
+                r[j] = __fadd_rn(cross_rn(fx[j], fy[j], Dx, Dy), kTiny);
+            }
         }
     };
     // p1 vertex i inside p2 (closed test, d never 0): bit i of in1, with its row
@@ -436,15 +496,36 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
             for (int j = 0; j < K; ++j) dn[j] = d0[j];
         }
         float lo = 0.f, hi = hi0;
+        if (DGAL_F32X2 & 2) {   // lines 2q, 2q+1 in one register pair (same arithmetic as below)
+            const uint64_t tiny2 = f2pack(kTiny, kTiny), big2 = f2pack(kBig, kBig);
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const float a = dc[j], b = dn[j];
-            const float den = (a - b) + kTiny;
-            const float r = rcp_approx(den);
-            const float m = __saturatef(-den * kBig);  // 1: bounds below
-            const float ve = enc_idx(a * r, j);
-            lo = fmaxf(lo, m * ve);                 // m * ve == ve (bits kept) or 0
-            hi = fminf(hi, fmaf(m, kBig, ve));      // ve (bits kept) or huge
+            for (int q = 0; q < K / 2; ++q) {
+                const uint64_t a = f2pack(dc[2 * q], dc[2 * q + 1]);
+                const uint64_t den = f2add(f2sub(a, f2pack(dn[2 * q], dn[2 * q + 1])), tiny2);
+                float d0_, d1_;
+                f2unpack(den, d0_, d1_);
+                const uint64_t r = f2pack(rcp_approx(d0_), rcp_approx(d1_));
+                const uint64_t m = f2pack(__saturatef(-d0_ * kBig), __saturatef(-d1_ * kBig));
+                float u0, u1;
+                f2unpack(f2mul(a, r), u0, u1);
+                const uint64_t ve = f2pack(enc_idx(u0, 2 * q), enc_idx(u1, 2 * q + 1));
+                float l0, l1, h0, h1;
+                f2unpack(f2mul(m, ve), l0, l1);
+                f2unpack(f2fma(m, big2, ve), h0, h1);
+                lo = fmaxf(lo, fmaxf(l0, l1));
+                hi = fminf(hi, fminf(h0, h1));
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const float a = dc[j], b = dn[j];
+                const float den = (a - b) + kTiny;
+                const float r = rcp_approx(den);
+                const float m = __saturatef(-den * kBig);  // 1: bounds below
+                const float ve = enc_idx(a * r, j);
+                lo = fmaxf(lo, m * ve);                 // m * ve == ve (bits kept) or 0
+                hi = fminf(hi, fmaf(m, kBig, ve));      // ve (bits kept) or huge
+            }
         }
         const bool in_s = (in1 >> i) & 1u, in_e = (in1 >> i1) & 1u;
         // per-event modes: clamped to the edge (an invalid piece keeps a0 >= a1 without
