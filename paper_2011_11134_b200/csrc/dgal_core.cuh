@@ -79,7 +79,7 @@ __device__ __forceinline__ float rcp_approx(float x)
 // candidates of two p2 lines halves their FMA-pipe instruction count with
 // bitwise the same results.
 #ifndef DGAL_F32X2
-#define DGAL_F32X2 3   // bit 0: decision rows, bit 1: Cyrus-Beck candidates
+#define DGAL_F32X2 7   // bit 0: decision rows, bit 1: Cyrus-Beck candidates, bit 2: backward epilogue (PK callers)
 #endif
 __device__ __forceinline__ uint64_t f2pack(float lo, float hi)
 {
@@ -972,7 +972,7 @@ __device__ __forceinline__ void bwd_crossing_exact(const float *sPx, const float
 }
 
 // V = OR of the flag table over the recorded bytes (vertex / crossing provenance).
-template <int K, int TILE>
+template <int K, int TILE, bool PK = false>
 __device__ __forceinline__ void bwd_epilogue(const float *sPx, const float *sPy, const float *sQx,
                                              const float *sQy, float g, uint32_t V, const float *scr,
                                              Poly<K> &G1, Poly<K> &G2, const Extrude ex = flat(),
@@ -983,6 +983,82 @@ __device__ __forceinline__ void bwd_epilogue(const float *sPx, const float *sPy,
     if (co) *co = VolCoef{0.f, 0.f, 0.f, 0.f, 0.f};
     if (V == 0) return;  // nx == 0: zero subgradient
 
+    if constexpr (PK && (DGAL_F32X2 & 4)) {
+    // paired FP32 along (p1, p2): X[k] = (v_k.x, w_k.x), Y[k] = (v_k.y, w_k.y) recentred
+    // on v_0; edge vectors EX/EY = (g, f), their negatives NX, shoelace terms C =
+    // (C1, C2); every per-edge / per-vertex quantity below is a (p1, p2) pair
+    uint64_t X[K], Y[K];
+    {
+        const float ox = sPx[0], oy = sPy[0];
+        const uint64_t o2x = f2pack(ox, ox), o2y = f2pack(oy, oy);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            X[k] = f2sub(f2pack(sPx[k], sQx[k]), o2x);
+            Y[k] = f2sub(f2pack(sPy[k], sQy[k]), o2y);
+        }
+    }
+    uint64_t EY[K], NX[K], C[K], A12 = 0ull;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        const int i1 = (i + 1) % K;
+        EY[i] = f2sub(Y[i1], Y[i]);
+        NX[i] = f2sub(X[i], X[i1]);
+        C[i] = f2fma(X[i], Y[i1], f2sub(0ull, f2mul(X[i1], Y[i])));
+        A12 = f2add(A12, C[i]);
+    }
+    float A1x2, A2x2;
+    f2unpack(A12, A1x2, A2x2);
+
+    // boundary pieces -> A_i and the edge weights
+    //   alpha = ∫ (1-t) dt = l (1 - h),  beta = ∫ t dt = l h,  l = t1 - t0, h = (t0 + t1)/2
+    // (edge i on the boundary, as masks: vertex i, vertex i+1 (rotated) or a crossing)
+    constexpr uint32_t KMASK = (1u << K) - 1u;
+    const uint32_t v1 = V & KMASK, v2 = (V >> 8) & KMASK;
+    const uint32_t on1m = v1 | ((v1 >> 1) | (v1 << (K - 1))) | (V >> 16);
+    const uint32_t on2m = v2 | ((v2 >> 1) | (v2 << (K - 1))) | (V >> 24);
+    uint64_t AL[K], BE[K], AIX = 0ull;
+    const uint64_t half2 = f2pack(0.5f, 0.5f);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        const uint64_t T0 = f2pack(scr[i * TILE], scr[(2 * K + i) * TILE]);
+        const uint64_t T1 = f2pack(scr[(K + i) * TILE], scr[(3 * K + i) * TILE]);
+        float d1, d2;
+        f2unpack(f2sub(T1, T0), d1, d2);
+        const uint64_t L = f2pack(((on1m >> i) & 1u) ? fmaxf(d1, 0.f) : 0.f, ((on2m >> i) & 1u) ? fmaxf(d2, 0.f) : 0.f);
+        const uint64_t H = f2mul(f2add(T0, T1), half2);
+        BE[i] = f2mul(L, H);
+        AL[i] = f2sub(L, BE[i]);
+        AIX = f2fma(L, C[i], AIX);
+    }
+    float ai1, ai2;
+    f2unpack(AIX, ai1, ai2);
+    const float Aix2 = ai1 + ai2;
+
+    // dIoU/dV_i = (V_u + V_i)/V_u^2, dIoU/dV_1,2 = -V_i/V_u^2; V = A d (2D: d = 1)
+    const float Ai = 0.5f * Aix2;
+    const float Vi = Ai * ex.dz;
+    const float Vu = 0.5f * ((A1x2 * ex.d1 + A2x2 * ex.d2) - Aix2 * ex.dz);
+    if (!(Vu > 0.f) || !(Vi > 0.f)) return;  // R10 guard
+    const float inv = 1.f / Vu;
+    const float q = Vi * inv;
+    const float cvi = g * ((1.f + q) * inv);
+    const float cvu = g * (-q * inv);
+    const float ci = cvi * ex.dz;
+    // area_grad of p1/p2 is (n_k + n_k-1)/2 per vertex
+    const float hu1 = (0.5f * cvu) * ex.d1, hu2 = (0.5f * cvu) * ex.d2;
+    if (co) *co = VolCoef{cvi, cvu, Ai, 0.5f * A1x2, 0.5f * A2x2};
+
+    // vertex k collects edge k (as its start, alpha) and edge k-1 (as its end, beta);
+    // n = perp(edge) = (e_y, -e_x)
+    const uint64_t CI = f2pack(ci, ci), HU = f2pack(hu1, hu2);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int km = (k + K - 1) % K;
+        const uint64_t WA = f2fma(CI, AL[k], HU), WB = f2fma(CI, BE[km], HU);
+        f2unpack(f2fma(WA, EY[k], f2mul(WB, EY[km])), G1.x[k], G2.x[k]);
+        f2unpack(f2fma(WA, NX[k], f2mul(WB, NX[km])), G1.y[k], G2.y[k]);
+    }
+    } else {
     Poly<K> P, Q;
     {
         const float ox = sPx[0], oy = sPy[0];
@@ -1058,6 +1134,7 @@ __device__ __forceinline__ void bwd_epilogue(const float *sPx, const float *sPy,
         G2.x[k] = fmaf(wa2, fy[k], wb2 * fy[km]);
         G2.y[k] = -fmaf(wa2, fx[k], wb2 * fx[km]);
     }
+    }
 }
 
 // One backward tile: thread tid owns pair tid of a tile of TILE pairs whose
@@ -1065,7 +1142,7 @@ __device__ __forceinline__ void bwd_epilogue(const float *sPx, const float *sPy,
 // flag bytes into provenance bits, queues its Cross bytes in the warp's queue
 // (warp prefix sum), evaluates the warp's crossings 32 at a time (full SIMT
 // width), then runs the epilogue.  Must be called by all 32 lanes of the warp.
-template <int K, int TILE, class GEO = TileGeometry<K>>
+template <int K, int TILE, class GEO = TileGeometry<K>, bool PK = false>
 __device__ __forceinline__ void bwd_tile_pair(const float *tx1, const float *ty1, const float *tx2,
                                               const float *ty2, const Seq<K> &sq, int m, float g, bool live,
                                               float *scr, uint16_t *queue, const FlagLut &lut,
@@ -1148,8 +1225,8 @@ __device__ __forceinline__ void bwd_tile_pair(const float *tx1, const float *ty1
     }
     __syncwarp();
     if (live)
-        bwd_epilogue<K, TILE>(tx1 + tid * K, ty1 + tid * K, tx2 + tid * K, ty2 + tid * K, g, V, scr + tid, G1, G2,
-                              ex, co);
+        bwd_epilogue<K, TILE, PK>(tx1 + tid * K, ty1 + tid * K, tx2 + tid * K, ty2 + tid * K, g, V, scr + tid, G1,
+                                  G2, ex, co);
 }
 
 }  // namespace dgal

@@ -392,8 +392,8 @@ paired_bwd_pt_kernel(int64_t n, const float *__restrict__ x1, const float *__res
 #pragma unroll
         for (int q = 0; q < K / 4; ++q) sq.w[q] = live ? D.xf[tid * (K / 4) + q] : 0ull;
         Poly<K> G1, G2;
-        bwd_tile_pair<K, T>(D.x1, D.y1, D.x2, D.y2, sq, m, live ? D.g[tid] : 0.f, live, S.scr,
-                            S.queue[tid >> 5], S.lut, G1, G2);
+        bwd_tile_pair<K, T, TileGeometry<K>, K == 4>(D.x1, D.y1, D.x2, D.y2, sq, m, live ? D.g[tid] : 0.f, live,
+                                                     S.scr, S.queue[tid >> 5], S.lut, G1, G2);
         if (live) {
             store_plane<K>(gx1, k, G1.x);
             store_plane<K>(gy1, k, G1.y);
