@@ -775,7 +775,7 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
 // trip, no crossing recomputation): dA_i/dv_i += n_i ∫(1-t)dt, dA_i/dv_i+1 +=
 // n_i ∫t dt over each boundary piece, then the S:303 chain.
 // p1, p2 recentred on p1.v0.  Returns IoU (identical to the pairwise path).
-template <int K, int MODE = kP2Pieces>
+template <int K, int MODE = kP2Pieces, bool PK = false>
 __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, float g, Poly<K> &G1,
                                            Poly<K> &G2, const Extrude ex = flat(), VolCoef *co = nullptr,
                                            QTable qt = QTable{nullptr, nullptr, 0})
@@ -792,6 +792,51 @@ __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, f
     if (!(Vux2 > 0.f) || !(Vix2 > 0.f)) return 0.f;
     const float iou = fminf(Vix2 / Vux2, 1.f);
 
+    if constexpr (PK && (DGAL_F32X2 & 4)) {
+        // the same weights and gradients with (p1, p2) quantities in paired FP32
+        const float *ax = c.ax, *ay = c.ay, *bx = c.bx, *by = c.by;
+        const uint64_t half2 = f2pack(0.5f, 0.5f);
+        uint64_t AL[K], BE[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const float fx = c.fx[i], fy = c.fy[i];
+            const float inv = rcp_approx(fmaf(fx, fx, fy * fy));
+            const uint64_t dx = f2sub(f2pack(ax[i], bx[i]), f2pack(Q.x[i], Q.x[i]));
+            const uint64_t dy = f2sub(f2pack(ay[i], by[i]), f2pack(Q.y[i], Q.y[i]));
+            float s0, s1;
+            f2unpack(f2mul(f2fma(dx, f2pack(fx, fx), f2mul(dy, f2pack(fy, fy))), f2pack(inv, inv)), s0, s1);
+            const uint64_t T0 = f2pack(__saturatef(c.t0[i]), __saturatef(s0));
+            const uint64_t T1 = f2pack(__saturatef(c.t1[i]), __saturatef(s1));
+            float d1, d2;
+            f2unpack(f2sub(T1, T0), d1, d2);
+            const uint64_t L = f2pack(fmaxf(d1, 0.f), ((c.on2 >> i) & 1u) ? fmaxf(d2, 0.f) : 0.f);
+            BE[i] = f2mul(L, f2mul(f2add(T0, T1), half2));
+            AL[i] = f2sub(L, BE[i]);
+        }
+        const float Vi = 0.5f * Vix2, Vu = 0.5f * Vux2;
+        const float inv = 1.f / Vu;
+        const float q = Vi * inv;
+        const float cvi = g * ((1.f + q) * inv);
+        const float cvu = g * (-q * inv);
+        const float ci = cvi * ex.dz;
+        const float hu1 = (0.5f * cvu) * ex.d1, hu2 = (0.5f * cvu) * ex.d2;
+        if (co) *co = VolCoef{cvi, cvu, 0.5f * c.Aix2, 0.5f * c.A1x2, 0.5f * c.A2x2};
+        const uint64_t CI = f2pack(ci, ci), HU = f2pack(hu1, hu2);
+        uint64_t EY[K], NX[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            EY[k] = f2pack(c.gy[k], c.fy[k]);
+            NX[k] = f2sub(0ull, f2pack(c.gx[k], c.fx[k]));
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int km = (k + K - 1) % K;
+            const uint64_t WA = f2fma(CI, AL[k], HU), WB = f2fma(CI, BE[km], HU);
+            f2unpack(f2fma(WA, EY[k], f2mul(WB, EY[km])), G1.x[k], G2.x[k]);
+            f2unpack(f2fma(WA, NX[k], f2mul(WB, NX[km])), G1.y[k], G2.y[k]);
+        }
+        return iou;
+    }
     // piece weights (saturate: dead edges carry arbitrary end points, length 0)
     // p2 pieces: parameters of their end points (the crossing points of the p1
     // side) along the edge (projection; exact 0 at w_j)

@@ -512,6 +512,9 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
                     float *__restrict__ gx1, float *__restrict__ gy1,
                     float *__restrict__ gx2, float *__restrict__ gy2)
 {
+#ifndef DGAL_FUSED_PK
+#define DGAL_FUSED_PK true   // K = 4: gradient part in paired FP32 (K = 8 would spill)
+#endif
 #ifndef DGAL_FUSED_P2MODE
 #define DGAL_FUSED_P2MODE kP2PiecesSmem   // A/B: kP2Pieces 0.571 ms, kP2PiecesSmem 0.526 ms (cfg3)
 #endif
@@ -524,7 +527,7 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
     load_poly<K>(x2, y2, k, Q);
     const float g = grad ? __ldcs(grad + k) : scale;
     recentre<K>(P, Q);
-    const float v = iou_fused<K, DGAL_FUSED_P2MODE>(P, Q, g, G1, G2, flat(), nullptr,
+    const float v = iou_fused<K, DGAL_FUSED_P2MODE, K == 4 && DGAL_FUSED_PK>(P, Q, g, G1, G2, flat(), nullptr,
                                                     QTable{pt + threadIdx.x, pt + 2 * K * T + threadIdx.x, T});
     if (iou) __stcs(iou + k, v);
     store_plane<K>(gx1, k, G1.x);
