@@ -47,6 +47,15 @@ def test_ragged_sizes(n):
     check_paired_against_oracle(margin_batch(1, n))
 
 
+@pytest.mark.parametrize("cfg,n", [(3, 127), (3, 1023), (3, 1025), (3, 8193), (4, 1), (4, 129), (4, 511),
+                                   (4, 513), (4, 2049)])
+def test_ragged_around_cta_chunks(cfg, n):
+    """Sizes around the kernels' CTA chunks (forward: 128 threads x 8 tiles for K=4,
+    x 4 tiles for K=8, with the cp.async ring; backward: 128-pair tiles x 8 (K=4) or
+    the 128-pair producer tiles (K=8)) — the partial last tile and the partial chunk."""
+    check_paired_against_oracle(margin_batch(cfg, n))
+
+
 def _pairs(P_list, Q_list, K):
     P = np.stack(P_list).astype(np.float32)
     Q = np.stack(Q_list).astype(np.float32)
