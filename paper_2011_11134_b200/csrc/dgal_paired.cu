@@ -298,6 +298,9 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
 #ifndef DGAL_BWD4_PT
 #define DGAL_BWD4_PT 1        // K = 4 backward: per-thread prefetch kernel (0: producer-warp kernel)
 #endif
+#ifndef DGAL_BWD_REV
+#define DGAL_BWD_REV 1
+#endif
 #ifndef DGAL_BWDPT_THREADS
 #define DGAL_BWDPT_THREADS 128
 #endif
@@ -351,7 +354,13 @@ paired_bwd_pt_kernel(int64_t n, const float *__restrict__ x1, const float *__res
     extern __shared__ __align__(128) unsigned char smem_raw[];
     BwdPtSmem<K> &S = *reinterpret_cast<BwdPtSmem<K> *>(smem_raw);
     const int tid = threadIdx.x;
-    const int64_t base = (int64_t)blockIdx.x * (NT * T);
+    // DGAL_BWD_REV: chunks and tiles in descending order, so the first tiles the
+    // backward reads are the last ones the forward touched (still in L2), and the
+    // next forward's first tiles are the last ones this kernel read.
+    const int64_t chunk = DGAL_BWD_REV ? (int64_t)(gridDim.x - 1 - blockIdx.x) : (int64_t)blockIdx.x;
+    const int64_t base = chunk * (NT * T);
+    const int nv = (int)min((int64_t)NT, (n - base + T - 1) / T);   // tiles of this chunk in range
+    auto tile_base = [&](int t) { return base + (int64_t)(DGAL_BWD_REV ? (nv - 1 - t) : t) * T; };
     auto prefetch = [&](int stage, int64_t k) {
         typename BwdPtSmem<K>::Stage &D = S.st[stage];
 #pragma unroll
@@ -366,23 +375,24 @@ paired_bwd_pt_kernel(int64_t n, const float *__restrict__ x1, const float *__res
         else cp_async16(D.xf + 2 * tid, xflags + k * 16);
     };
     int m_next = 0;
-    if (base + tid < n) {
-        prefetch(0, base + tid);
-        m_next = nx[base + tid];
+    if (tile_base(0) + tid < n) {
+        prefetch(0, tile_base(0) + tid);
+        m_next = nx[tile_base(0) + tid];
     }
     cp_async_commit();
     fill_flag_lut(S.lut, tid, T);
     __syncthreads();
 #pragma unroll 1
-    for (int t = 0; t < NT; ++t) {
-        const int64_t kb = base + (int64_t)t * T;
-        if (kb >= n) break;                      // CTA-uniform
-        const int64_t k = kb + tid;
+    for (int t = 0; t < nv; ++t) {
+        const int64_t k = tile_base(t) + tid;
         const bool live = k < n;
         const int m = live ? m_next : 0;
-        if (t + 1 < NT && k + T < n) {
-            prefetch((t + 1) & 1, k + T);
-            m_next = nx[k + T];
+        if (t + 1 < nv) {
+            const int64_t kn = tile_base(t + 1) + tid;
+            if (kn < n) {
+                prefetch((t + 1) & 1, kn);
+                m_next = nx[kn];
+            }
         }
         cp_async_commit();
         cp_async_wait<1>();                      // this thread's copies of tile t landed
