@@ -33,4 +33,23 @@ for cfg, n in ((3, 1 << 24), (4, 1 << 22)):
     z.record()
     torch.cuda.synchronize()
     res[f"cfg{cfg}_step"] = round(a.elapsed_time(z) / 50, 4)
+for dims in (2, 3):
+    bb = synth.gen_box_pairs(1 << 24, dims)
+    n = bb.n
+    B1, B2 = torch.from_numpy(bb.b1).to(dev), torch.from_numpy(bb.b2).to(dev)
+    g = torch.full((n,), -1.0 / n, device=dev)
+    fo = dgal.box_iou_paired_fwd(B1, B2)
+    go = dgal.box_iou_paired_bwd(B1, B2, g, fo[1], fo[2])
+    for _ in range(5):
+        dgal.box_iou_paired_fwd(B1, B2, out=fo)
+        dgal.box_iou_paired_bwd(B1, B2, g, fo[1], fo[2], out=go)
+    a, z = E(), E()
+    a.record()
+    for _ in range(30):
+        dgal.box_iou_paired_fwd(B1, B2, out=fo)
+        dgal.box_iou_paired_bwd(B1, B2, g, fo[1], fo[2], out=go)
+    z.record()
+    torch.cuda.synchronize()
+    res[f"box{dims}_step"] = round(a.elapsed_time(z) / 30, 4)
+    del B1, B2, g, fo, go
 print(label, res, flush=True)
