@@ -22,6 +22,9 @@ METRICS = [
     ("lsu_pipe_pct", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
     ("local_ld_bytes", "l1tex__t_bytes_pipe_lsu_mem_local_op_ld.sum"),
     ("local_st_bytes", "l1tex__t_bytes_pipe_lsu_mem_local_op_st.sum"),
+    # --set full on ncu 2025.2 carries sectors (32 B) rather than bytes for local memory
+    ("local_ld_sectors", "l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum"),
+    ("local_st_sectors", "l1tex__t_sectors_pipe_lsu_mem_local_op_st.sum"),
 ]
 
 

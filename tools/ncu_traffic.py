@@ -11,7 +11,7 @@ import re
 import sys
 
 KEYS = [  # (key, kernel regex); first match in launch order (the second pw_zero is the mask fill)
-    ("paired_fwd_k4", r"paired_fwd_direct_kernel<4>"), ("paired_bwd_k4", r"paired_bwd_kernel<4>"),
+    ("paired_fwd_k4", r"paired_fwd_direct_kernel<4>"), ("paired_bwd_k4", r"paired_bwd(_pt)?_kernel<4>"),
     ("paired_fused_k4", r"paired_fused_kernel<4>"), ("paired_fwd_k8", r"paired_fwd_direct_kernel<8>"),
     ("paired_bwd_k8", r"paired_bwd_kernel<8>"), ("paired_fused_k8", r"paired_fused_kernel<8>"),
     ("box_fwd_d2", r"box_fwd_kernel<2>"), ("box_bwd_d2", r"box_bwd_kernel<2>"), ("box_fused_d2", r"box_fused_kernel<2>"),
