@@ -168,12 +168,14 @@ def run_reference(args, rank):
     import synth
     batch = synth.gen_cfg3_pairs(1 << 18)
     nt = oracle.max_threads()
-    # each step = fwd+bwd over a bounded sample sized from a probe to ~1 s/step
+    # each step = fwd+bwd over a bounded sample sized from a probe to ~1 s/step, less when
+    # many steps are asked for, so the whole run stays near 2 minutes
     probe = batch.take(np.arange(20000))
     t = time.perf_counter()
     oracle_fwdbwd(probe, nt)
     rate = probe.n / (time.perf_counter() - t)
-    n = int(min(batch.n, max(20000, rate * 1.0)))
+    per_step_s = min(1.0, 120.0 / max(1, args.steps + args.warmup))
+    n = int(min(batch.n, max(4096, rate * per_step_s)))
     s = batch.take(np.arange(n))
     for _ in range(args.warmup):
         oracle_fwdbwd(s, nt)
