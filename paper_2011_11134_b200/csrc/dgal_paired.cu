@@ -513,6 +513,19 @@ cudaError_t launch_paired_bwd(int K, int64_t n, const float *x1, const float *y1
 #endif
 constexpr int kFused4Threads = DGAL_FUSED4_THREADS, kFused8Threads = DGAL_FUSED8_THREADS;
 
+#ifndef DGAL_FUSED_PF
+#define DGAL_FUSED_PF 1       // NT consecutive tiles per CTA, tile t+1 copied (cp.async) while tile t computes
+#endif
+#ifndef DGAL_FUSED4_NT
+#define DGAL_FUSED4_NT 8
+#endif
+#ifndef DGAL_FUSED8_NT
+#define DGAL_FUSED8_NT 4
+#endif
+#ifndef DGAL_FUSED8_PF
+#define DGAL_FUSED8_PF 0      // K = 8: ring + piece table exceed 48 KB of static shared memory
+#endif
+
 template <int K>
 __global__ void __launch_bounds__((K == 4) ? kFused4Threads : kFused8Threads,
                                   (K == 4) ? DGAL_FUSED4_MINB : DGAL_FUSED8_MINB)
@@ -529,32 +542,80 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
 #define DGAL_FUSED_P2MODE kP2PiecesSmem   // A/B: kP2Pieces 0.571 ms, kP2PiecesSmem 0.526 ms (cfg3)
 #endif
     constexpr int T = (K == 4) ? kFused4Threads : kFused8Threads;
+    constexpr bool PF = (K == 4) ? DGAL_FUSED_PF : DGAL_FUSED8_PF;
+    constexpr int NT = !PF ? 1 : (K == 4) ? DGAL_FUSED4_NT : DGAL_FUSED8_NT;
     __shared__ float pt[(DGAL_FUSED_P2MODE == kP2PiecesSmem) ? 4 * K * T : 1];   // piece table, [slot][thread]
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    Poly<K> P, Q, G1, G2;
-    load_poly<K>(x1, y1, k, P);
-    load_poly<K>(x2, y2, k, Q);
-    const float g = grad ? __ldcs(grad + k) : scale;
-    recentre<K>(P, Q);
-    const float v = iou_fused<K, DGAL_FUSED_P2MODE, K == 4 && DGAL_FUSED_PK>(P, Q, g, G1, G2, flat(), nullptr,
-                                                    QTable{pt + threadIdx.x, pt + 2 * K * T + threadIdx.x, T});
-    if (iou) __stcs(iou + k, v);
-    store_plane<K>(gx1, k, G1.x);
-    store_plane<K>(gy1, k, G1.y);
-    store_plane<K>(gx2, k, G2.x);
-    store_plane<K>(gy2, k, G2.y);
+    // PF: 2-stage per-thread ring [stage][plane][thread][K] + [stage][thread] for dL/dIoU
+    // (each thread copies and reads only its own bytes: no CTA barrier)
+    __shared__ __align__(16) float ring[PF ? 2 * 4 * T * K : 4];
+    __shared__ float gring[PF ? 2 * T : 1];
+    const int tid = threadIdx.x;
+    const int64_t k0 = (int64_t)blockIdx.x * (NT * T) + tid;
+    auto prefetch = [&](int stage, int64_t k) {
+        float *r = ring + stage * (4 * T * K) + tid * K;
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q) {
+            cp_async16(r + 4 * q, x1 + k * K + 4 * q);
+            cp_async16(r + T * K + 4 * q, y1 + k * K + 4 * q);
+            cp_async16(r + 2 * T * K + 4 * q, x2 + k * K + 4 * q);
+            cp_async16(r + 3 * T * K + 4 * q, y2 + k * K + 4 * q);
+        }
+        if (grad) cp_async4(gring + stage * T + tid, grad + k);
+    };
+    if (PF) {
+        if (k0 < n) prefetch(0, k0);
+        cp_async_commit();
+    }
+#pragma unroll 1
+    for (int t = 0; t < NT; ++t) {
+        const int64_t k = k0 + (int64_t)t * T;
+        if (k >= n) break;
+        Poly<K> P, Q, G1, G2;
+        float g = scale;
+        if (PF) {
+            if (t + 1 < NT && k + T < n) prefetch((t + 1) & 1, k + T);
+            cp_async_commit();
+            cp_async_wait<1>();   // this thread's copies of tile t have landed
+            const float *r = ring + (t & 1) * (4 * T * K) + tid * K;
+#pragma unroll
+            for (int q = 0; q < K / 4; ++q) {
+                const float4 u = *reinterpret_cast<const float4 *>(r + 4 * q);
+                const float4 v = *reinterpret_cast<const float4 *>(r + T * K + 4 * q);
+                const float4 w = *reinterpret_cast<const float4 *>(r + 2 * T * K + 4 * q);
+                const float4 z = *reinterpret_cast<const float4 *>(r + 3 * T * K + 4 * q);
+                P.x[4 * q] = u.x; P.x[4 * q + 1] = u.y; P.x[4 * q + 2] = u.z; P.x[4 * q + 3] = u.w;
+                P.y[4 * q] = v.x; P.y[4 * q + 1] = v.y; P.y[4 * q + 2] = v.z; P.y[4 * q + 3] = v.w;
+                Q.x[4 * q] = w.x; Q.x[4 * q + 1] = w.y; Q.x[4 * q + 2] = w.z; Q.x[4 * q + 3] = w.w;
+                Q.y[4 * q] = z.x; Q.y[4 * q + 1] = z.y; Q.y[4 * q + 2] = z.z; Q.y[4 * q + 3] = z.w;
+            }
+            if (grad) g = gring[(t & 1) * T + tid];
+        } else {
+            load_poly<K>(x1, y1, k, P);
+            load_poly<K>(x2, y2, k, Q);
+            if (grad) g = __ldcs(grad + k);
+        }
+        recentre<K>(P, Q);
+        const float v = iou_fused<K, DGAL_FUSED_P2MODE, K == 4 && DGAL_FUSED_PK>(P, Q, g, G1, G2, flat(), nullptr,
+                                                        QTable{pt + tid, pt + 2 * K * T + tid, T});
+        if (iou) __stcs(iou + k, v);
+        store_plane<K>(gx1, k, G1.x);
+        store_plane<K>(gy1, k, G1.y);
+        store_plane<K>(gx2, k, G2.x);
+        store_plane<K>(gy2, k, G2.y);
+    }
 }
 
 cudaError_t launch_paired_fused(int K, int64_t n, const float *x1, const float *y1, const float *x2,
                                 const float *y2, const float *grad, float scale, float *iou, float *gx1,
                                 float *gy1, float *gx2, float *gy2, cudaStream_t st)
 {
+    constexpr int64_t per4 = (int64_t)(DGAL_FUSED_PF ? DGAL_FUSED4_NT : 1) * kFused4Threads;
+    constexpr int64_t per8 = (int64_t)(DGAL_FUSED8_PF ? DGAL_FUSED8_NT : 1) * kFused8Threads;
     if (K == 4)
-        paired_fused_kernel<4><<<(unsigned)((n + kFused4Threads - 1) / kFused4Threads), kFused4Threads, 0, st>>>(
+        paired_fused_kernel<4><<<(unsigned)((n + per4 - 1) / per4), kFused4Threads, 0, st>>>(
             n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2);
     else
-        paired_fused_kernel<8><<<(unsigned)((n + kFused8Threads - 1) / kFused8Threads), kFused8Threads, 0, st>>>(
+        paired_fused_kernel<8><<<(unsigned)((n + per8 - 1) / per8), kFused8Threads, 0, st>>>(
             n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2);
     return cudaGetLastError();
 }
