@@ -17,6 +17,7 @@
 // Parameter order: 2D (cx, cy, w, h, theta), 3D (cx, cy, cz, w, h, d, theta).
 #include "dgal_core.cuh"
 #include "dgal_internal.h"
+#include "dgal_pipe.cuh"
 
 namespace dgal {
 
@@ -42,6 +43,9 @@ namespace {
 #endif
 constexpr int kBoxTile = DGAL_BOX_BWD_TILE;  // backward tile = CTA size
 constexpr int kBoxFusedT = DGAL_BOX_FUSED_T;
+#ifndef DGAL_BOX_FUSED_NT
+#define DGAL_BOX_FUSED_NT 8   // tiles per CTA with the prefetch ring (DGAL_BOX_PF)
+#endif
 // CTAs per SM the box forward / fused kernels are register-budgeted for (the
 // largest without local-memory spills, tools/sass_stats.py)
 #ifndef DGAL_BOX_FWD2_MINB
@@ -86,6 +90,45 @@ __device__ __forceinline__ Box<DIMS> load_box(const float *__restrict__ b, int64
     }
     return r;
 }
+
+// Per-thread prefetch ring of box parameters (DGAL_BOX_PF): parameter q of box 1 /
+// box 2 of this thread's pair at v[stage][q][tid] / v[stage][P + q][tid], copied
+// with 4-byte cp.async (any layout: planes or rows), dL/dIoU at g[stage][tid].
+// Each thread copies and reads only its own words (no CTA barrier).
+#ifndef DGAL_BOX_PF
+#define DGAL_BOX_PF 1
+#endif
+template <int DIMS, int T>
+struct BoxRing {
+    static constexpr int P = DIMS == 3 ? 7 : 5;
+    float v[2][2 * P][T];
+    float g[2][T];
+    __device__ __forceinline__ void prefetch(int stage, const float *__restrict__ b1, const float *__restrict__ b2,
+                                             const float *__restrict__ grad, int64_t k, int64_t sk, int64_t sp,
+                                             int tid)
+    {
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            cp_async4(&v[stage][q][tid], b1 + k * sk + q * sp);
+            cp_async4(&v[stage][P + q][tid], b2 + k * sk + q * sp);
+        }
+        if (grad) cp_async4(&g[stage][tid], grad + k);
+    }
+    __device__ __forceinline__ Box<DIMS> get(int stage, int which, int tid) const
+    {
+        const float *r = &v[stage][which * P][0];
+        Box<DIMS> b;
+        b.cx = r[0 * T + tid];
+        b.cy = r[1 * T + tid];
+        if (DIMS == 3) {
+            b.cz = r[2 * T + tid]; b.w = r[3 * T + tid]; b.h = r[4 * T + tid]; b.d = r[5 * T + tid];
+            b.th = r[6 * T + tid];
+        } else {
+            b.cz = 0.f; b.w = r[2 * T + tid]; b.h = r[3 * T + tid]; b.d = 1.f; b.th = r[4 * T + tid];
+        }
+        return b;
+    }
+};
 
 // cos / sin of theta: exact reduction of theta / pi (no Payne-Hanek slow path, no
 // local memory); theta is accepted unbounded.
@@ -220,21 +263,33 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
                float *__restrict__ iou, uint8_t *__restrict__ nx, uint8_t *__restrict__ xflags)
 {
     constexpr int T = kBoxFwdT;
+    constexpr bool PF = DGAL_BOX_PF;
     __shared__ float sq[8 * T];   // per-thread p2 vertex table (kP2Smem), [k][thread]
     __shared__ WalkLut4 wlut;     // flag-walk tables
-    const int64_t k0 = (int64_t)blockIdx.x * (kBoxFwdNT * T) + threadIdx.x;
+    __shared__ __align__(16) BoxRing<DIMS, PF ? T : 1> ring;   // tile t+1 in flight while tile t computes
+    const int tid = threadIdx.x;
+    const int64_t k0 = (int64_t)blockIdx.x * (kBoxFwdNT * T) + tid;
     Box<DIMS> a, b;
-    if (k0 < n) {   // the first tile's loads go out before the table fill
+    if (PF) {
+        if (k0 < n) ring.prefetch(0, b1, b2, nullptr, k0, sk, sp, tid);
+        cp_async_commit();
+    } else if (k0 < n) {   // the first tile's loads go out before the table fill
         a = load_box<DIMS>(b1, k0, sk, sp);
         b = load_box<DIMS>(b2, k0, sk, sp);
     }
-    load_walk_lut4(wlut, threadIdx.x, T);
+    load_walk_lut4(wlut, tid, T);
     __syncthreads();
 #pragma unroll 1
     for (int t = 0; t < kBoxFwdNT; ++t) {
         const int64_t k = k0 + (int64_t)t * T;
         if (k >= n) break;
-        if (t > 0) {
+        if (PF) {
+            if (t + 1 < kBoxFwdNT && k + T < n) ring.prefetch((t + 1) & 1, b1, b2, nullptr, k + T, sk, sp, tid);
+            cp_async_commit();
+            cp_async_wait<1>();   // this thread's copies of tile t have landed
+            a = ring.get(t & 1, 0, tid);
+            b = ring.get(t & 1, 1, tid);
+        } else if (t > 0) {
             a = load_box<DIMS>(b1, k, sk, sp);
             b = load_box<DIMS>(b2, k, sk, sp);
         }
@@ -370,22 +425,46 @@ box_fused_kernel(int64_t n, const float *__restrict__ b1, const float *__restric
                  float *__restrict__ gb2)
 {
     constexpr int T = kBoxFusedT;
+    constexpr bool PF = DGAL_BOX_PF;
+    constexpr int NT = PF ? DGAL_BOX_FUSED_NT : 1;
     __shared__ float pt[16 * T];   // per-thread piece table (kP2PiecesSmem), [slot][thread]
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    const Box<DIMS> a = load_box<DIMS>(b1, k, sk, sp), b = load_box<DIMS>(b2, k, sk, sp);
-    const float g = grad ? __ldcs(grad + k) : scale;
-    Poly<4> P, Q, G1, G2;
-    const Trig t = box_pair_polys<DIMS>(a, b, P, Q);
-    const ZOver z = z_overlap<DIMS>(a, b);
-    VolCoef co;
-    const float v = iou_fused<4, kP2PiecesSmem, DIMS == 2 && DGAL_BOX_FUSED_PK>(P, Q, g, G1, G2, Extrude{z.dz, a.d, b.d}, &co,
-                                                QTable{pt + threadIdx.x, pt + 8 * T + threadIdx.x, T});
-    if (iou) __stcs(iou + k, v);
-    float gcz1, gd1, gcz2, gd2;
-    z_grads<DIMS>(co, z, gcz1, gd1, gcz2, gd2);
-    store_box_grad<DIMS>(gb1, k, sk, sp, box_vjp(a.w, a.h, t.c1, t.s1, G1), gcz1, gd1);
-    store_box_grad<DIMS>(gb2, k, sk, sp, box_vjp(b.w, b.h, t.c2, t.s2, G2), gcz2, gd2);
+    __shared__ __align__(16) BoxRing<DIMS, PF ? T : 1> ring;   // tile t+1 in flight while tile t computes
+    const int tid = threadIdx.x;
+    const int64_t k0 = (int64_t)blockIdx.x * (NT * T) + tid;
+    if (PF) {
+        if (k0 < n) ring.prefetch(0, b1, b2, grad, k0, sk, sp, tid);
+        cp_async_commit();
+    }
+#pragma unroll 1
+    for (int it = 0; it < NT; ++it) {
+        const int64_t k = k0 + (int64_t)it * T;
+        if (k >= n) break;
+        Box<DIMS> a, b;
+        float g = scale;
+        if (PF) {
+            if (it + 1 < NT && k + T < n) ring.prefetch((it + 1) & 1, b1, b2, grad, k + T, sk, sp, tid);
+            cp_async_commit();
+            cp_async_wait<1>();   // this thread's copies of tile it have landed
+            a = ring.get(it & 1, 0, tid);
+            b = ring.get(it & 1, 1, tid);
+            if (grad) g = ring.g[it & 1][tid];
+        } else {
+            a = load_box<DIMS>(b1, k, sk, sp);
+            b = load_box<DIMS>(b2, k, sk, sp);
+            if (grad) g = __ldcs(grad + k);
+        }
+        Poly<4> P, Q, G1, G2;
+        const Trig t = box_pair_polys<DIMS>(a, b, P, Q);
+        const ZOver z = z_overlap<DIMS>(a, b);
+        VolCoef co;
+        const float v = iou_fused<4, kP2PiecesSmem, DIMS == 2 && DGAL_BOX_FUSED_PK>(P, Q, g, G1, G2, Extrude{z.dz, a.d, b.d},
+                                                    &co, QTable{pt + tid, pt + 8 * T + tid, T});
+        if (iou) __stcs(iou + k, v);
+        float gcz1, gd1, gcz2, gd2;
+        z_grads<DIMS>(co, z, gcz1, gd1, gcz2, gd2);
+        store_box_grad<DIMS>(gb1, k, sk, sp, box_vjp(a.w, a.h, t.c1, t.s1, G1), gcz1, gd1);
+        store_box_grad<DIMS>(gb2, k, sk, sp, box_vjp(b.w, b.h, t.c2, t.s2, G2), gcz2, gd2);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -431,7 +510,8 @@ cudaError_t launch_box_fused(int dims, int layout, int64_t n, const float *b1, c
 {
     int64_t sk, sp;
     box_strides(dims, layout, n, sk, sp);
-    const unsigned grid = (unsigned)((n + kBoxFusedT - 1) / kBoxFusedT);
+    constexpr int64_t per = (int64_t)(DGAL_BOX_PF ? DGAL_BOX_FUSED_NT : 1) * kBoxFusedT;
+    const unsigned grid = (unsigned)((n + per - 1) / per);
     if (dims == 3)
         box_fused_kernel<3><<<grid, kBoxFusedT, 0, st>>>(n, b1, b2, sk, sp, grad, scale, iou, gb1, gb2);
     else

@@ -332,15 +332,6 @@ struct BwdPtSmem {
     FlagLut lut;
 };
 
-__device__ __forceinline__ void cp_async4(void *dst, const void *src)
-{
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void *dst, const void *src)
-{
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-
 template <int K>
 __global__ void __launch_bounds__(kBwdPtThreads, (K == 4) ? DGAL_BWDPT_MINB : DGAL_BWDPT8_MINB)
 paired_bwd_pt_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
