@@ -511,10 +511,10 @@ constexpr int kFused4Threads = DGAL_FUSED4_THREADS, kFused8Threads = DGAL_FUSED8
 #define DGAL_FUSED4_NT 8
 #endif
 #ifndef DGAL_FUSED8_NT
-#define DGAL_FUSED8_NT 4
+#define DGAL_FUSED8_NT 8
 #endif
 #ifndef DGAL_FUSED8_PF
-#define DGAL_FUSED8_PF 0      // K = 8: ring + piece table exceed 48 KB of static shared memory
+#define DGAL_FUSED8_PF 1
 #endif
 
 template <int K>
@@ -535,11 +535,15 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
     constexpr int T = (K == 4) ? kFused4Threads : kFused8Threads;
     constexpr bool PF = (K == 4) ? DGAL_FUSED_PF : DGAL_FUSED8_PF;
     constexpr int NT = !PF ? 1 : (K == 4) ? DGAL_FUSED4_NT : DGAL_FUSED8_NT;
-    __shared__ float pt[(DGAL_FUSED_P2MODE == kP2PiecesSmem) ? 4 * K * T : 1];   // piece table, [slot][thread]
-    // PF: 2-stage per-thread ring [stage][plane][thread][K] + [stage][thread] for dL/dIoU
-    // (each thread copies and reads only its own bytes: no CTA barrier)
-    __shared__ __align__(16) float ring[PF ? 2 * 4 * T * K : 4];
-    __shared__ float gring[PF ? 2 * T : 1];
+    // dynamic shared memory (FusedSmem<K>; K = 8 with the ring exceeds 48 KB):
+    //   pt     piece table [slot][thread] (kP2PiecesSmem)
+    //   ring   PF: 2-stage per-thread ring [stage][plane][thread][K]
+    //   gring  PF: [stage][thread] dL/dIoU
+    // (each thread copies and reads only its own words: no CTA barrier)
+    extern __shared__ __align__(16) float fsm[];
+    float *ring = fsm;
+    float *gring = ring + (PF ? 2 * 4 * T * K : 0);
+    float *pt = gring + (PF ? 2 * T : 0);
     const int tid = threadIdx.x;
     const int64_t k0 = (int64_t)blockIdx.x * (NT * T) + tid;
     auto prefetch = [&](int stage, int64_t k) {
@@ -596,19 +600,44 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
     }
 }
 
+namespace {
+template <int K>
+constexpr size_t fused_smem_bytes()
+{
+    constexpr int T = (K == 4) ? kFused4Threads : kFused8Threads;
+    constexpr bool PF = (K == 4) ? DGAL_FUSED_PF : DGAL_FUSED8_PF;
+    return sizeof(float) * ((PF ? 2 * 4 * T * K + 2 * T : 0) + 4 * K * T);
+}
+template <int K>
+cudaError_t launch_fused_k(int64_t n, const float *x1, const float *y1, const float *x2, const float *y2,
+                           const float *grad, float scale, float *iou, float *gx1, float *gy1, float *gx2,
+                           float *gy2, cudaStream_t st)
+{
+    constexpr int T = (K == 4) ? kFused4Threads : kFused8Threads;
+    constexpr bool PF = (K == 4) ? DGAL_FUSED_PF : DGAL_FUSED8_PF;
+    constexpr int64_t per = (int64_t)(PF ? ((K == 4) ? DGAL_FUSED4_NT : DGAL_FUSED8_NT) : 1) * T;
+    constexpr size_t smem = fused_smem_bytes<K>();
+    static int dev_cached = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != dev_cached) {
+        cudaError_t e = cudaFuncSetAttribute(paired_fused_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        dev_cached = dev;
+    }
+    paired_fused_kernel<K><<<(unsigned)((n + per - 1) / per), T, smem, st>>>(n, x1, y1, x2, y2, grad, scale, iou,
+                                                                               gx1, gy1, gx2, gy2);
+    return cudaGetLastError();
+}
+}  // namespace
+
 cudaError_t launch_paired_fused(int K, int64_t n, const float *x1, const float *y1, const float *x2,
                                 const float *y2, const float *grad, float scale, float *iou, float *gx1,
                                 float *gy1, float *gx2, float *gy2, cudaStream_t st)
 {
-    constexpr int64_t per4 = (int64_t)(DGAL_FUSED_PF ? DGAL_FUSED4_NT : 1) * kFused4Threads;
-    constexpr int64_t per8 = (int64_t)(DGAL_FUSED8_PF ? DGAL_FUSED8_NT : 1) * kFused8Threads;
-    if (K == 4)
-        paired_fused_kernel<4><<<(unsigned)((n + per4 - 1) / per4), kFused4Threads, 0, st>>>(
-            n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2);
-    else
-        paired_fused_kernel<8><<<(unsigned)((n + per8 - 1) / per8), kFused8Threads, 0, st>>>(
-            n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2);
-    return cudaGetLastError();
+    if (K == 4) return launch_fused_k<4>(n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2, st);
+    return launch_fused_k<8>(n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2, st);
 }
 
 }  // namespace dgal
