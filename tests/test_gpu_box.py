@@ -130,6 +130,24 @@ def test_box_fused_matches_oracle_and_split(dims):
     assert torch.equal(h1, k1)
 
 
+@pytest.mark.parametrize("dims", [2, 3])
+@pytest.mark.parametrize("n", [127, 1023, 1025, 8193])
+def test_box_ragged_around_cta_chunks(dims, n):
+    """Forward and fused box kernels: 128 threads x 8 tiles per CTA with the
+    parameter prefetch ring — partial last tile and partial chunk."""
+    b = box_margin_batch(dims, n)
+    check_box_against_oracle(b)
+    B1, B2 = torch.from_numpy(b.b1).to(dev()), torch.from_numpy(b.b2).to(dev())
+    g = torch.from_numpy(b.grad).to(dev())
+    iou, g1, g2 = dgal.box_iou_paired_fused(B1, B2, grad=g)
+    torch.cuda.synchronize()
+    r1, r2 = b.rows64()
+    ref = oracle.box_iou_paired(r1, r2, b.grad.astype(np.float64))
+    assert_iou_close(iou.cpu().numpy(), ref["iou"])
+    assert_grad_close(g1.cpu().numpy().T, ref["gb1"])
+    assert_grad_close(g2.cpu().numpy().T, ref["gb2"])
+
+
 def test_box_autograd_and_loss():
     b = box_margin_batch(3, 2000)
     B1 = torch.from_numpy(b.b1).to(dev()).requires_grad_(True)

@@ -222,6 +222,26 @@ def test_fused_matches_oracle(cfg, n):
         assert_grad_close(got.cpu().numpy().reshape(want.shape), want)
 
 
+@pytest.mark.parametrize("cfg,n", [(3, 1), (3, 127), (3, 1023), (3, 1025), (3, 8193), (4, 129), (4, 1023),
+                                   (4, 1025), (4, 4097)])
+def test_fused_ragged_around_cta_chunks(cfg, n):
+    """The fused kernel's CTA chunk is 128 threads x 8 tiles with the cp.async ring
+    (both K): partial last tile and partial chunk, per-pair and scalar dL/dIoU."""
+    b = margin_batch(cfg, n)
+    x1, y1 = to_dev(b.p1)
+    x2, y2 = to_dev(b.p2)
+    g = torch.from_numpy(b.grad).to(dev())
+    iou, *gr = dgal.iou_paired_fused(x1, y1, x2, y2, grad=g)
+    torch.cuda.synchronize()
+    assert_iou_close(iou.cpu().numpy(), oracle.iou_paired_fwd(b.p1, b.p2)["iou"])
+    for got, want in zip(gr, oracle.iou_paired_bwd(b.p1, b.p2, b.grad)):
+        assert_grad_close(got.cpu().numpy().reshape(want.shape), want)
+    _, *ga = dgal.iou_paired_fused(x1, y1, x2, y2, scale=0.5)
+    _, *gb = dgal.iou_paired_fused(x1, y1, x2, y2, grad=torch.full_like(g, 0.5))
+    for a_, c_ in zip(ga, gb):
+        assert torch.equal(a_, c_)
+
+
 def test_fused_consistent_with_split_and_pairwise():
     b = margin_batch(3, 20_000)
     x1, y1 = to_dev(b.p1)
