@@ -13,8 +13,10 @@
  *    Vertex k of polygon n is (x[n*K + k], y[n*K + k]).  Exactly K vertices per
  *    polygon, convex, counter-clockwise.  K is 4 or 8.
  *  - ALL pointers are DEVICE pointers owned by the caller; the library never
- *    allocates, never frees, keeps no global state and never synchronises the
- *    host ("fix-size allocated memory").  Work is enqueued on `stream`
+ *    allocates, never frees and never synchronises the host ("fix-size
+ *    allocated memory"); its only state is a per-device cache of launch
+ *    attributes (set once per kernel and device, thread-safe, idempotent).
+ *    Work is enqueued on `stream`
  *    (a cudaStream_t; NULL = legacy default stream).
  *  - Inputs are trusted: no CCW/convexity check on the device.
  *    Invalid polygons give unspecified but finite results.

@@ -2,6 +2,7 @@
 // .cu translation units of libdgal.so (not part of the public ABI).
 #pragma once
 
+#include <atomic>
 #include <cassert>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -16,6 +17,36 @@
 #endif
 
 namespace dgal {
+
+// Per-device, per-launcher cache of a launch-configuration value (a kernel's
+// dynamic-shared-memory attribute having been set, a co-resident grid size).
+// The value is a pure function of (device, kernel), so racing first calls just
+// compute it twice; each device has its own slot (one process may drive several
+// GPUs from several threads).  0 = not yet known; a failed computation (<= 0) is
+// not cached.  This is the only state the library keeps.
+constexpr int kMaxDevices = 64;
+struct DeviceCache {
+    std::atomic<int> v[kMaxDevices];
+    template <class F>
+    int get(F compute)
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return compute(dev);
+        int x = v[dev].load(std::memory_order_relaxed);
+        if (x <= 0) {
+            x = compute(dev);
+            if (x > 0) v[dev].store(x, std::memory_order_relaxed);
+        }
+        return x;
+    }
+};
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per device: 1, or -error
+template <class K>
+int set_smem_attr(K kernel, size_t bytes)
+{
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    return e == cudaSuccess ? 1 : -(int)e;
+}
 
 constexpr int kPairedThreads = 256;     // paired kernels: one pair per thread
 

@@ -157,17 +157,14 @@ cudaError_t launch_nms_keep(int64_t n, const uint64_t *mask, int64_t mask_words,
                             uint8_t *status, uint8_t *keep, int32_t *scratch, cudaStream_t st)
 {
     if (scratch) {
-        static int dev_cached = -1, limit = 0;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (dev != dev_cached) {
+        static DeviceCache cache;   // co-resident grid size (-1: no cooperative launch)
+        const int limit = cache.get([&](int dev) {
             int sms = 0, per = 0, coop = 0;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, nms_keep_grid_kernel, kNmsRoundThreads, 0);
-            limit = coop ? sms * (per > 0 ? per : 1) : 0;
-            dev_cached = dev;
-        }
+            return coop ? sms * (per > 0 ? per : 1) : -1;
+        });
         if (limit > 0) {
             const int64_t need = (n + kNmsRoundThreads - 1) / kNmsRoundThreads;
             unsigned grid = (unsigned)(need < limit ? need : limit);

@@ -425,20 +425,17 @@ cudaError_t launch_bwd_k(int64_t n, const float *x1, const float *y1, const floa
                          const float *grad, const uint8_t *nx, const uint8_t *xflags, float *gx1, float *gy1,
                          float *gx2, float *gy2, cudaStream_t st)
 {
-    static int dev_cached = -1, limit = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
     const size_t smem = sizeof(BwdSmem<K>);
-    if (dev != dev_cached) {
-        cudaError_t e = cudaFuncSetAttribute(paired_bwd_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
+    static DeviceCache cache;
+    const int limit = cache.get([&](int dev) {
+        const int a = set_smem_attr(paired_bwd_kernel<K>, smem);
+        if (a <= 0) return a;
         int sms = 0, per = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, paired_bwd_kernel<K>, BwdCfg<K>::threads, smem);
-        limit = sms * (per > 0 ? per : 1);
-        dev_cached = dev;
-    }
+        return sms * (per > 0 ? per : 1);
+    });
+    if (limit <= 0) return (cudaError_t)(-limit);
     constexpr int kTile = BwdCfg<K>::tile;
     const int64_t ntiles = (n + kTile - 1) / kTile;
     const unsigned grid = (unsigned)(ntiles < limit ? ntiles : limit);
@@ -453,16 +450,10 @@ cudaError_t launch_bwd_pt(int64_t n, const float *x1, const float *y1, const flo
                           const float *grad, const uint8_t *nx, const uint8_t *xflags, float *gx1, float *gy1,
                           float *gx2, float *gy2, cudaStream_t st)
 {
-    static int dev_cached = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
     const size_t smem = sizeof(BwdPtSmem<K>);
-    if (dev != dev_cached) {
-        cudaError_t e = cudaFuncSetAttribute(paired_bwd_pt_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        dev_cached = dev;
-    }
+    static DeviceCache cache;
+    const int a = cache.get([&](int) { return set_smem_attr(paired_bwd_pt_kernel<K>, smem); });
+    if (a <= 0) return (cudaError_t)(-a);
     constexpr int64_t per = (int64_t)DGAL_BWDPT_NT * kBwdPtThreads;
     paired_bwd_pt_kernel<K><<<(unsigned)((n + per - 1) / per), kBwdPtThreads, smem, st>>>(
         n, x1, y1, x2, y2, grad, nx, xflags, gx1, gy1, gx2, gy2);
@@ -617,15 +608,9 @@ cudaError_t launch_fused_k(int64_t n, const float *x1, const float *y1, const fl
     constexpr bool PF = (K == 4) ? DGAL_FUSED_PF : DGAL_FUSED8_PF;
     constexpr int64_t per = (int64_t)(PF ? ((K == 4) ? DGAL_FUSED4_NT : DGAL_FUSED8_NT) : 1) * T;
     constexpr size_t smem = fused_smem_bytes<K>();
-    static int dev_cached = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev != dev_cached) {
-        cudaError_t e = cudaFuncSetAttribute(paired_fused_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        dev_cached = dev;
-    }
+    static DeviceCache cache;
+    const int a = cache.get([&](int) { return set_smem_attr(paired_fused_kernel<K>, smem); });
+    if (a <= 0) return (cudaError_t)(-a);
     paired_fused_kernel<K><<<(unsigned)((n + per - 1) / per), T, smem, st>>>(n, x1, y1, x2, y2, grad, scale, iou,
                                                                                gx1, gy1, gx2, gy2);
     return cudaGetLastError();

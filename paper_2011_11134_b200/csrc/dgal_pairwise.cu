@@ -210,24 +210,16 @@ cudaError_t launch_pairwise(int K, int64_t n_rows, const float *rx, const float 
                     (unsigned)((m + kPwTileCols - 1) / kPwTileCols));
     if (K == 4) {
         const size_t sm = sizeof(PwSmem<4>);
-        static int attr = -1;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (attr != dev) {
-            cudaFuncSetAttribute(pairwise_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            attr = dev;
-        }
+        static DeviceCache cache;
+        const int a = cache.get([&](int) { return set_smem_attr(pairwise_kernel<4>, sm); });
+        if (a <= 0) return (cudaError_t)(-a);
         pairwise_kernel<4><<<grid, kPwThreads, sm, st>>>(n_rows, rx, ry, m, cx, cy, row_offset, iou, thr,
                                                          mask, mask_words, nbr_count, nbr_idx, cap);
     } else {
         const size_t sm = sizeof(PwSmem<8>);
-        static int attr = -1;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (attr != dev) {
-            cudaFuncSetAttribute(pairwise_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            attr = dev;
-        }
+        static DeviceCache cache;
+        const int a = cache.get([&](int) { return set_smem_attr(pairwise_kernel<8>, sm); });
+        if (a <= 0) return (cudaError_t)(-a);
         pairwise_kernel<8><<<grid, kPwThreads, sm, st>>>(n_rows, rx, ry, m, cx, cy, row_offset, iou, thr,
                                                          mask, mask_words, nbr_count, nbr_idx, cap);
     }
