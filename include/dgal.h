@@ -100,7 +100,8 @@ dgal_status dgal_iou_paired_bwd(int K, int64_t n,
  * the paper's; this is its fusion).  dL/dIoU of pair k is grad_iou[k] when
  * grad_iou != NULL, else grad_scale.  iou [n] nullable; gx1, gy1, gx2, gy2
  * [n * K] overwritten (same values as dgal_iou_paired_fwd + _bwd up to rounding;
- * IoU bit-identical to dgal_iou_pairwise).
+ * IoU bit-identical to dgal_iou_pairwise).  Alignment: planes and gradient
+ * planes 16 B, grad_iou and iou 4 B (DGAL_ERR_MISALIGNED otherwise).
  */
 dgal_status dgal_iou_paired_fused(int K, int64_t n,
                                   const float *x1, const float *y1,

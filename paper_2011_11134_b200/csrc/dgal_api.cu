@@ -64,7 +64,8 @@ dgal_status dgal_iou_paired_fused(int K, int64_t n, const float *x1, const float
     if (n == 0) return DGAL_OK;
     if (!x1 || !y1 || !x2 || !y2 || !gx1 || !gy1 || !gx2 || !gy2) return DGAL_ERR_INVALID_ARG;
     if (!aligned(x1, 16) || !aligned(y1, 16) || !aligned(x2, 16) || !aligned(y2, 16) ||
-        !aligned(gx1, 16) || !aligned(gy1, 16) || !aligned(gx2, 16) || !aligned(gy2, 16))
+        !aligned(gx1, 16) || !aligned(gy1, 16) || !aligned(gx2, 16) || !aligned(gy2, 16) ||
+        (grad_iou && !aligned(grad_iou, 4)) || (iou && !aligned(iou, 4)))
         return DGAL_ERR_MISALIGNED;
     return from_cuda(dgal::launch_paired_fused(K, n, x1, y1, x2, y2, grad_iou, grad_scale, iou, gx1, gy1, gx2,
                                                gy2, as_cuda(stream)));

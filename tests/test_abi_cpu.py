@@ -65,6 +65,13 @@ def test_host_side_validation_without_gpu():
     assert L.dgal_iou_paired_fwd(4, 8, P(a + 4), P(a), P(a), P(a), P(a), P(a), P(a), None) == 3
     # misaligned xflags for K=8 (needs 16 B)
     assert L.dgal_iou_paired_fwd(8, 8, P(a), P(a), P(a), P(a), P(a), P(a), P(a + 8), None) == 3
+    # fused: misaligned dL/dIoU or IoU output (4 B), misaligned gradient plane (16 B)
+    assert L.dgal_iou_paired_fused(4, 8, P(a), P(a), P(a), P(a), P(a + 2), ctypes.c_float(1.0), None,
+                                   P(a), P(a), P(a), P(a), None) == 3
+    assert L.dgal_iou_paired_fused(4, 8, P(a), P(a), P(a), P(a), None, ctypes.c_float(1.0), P(a + 1),
+                                   P(a), P(a), P(a), P(a), None) == 3
+    assert L.dgal_iou_paired_fused(8, 8, P(a), P(a), P(a), P(a), None, ctypes.c_float(1.0), None,
+                                   P(a), P(a + 8), P(a), P(a), None) == 3
     # n == 0 is a no-op
     assert L.dgal_iou_paired_fwd(4, 0, None, None, None, None, None, None, None, None) == 0
     assert L.dgal_iou_paired_bwd(4, 0, *([None] * 11), None) == 0
