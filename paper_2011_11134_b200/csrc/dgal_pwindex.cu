@@ -274,10 +274,19 @@ pw_candidates(int64_t n_rows, const float *__restrict__ rx, const float *__restr
 
     auto evaluate = [&](int64_t rr, int32_t c) {
         Poly<K> P, Q;
+        // 16-byte loads (planes are 16-byte aligned, include/dgal.h): K/4 per plane;
+        // (cached loads: a row's polygon serves all its candidates, a column's its neighbours)
+        DGAL_ASSERT(rr >= 0 && rr < n_rows && c >= 0 && c < m);
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            P.x[k] = __ldg(rx + rr * K + k); P.y[k] = __ldg(ry + rr * K + k);
-            Q.x[k] = __ldg(cxg + (int64_t)c * K + k); Q.y[k] = __ldg(cyg + (int64_t)c * K + k);
+        for (int q = 0; q < K / 4; ++q) {
+            const float4 a = __ldg(reinterpret_cast<const float4 *>(rx + rr * K) + q);
+            const float4 b = __ldg(reinterpret_cast<const float4 *>(ry + rr * K) + q);
+            const float4 u = __ldg(reinterpret_cast<const float4 *>(cxg + (int64_t)c * K) + q);
+            const float4 w = __ldg(reinterpret_cast<const float4 *>(cyg + (int64_t)c * K) + q);
+            P.x[4 * q] = a.x; P.x[4 * q + 1] = a.y; P.x[4 * q + 2] = a.z; P.x[4 * q + 3] = a.w;
+            P.y[4 * q] = b.x; P.y[4 * q + 1] = b.y; P.y[4 * q + 2] = b.z; P.y[4 * q + 3] = b.w;
+            Q.x[4 * q] = u.x; Q.x[4 * q + 1] = u.y; Q.x[4 * q + 2] = u.z; Q.x[4 * q + 3] = u.w;
+            Q.y[4 * q] = w.x; Q.y[4 * q + 1] = w.y; Q.y[4 * q + 2] = w.z; Q.y[4 * q + 3] = w.w;
         }
         const float ox = P.x[0], oy = P.y[0];
 #pragma unroll
@@ -287,7 +296,6 @@ pw_candidates(int64_t n_rows, const float *__restrict__ rx, const float *__restr
         }
         P.x[0] = 0.f;   // exact for finite input; lets the compiler fold it
         P.y[0] = 0.f;
-        DGAL_ASSERT(rr >= 0 && rr < n_rows && c >= 0 && c < m);
         const float v = iou_fwd<K, false>(P, Q).iou;
         if (iou && v != 0.f) iou[rr * m + c] = v;
         const int64_t grow = row_offset + rr;
