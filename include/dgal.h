@@ -23,7 +23,9 @@
  *  - Alignment: every x/y plane and gradient plane must be 16-byte aligned
  *    (float4 loads/stores); xflags must be 2K-byte aligned (8 B for K=4, 16 B
  *    for K=8); uint64 masks 8-byte aligned.  Violations -> DGAL_ERR_MISALIGNED.
- *  - n == 0 (or m == 0) is a no-op returning DGAL_OK.
+ *  - n == 0 (or m == 0) is a no-op returning DGAL_OK; the one exception is
+ *    dgal_iou_pairwise with n_rows > 0 and m == 0, which still zeroes
+ *    nbr_count (when given): no row has a suppressor.
  *  - Errors are detected on the host before launch (nothing is enqueued); a
  *    launch failure (cudaGetLastError) returns DGAL_ERR_CUDA.  Asynchronous
  *    device faults surface at the caller's next synchronisation.

@@ -128,7 +128,12 @@ dgal_status dgal_iou_pairwise(int K, int64_t n_rows, const float *row_x, const f
 {
     if (K != 4 && K != 8) return DGAL_ERR_UNSUPPORTED_K;
     if (n_rows < 0 || m < 0 || row_offset < 0) return DGAL_ERR_INVALID_ARG;
-    if (n_rows == 0 || m == 0) return DGAL_OK;
+    if (n_rows == 0) return DGAL_OK;
+    if (m == 0) {   // no columns: every row has zero suppressors (nbr_count is an output)
+        if ((nbr_count == nullptr) != (nbr_idx == nullptr)) return DGAL_ERR_INVALID_ARG;
+        if (!nbr_count) return DGAL_OK;
+        return from_cuda(cudaMemsetAsync(nbr_count, 0, sizeof(int32_t) * (size_t)n_rows, as_cuda(stream)));
+    }
     if (!row_x || !row_y || !col_x || !col_y) return DGAL_ERR_INVALID_ARG;
     if (!iou && !mask) return DGAL_ERR_INVALID_ARG;                 // nothing to compute
     if (m > (int64_t)65535 * dgal::kPwTileCols) return DGAL_ERR_INVALID_ARG;

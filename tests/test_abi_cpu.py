@@ -94,6 +94,11 @@ def test_host_side_validation_without_gpu():
     assert L.dgal_iou_pairwise(*args, P(a), 0.5, None, 0, P(a), P(a), 4, None, 0, None) == 1
     assert L.dgal_iou_pairwise(*args, P(a), 0.5, None, 0, None, None, 0, P(a), 16, None) == 1
     assert L.dgal_pairwise_workspace_bytes(100_000) > 100_000 * 24
+    # no columns: a no-op without lists, half-given lists rejected (with lists it zeroes nbr_count: GPU test)
+    assert L.dgal_iou_pairwise(*[4, 8, None, None, 0, None, None, 0], None, 0.5, None, 0, None, None, 0, None, 0,
+                               None) == 0
+    assert L.dgal_iou_pairwise(*[4, 8, None, None, 0, None, None, 0], None, 0.5, None, 0, P(a), None, 0, None, 0,
+                               None) == 1
     # NMS: row block outside the problem
     assert L.dgal_nms_round(10, 8, 4, P(a), 1, None, None, 0, P(a), P(a), None) == 1
     assert L.dgal_nms_keep(0, None, 0, None, None, 0, None, None, None, None) == 0

@@ -217,3 +217,31 @@ def test_keep_grid_equals_single_cta_and_oracle():
     assert torch.equal(kg, kc) and torch.equal(kg, kl)
     ref = oracle.nms_scan_mask(mask.cpu().numpy().view(np.uint64))
     assert np.array_equal(kg.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("indexed", [True, False])
+@pytest.mark.parametrize("nr,m", [(0, 5), (5, 0), (0, 0), (1, 1)])
+def test_empty_and_single_shapes(nr, m, indexed):
+    """Empty row or column sets (include/dgal.h: n_rows == 0 is a no-op; m == 0
+    still zeroes nbr_count) and the 1 x 1 matrix (IoU of a polygon with itself
+    is 1, no mask bit on the diagonal); then the keep of the empty / single set."""
+    p = synth.gen_cfg5_scene(n_objects=1, per_object=max(nr, m, 1), seed=11).polys
+    rows, cols = p.take(np.arange(nr)), p.take(np.arange(m))
+    rx, ry = to_dev(rows)
+    cx, cy = to_dev(cols)
+    K = p.K
+    # poison the outputs: whatever the library must write is overwritten
+    out = (torch.full((nr, m), -7.0, device=dev()), torch.full((nr, (m + 63) // 64), -1, dtype=torch.int64,
+                                                             device=dev()),
+           torch.full((nr,), 123, dtype=torch.int32, device=dev()), torch.full((nr, 4), -1, dtype=torch.int32,
+                                                                             device=dev()))
+    iou, mask, cnt, idx = dgal.iou_pairwise(rx, ry, cx, cy, K=K, thr=0.5, nbr_cap=4, out=out, indexed=indexed)
+    torch.cuda.synchronize()
+    assert torch.all(cnt == 0)
+    if nr and m:
+        assert iou.cpu().numpy().tolist() == [[1.0]]
+        assert int(mask[0, 0]) == 0
+    if nr == m:   # the keep of a square (self) mask
+        keep = dgal.nms_keep(mask, cnt, idx)
+        torch.cuda.synchronize()
+        assert keep.shape == (nr,) and torch.all(keep == 1)
