@@ -245,3 +245,23 @@ def test_empty_and_single_shapes(nr, m, indexed):
         keep = dgal.nms_keep(mask, cnt, idx)
         torch.cuda.synchronize()
         assert keep.shape == (nr,) and torch.all(keep == 1)
+
+
+def test_pairwise_nms_sharded_single_rank():
+    """dist.pairwise_nms_sharded without a process group (world 1): the whole
+    problem is rank 0's row block; its keep equals the single-GPU keep and the
+    oracle's greedy scan of the mask, its local IoU the full matrix."""
+    from paper_2011_11134_b200.dist import pairwise_nms_sharded
+    sc = synth.gen_cfg5_scene(n_objects=60, per_object=50, seed=21)
+    p = sc.polys
+    x, y = to_dev(p)
+    keep, iou, (lo, hi), rounds = pairwise_nms_sharded(x, y, thr=sc.thr, want_iou=True)
+    iou1, mask, cnt, idx = dgal.iou_pairwise(x, y, x, y, thr=sc.thr, nbr_cap=64)
+    keep1 = dgal.nms_keep(mask, cnt, idx)
+    torch.cuda.synchronize()
+    assert (lo, hi) == (0, p.n) and rounds >= 1
+    assert torch.equal(iou, iou1)
+    k = keep.cpu().numpy()
+    assert np.array_equal(k, keep1.cpu().numpy())
+    assert np.array_equal(k, oracle.nms_scan_mask(mask.cpu().numpy().view(np.uint64)))
+    assert 0 < k.sum() < p.n
