@@ -34,8 +34,15 @@
  *
  * Flag bytes xflags (R2, following S:102-103): FromP1(i) = 0x40|i, FromP2(j) =
  * 0x80|j, Cross(i,j) = 0xC0|i<<3|j (p1 edge i x p2 edge j), padding 0x00.  The
- * nx valid bytes list the intersection's vertices counter-clockwise, rotated to
- * start at the smallest byte (R3).  nx == 0 <=> empty intersection (IoU 0).
+ * nx valid bytes list the intersection's vertices counter-clockwise,
+ * starting at the first vertex met when walking p1's boundary counter-clockwise
+ * from p1's vertex 0 (R3): a vertex on p1 edge i sits at boundary position
+ * i + t (t in [0, 1) its parameter along that edge; FromP1(i) is t = 0), and the
+ * sequence starts at the smallest position.  When no vertex of the intersection
+ * lies on p1's boundary (p2 strictly inside p1) it is FromP2(0), FromP2(1), ...
+ * Example (offset unit squares p1 = [0,1]^2, p2 = p1 + (0.5, 0.5)):
+ * C8 42 D3 80 = Cross(1,0) FromP1(2) Cross(2,3) FromP2(0) — NOT sorted by byte
+ * value.  nx == 0 <=> empty intersection (IoU 0).
  */
 #ifndef DGAL_H_
 #define DGAL_H_
@@ -101,16 +108,37 @@ dgal_status dgal_iou_paired_bwd(int K, int64_t n,
  * intervals — no nx/xflags round trip through memory (the split API above is
  * the paper's; this is its fusion).  dL/dIoU of pair k is grad_iou[k] when
  * grad_iou != NULL, else grad_scale.  iou [n] nullable; gx1, gy1, gx2, gy2
- * [n * K] overwritten (same values as dgal_iou_paired_fwd + _bwd up to rounding;
- * IoU bit-identical to dgal_iou_pairwise).  Alignment: planes and gradient
- * planes 16 B, grad_iou and iou 4 B (DGAL_ERR_MISALIGNED otherwise).
+ * [n * K] overwritten.  Alignment: planes and gradient planes 16 B, grad_iou
+ * and iou 4 B, workspace 16 B (DGAL_ERR_MISALIGNED otherwise).
+ *
+ * Exactness (north_star tolerances on every input, like the split path): the
+ * one-pass float arithmetic is not accurate enough for two rare kinds of pair —
+ * a nearly parallel (p1 edge, p2 edge) pair (|sin| < 2^-9: float crossing
+ * parameters are conditioned by 1/sin) and a thin pair (R^2 > 8 A_u, R the
+ * pair's extent: the float area sum is conditioned by R^2 / A_u).  The first
+ * kernel marks them in the refine mask `workspace` (one bit per pair) and a
+ * second kernel, enqueued right after it, recomputes exactly those pairs with
+ * the split path's arithmetic (dgal_iou_paired_fwd + _bwd: crossings refined in
+ * double, thin areas in double), overwriting their iou and gradients.  Unmarked
+ * pairs: IoU bit-identical to dgal_iou_pairwise, gradients equal to the split
+ * path's up to rounding.
+ *   workspace        >= dgal_fused_workspace_bytes(n) bytes of device memory,
+ *                    ZERO-FILLED by the caller before its first use; every call
+ *                    leaves it zero-filled again (the refine pass clears the bits
+ *                    it consumes), so it is reused across calls without clearing.
+ *                    One workspace per stream: calls that may run concurrently
+ *                    need separate workspaces.  NULL or too small ->
+ *                    DGAL_ERR_INVALID_ARG.
  */
+size_t dgal_fused_workspace_bytes(int64_t n);   /* 4 * ceil(n / 32), rounded up to 8 */
+
 dgal_status dgal_iou_paired_fused(int K, int64_t n,
                                   const float *x1, const float *y1,
                                   const float *x2, const float *y2,
                                   const float *grad_iou, float grad_scale,
                                   float *iou,
                                   float *gx1, float *gy1, float *gx2, float *gy2,
+                                  void *workspace, size_t workspace_bytes,
                                   dgal_stream stream);
 
 /*
@@ -149,12 +177,15 @@ dgal_status dgal_box_iou_paired_bwd(int dims, int layout, int64_t n,
                                     dgal_stream stream);
 
 /* fused forward + backward (f2 on boxes): dL/dIoU = grad_iou[k], or grad_scale
- * when grad_iou == NULL; iou nullable. */
+ * when grad_iou == NULL; iou nullable; workspace: the refine mask as for
+ * dgal_iou_paired_fused (dgal_fused_workspace_bytes(n), zero-filled once; the
+ * marked pairs are redone with the box split path's arithmetic). */
 dgal_status dgal_box_iou_paired_fused(int dims, int layout, int64_t n,
                                       const float *b1, const float *b2,
                                       const float *grad_iou, float grad_scale,
                                       float *iou,
                                       float *grad_b1, float *grad_b2,
+                                      void *workspace, size_t workspace_bytes,
                                       dgal_stream stream);
 
 /*

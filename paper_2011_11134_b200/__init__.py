@@ -20,7 +20,7 @@ import torch
 from ._lib import DgalError, call, lib  # noqa: F401
 
 __all__ = ["iou_paired_fwd", "iou_paired_bwd", "iou_paired_fused", "iou_paired", "iou_paired_backward", "PolyIoULoss",
-           "box_iou_paired_fwd", "box_iou_paired_bwd", "box_iou_paired_fused", "BoxIoU", "BoxIoULoss", "iou_pairwise", "pairwise_workspace", "nms_round", "nms_keep",
+           "box_iou_paired_fwd", "box_iou_paired_bwd", "box_iou_paired_fused", "BoxIoU", "BoxIoULoss", "iou_pairwise", "pairwise_workspace", "fused_workspace", "nms_round", "nms_keep",
            "nms", "PolyIoU", "DgalError", "build_info"]
 
 
@@ -32,14 +32,28 @@ def _stream(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
-def _plane(t: torch.Tensor, name: str) -> torch.Tensor:
+def _plane(t: torch.Tensor, name: str, dtype=torch.float32, numel: int | None = None,
+           device=None) -> torch.Tensor:
+    """Validate one tensor handed to the C ABI: a contiguous CUDA tensor of `dtype`
+    (on `device`, with `numel` elements when given).  The ABI receives raw pointers
+    and cannot check sizes, so a short buffer here would be an out-of-bounds device
+    access, not an error: every input and out= tensor goes through this."""
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError(f"{name}: expected a CUDA tensor (there is no CPU path)")
-    if t.dtype != torch.float32:
-        raise TypeError(f"{name}: expected float32, got {t.dtype}")
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
     if not t.is_contiguous():
         raise ValueError(f"{name}: must be contiguous")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name}: on {t.device}, expected {device} (all tensors of a call share one device)")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name}: {t.numel()} elements, expected {numel}")
     return t
+
+
+def _planes(K, n, dev, **ts):
+    for nm, t in ts.items():
+        _plane(t, nm, numel=n * K, device=dev)
 
 
 def _K_n(x: torch.Tensor, K: int | None):
@@ -57,19 +71,41 @@ def _ptr(t):
     return None if t is None else t.data_ptr()
 
 
+_FUSED_WS = {}
+
+
+def fused_workspace(n: int, device=None, stream=None) -> torch.Tensor:
+    """Refine mask of the fused kernels (dgal_fused_workspace_bytes(n) bytes, zero-filled
+    once; every call leaves it zero-filled).  Cached per (device, stream) — one
+    workspace per stream, as include/dgal.h requires — and grown on demand."""
+    dev = torch.device(device or "cuda")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    st = stream if stream is not None else _stream(dev)
+    need = int(lib().dgal_fused_workspace_bytes(int(n)))
+    ws = _FUSED_WS.get((dev, st))
+    if ws is None or ws.numel() < need:
+        ws = torch.zeros(max(need, 16), dtype=torch.uint8, device=dev)
+        _FUSED_WS[(dev, st)] = ws
+    return ws
+
+
 def iou_paired_fwd(x1, y1, x2, y2, K: int | None = None, out=None):
     """Forward IoU of n pairs (dgal_iou_paired_fwd).  Returns (iou f32[n], nx u8[n],
     xflags u8[n, 2K]); `out` may supply those three tensors."""
-    for t, nm in ((x1, "x1"), (y1, "y1"), (x2, "x2"), (y2, "y2")):
-        _plane(t, nm)
+    _plane(x1, "x1")
     K, n = _K_n(x1, K)
     dev = x1.device
+    _planes(K, n, dev, x1=x1, y1=y1, x2=x2, y2=y2)
     if out is None:
         iou = torch.empty(n, dtype=torch.float32, device=dev)
         nx = torch.empty(n, dtype=torch.uint8, device=dev)
         xf = torch.empty((n, 2 * K), dtype=torch.uint8, device=dev)
     else:
         iou, nx, xf = out
+        _plane(iou, "iou", numel=n, device=dev)
+        _plane(nx, "nx", torch.uint8, n, dev)
+        _plane(xf, "xflags", torch.uint8, 2 * K * n, dev)
     call("dgal_iou_paired_fwd", K, n, _ptr(x1), _ptr(y1), _ptr(x2), _ptr(y2), _ptr(iou), _ptr(nx),
          _ptr(xf), _stream(dev))
     return iou, nx, xf
@@ -77,33 +113,44 @@ def iou_paired_fwd(x1, y1, x2, y2, K: int | None = None, out=None):
 
 def iou_paired_bwd(x1, y1, x2, y2, grad_iou, nx, xflags, K: int | None = None, out=None):
     """iou_grad (dgal_iou_paired_bwd): returns (gx1, gy1, gx2, gy2), each shaped like x1."""
-    for t, nm in ((x1, "x1"), (y1, "y1"), (x2, "x2"), (y2, "y2"), (grad_iou, "grad_iou")):
-        _plane(t, nm)
+    _plane(x1, "x1")
     K, n = _K_n(x1, K)
+    dev = x1.device
+    _planes(K, n, dev, x1=x1, y1=y1, x2=x2, y2=y2)
+    _plane(grad_iou, "grad_iou", numel=n, device=dev)
+    _plane(nx, "nx", torch.uint8, n, dev)
+    _plane(xflags, "xflags", torch.uint8, 2 * K * n, dev)
     if out is None:
         out = tuple(torch.empty_like(x1) for _ in range(4))
     gx1, gy1, gx2, gy2 = out
+    _planes(K, n, dev, gx1=gx1, gy1=gy1, gx2=gx2, gy2=gy2)
     call("dgal_iou_paired_bwd", K, n, _ptr(x1), _ptr(y1), _ptr(x2), _ptr(y2), _ptr(grad_iou), _ptr(nx),
          _ptr(xflags), _ptr(gx1), _ptr(gy1), _ptr(gx2), _ptr(gy2), _stream(x1.device))
     return gx1, gy1, gx2, gy2
 
 
 def iou_paired_fused(x1, y1, x2, y2, grad=None, scale: float = 1.0, K: int | None = None, out=None,
-                     want_iou: bool = True):
+                     want_iou: bool = True, workspace: torch.Tensor | None = None):
     """Fused loss forward + backward (dgal_iou_paired_fused): dL/dIoU = grad[k] (a
-    CUDA float tensor [n]) or the scalar `scale`.  Returns (iou | None, gx1, gy1, gx2, gy2)."""
-    for t, nm in ((x1, "x1"), (y1, "y1"), (x2, "x2"), (y2, "y2")):
-        _plane(t, nm)
-    if grad is not None:
-        _plane(grad, "grad")
+    CUDA float tensor [n]) or the scalar `scale`.  Returns (iou | None, gx1, gy1, gx2, gy2).
+    workspace: the refine mask (fused_workspace(n), cached per stream when omitted)."""
+    _plane(x1, "x1")
     K, n = _K_n(x1, K)
+    dev = x1.device
+    _planes(K, n, dev, x1=x1, y1=y1, x2=x2, y2=y2)
+    if grad is not None:
+        _plane(grad, "grad", numel=n, device=dev)
     if out is None:
-        iou = torch.empty(n, dtype=torch.float32, device=x1.device) if want_iou else None
+        iou = torch.empty(n, dtype=torch.float32, device=dev) if want_iou else None
         g4 = tuple(torch.empty_like(x1) for _ in range(4))
     else:
         iou, g4 = out[0], out[1:]
+    if iou is not None:
+        _plane(iou, "iou", numel=n, device=dev)
+    _planes(K, n, dev, gx1=g4[0], gy1=g4[1], gx2=g4[2], gy2=g4[3])
+    ws = fused_workspace(n, dev) if workspace is None else _plane(workspace, "workspace", torch.uint8, device=dev)
     call("dgal_iou_paired_fused", K, n, _ptr(x1), _ptr(y1), _ptr(x2), _ptr(y2), _ptr(grad), float(scale),
-         _ptr(iou), *[_ptr(t) for t in g4], _stream(x1.device))
+         _ptr(iou), *[_ptr(t) for t in g4], _ptr(ws), ws.numel(), _stream(dev))
     return (iou, *g4)
 
 
@@ -137,7 +184,7 @@ def _box_args(b1, b2, layout):
     if layout not in _LAYOUT:
         raise ValueError("layout must be 'planes' or 'rows'")
     _plane(b1, "b1")
-    _plane(b2, "b2")
+    _plane(b2, "b2", device=b1.device)
     if b1.dim() != 2 or b1.shape != b2.shape:
         raise ValueError("b1, b2 must be 2-D tensors of the same shape")
     P, n = (b1.shape[0], b1.shape[1]) if layout == "planes" else (b1.shape[1], b1.shape[0])
@@ -155,6 +202,10 @@ def box_iou_paired_fwd(b1, b2, layout: str = "planes", out=None):
         out = (torch.empty(n, dtype=torch.float32, device=dev), torch.empty(n, dtype=torch.uint8, device=dev),
                torch.empty(n, 8, dtype=torch.uint8, device=dev))
     iou, nx, xf = out
+    dev = b1.device
+    _plane(iou, "iou", numel=n, device=dev)
+    _plane(nx, "nx", torch.uint8, n, dev)
+    _plane(xf, "xflags", torch.uint8, 8 * n, dev)
     call("dgal_box_iou_paired_fwd", dims, lay, n, _ptr(b1), _ptr(b2), _ptr(iou), _ptr(nx), _ptr(xf),
          _stream(b1.device))
     return iou, nx, xf
@@ -164,27 +215,38 @@ def box_iou_paired_bwd(b1, b2, grad_iou, nx, xflags, layout: str = "planes", out
     """dL/d(box parameters) from dL/dIoU through the recorded nx / xflags
     (dgal_box_iou_paired_bwd).  Returns (grad_b1, grad_b2) shaped like b1, b2."""
     dims, lay, n = _box_args(b1, b2, layout)
-    _plane(grad_iou, "grad_iou")
+    dev = b1.device
+    _plane(grad_iou, "grad_iou", numel=n, device=dev)
+    _plane(nx, "nx", torch.uint8, n, dev)
+    _plane(xflags, "xflags", torch.uint8, 8 * n, dev)
     if out is None:
         out = (torch.empty_like(b1), torch.empty_like(b2))
+    _plane(out[0], "grad_b1", numel=b1.numel(), device=dev)
+    _plane(out[1], "grad_b2", numel=b1.numel(), device=dev)
     call("dgal_box_iou_paired_bwd", dims, lay, n, _ptr(b1), _ptr(b2), _ptr(grad_iou), _ptr(nx), _ptr(xflags),
          _ptr(out[0]), _ptr(out[1]), _stream(b1.device))
     return out
 
 
 def box_iou_paired_fused(b1, b2, grad=None, scale: float = 1.0, layout: str = "planes", out=None,
-                         want_iou: bool = True):
+                         want_iou: bool = True, workspace: torch.Tensor | None = None):
     """Fused forward + backward on boxes (dgal_box_iou_paired_fused).  Returns
-    (iou | None, grad_b1, grad_b2)."""
+    (iou | None, grad_b1, grad_b2); workspace as for iou_paired_fused."""
     dims, lay, n = _box_args(b1, b2, layout)
+    dev = b1.device
     if grad is not None:
-        _plane(grad, "grad")
+        _plane(grad, "grad", numel=n, device=dev)
     if out is None:
-        iou = torch.empty(n, dtype=torch.float32, device=b1.device) if want_iou else None
+        iou = torch.empty(n, dtype=torch.float32, device=dev) if want_iou else None
         out = (iou, torch.empty_like(b1), torch.empty_like(b2))
     iou, g1, g2 = out
+    if iou is not None:
+        _plane(iou, "iou", numel=n, device=dev)
+    _plane(g1, "grad_b1", numel=b1.numel(), device=dev)
+    _plane(g2, "grad_b2", numel=b1.numel(), device=dev)
+    ws = fused_workspace(n, dev) if workspace is None else _plane(workspace, "workspace", torch.uint8, device=dev)
     call("dgal_box_iou_paired_fused", dims, lay, n, _ptr(b1), _ptr(b2), _ptr(grad), float(scale), _ptr(iou),
-         _ptr(g1), _ptr(g2), _stream(b1.device))
+         _ptr(g1), _ptr(g2), _ptr(ws), ws.numel(), _stream(dev))
     return iou, g1, g2
 
 
@@ -238,14 +300,27 @@ def iou_pairwise(rx, ry, cx, cy, K: int | None = None, row_offset: int = 0, thr:
      nbr_idx i32[nr, nbr_cap] | None).  mask/nbr semantics: include/dgal.h.
     indexed=True uses the grid-indexed path (a workspace is allocated unless given),
     indexed=False the tiled sweep."""
-    for t, nm in ((rx, "rx"), (ry, "ry"), (cx, "cx"), (cy, "cy")):
-        _plane(t, nm)
+    _plane(rx, "rx")
+    _plane(cx, "cx", device=rx.device)
     K, nr = _K_n(rx, K)
     _, m = _K_n(cx, K)
     dev = rx.device
+    _planes(K, nr, dev, rx=rx, ry=ry)
+    _planes(K, m, dev, cx=cx, cy=cy)
     words = (m + 63) // 64
     if out is not None:
         iou, mask, cnt, idx = out
+        if iou is not None:
+            _plane(iou, "iou", numel=nr * m, device=dev)
+        if mask is not None:
+            _plane(mask, "mask", torch.int64, nr * words, dev)
+        if (cnt is None) != (idx is None):
+            raise ValueError("nbr_count and nbr_idx go together")
+        if cnt is not None:
+            _plane(cnt, "nbr_count", torch.int32, nr, dev)
+            if idx.dim() != 2 or idx.shape[0] != nr:
+                raise ValueError(f"nbr_idx: expected shape [{nr}, cap], got {tuple(idx.shape)}")
+            _plane(idx, "nbr_idx", torch.int32, device=dev)
     else:
         iou = torch.empty((nr, m), dtype=torch.float32, device=dev) if want_iou else None
         mask = torch.empty((nr, words), dtype=torch.int64, device=dev) if want_mask else None
@@ -253,6 +328,11 @@ def iou_pairwise(rx, ry, cx, cy, K: int | None = None, row_offset: int = 0, thr:
         idx = torch.empty((nr, nbr_cap), dtype=torch.int32, device=dev) if nbr_cap > 0 else None
     if indexed and workspace is None:
         workspace = pairwise_workspace(m, dev)
+    if indexed:
+        _plane(workspace, "workspace", torch.uint8, device=dev)
+        need = int(lib().dgal_pairwise_workspace_bytes(int(m)))
+        if workspace.numel() < need:
+            raise ValueError(f"workspace: {workspace.numel()} bytes, need {need}")
     ws = workspace if indexed else None
     call("dgal_iou_pairwise", K, nr, _ptr(rx), _ptr(ry), m, _ptr(cx), _ptr(cy), int(row_offset), _ptr(iou),
          float(thr), _ptr(mask), words if mask is not None else 0, _ptr(cnt), _ptr(idx),
@@ -261,10 +341,32 @@ def iou_pairwise(rx, ry, cx, cy, K: int | None = None, row_offset: int = 0, thr:
     return iou, mask, cnt, idx
 
 
+def _nbr_check(nbr_count, nbr_idx, n_rows, dev) -> int:
+    """Validate the optional suppressor lists; returns their capacity (0 if absent)."""
+    if nbr_count is None and nbr_idx is None:
+        return 0
+    if (nbr_count is None) != (nbr_idx is None):
+        raise ValueError("nbr_count and nbr_idx go together")
+    _plane(nbr_count, "nbr_count", torch.int32, n_rows, dev)
+    _plane(nbr_idx, "nbr_idx", torch.int32, device=dev)
+    if nbr_idx.dim() != 2 or nbr_idx.shape[0] != n_rows:
+        raise ValueError(f"nbr_idx: expected shape [{n_rows}, cap], got {tuple(nbr_idx.shape)}")
+    return nbr_idx.shape[1]
+
+
 def nms_round(n_total: int, row_offset: int, mask, nbr_count, nbr_idx, status, undecided):
     """One parallel NMS round over this rank's rows (dgal_nms_round)."""
+    _plane(mask, "mask", torch.int64)
+    dev = mask.device
     n_rows = mask.shape[0]
-    cap = nbr_idx.shape[1] if nbr_idx is not None else 0
+    if mask.dim() != 2 or mask.shape[1] != (n_total + 63) // 64:
+        raise ValueError(f"mask: expected shape [n_rows, {(n_total + 63) // 64}], got {tuple(mask.shape)}")
+    cap = _nbr_check(nbr_count, nbr_idx, n_rows, dev)
+    _plane(status, "status", torch.uint8, device=dev)
+    if status.numel() < n_total or row_offset < 0 or row_offset + n_rows > status.numel():
+        raise ValueError(f"status: {status.numel()} entries for n_total {n_total}, rows "
+                         f"[{row_offset}, {row_offset + n_rows})")
+    _plane(undecided, "undecided", torch.int32, 1, dev)
     call("dgal_nms_round", int(n_total), n_rows, int(row_offset), _ptr(mask), mask.shape[1], _ptr(nbr_count),
          _ptr(nbr_idx), cap, _ptr(status), _ptr(undecided), _stream(mask.device))
 
@@ -272,11 +374,16 @@ def nms_round(n_total: int, row_offset: int, mask, nbr_count, nbr_idx, status, u
 def nms_keep(mask, nbr_count=None, nbr_idx=None, status=None, keep=None, grid: bool = True):
     """Greedy NMS keep vector u8[n] from a single-GPU pairwise mask (dgal_nms_keep).
     grid=True runs the rounds grid-wide (cooperative launch); False in one CTA."""
+    _plane(mask, "mask", torch.int64)
     n = mask.shape[0]
     dev = mask.device
-    cap = nbr_idx.shape[1] if nbr_idx is not None else 0
+    if mask.dim() != 2 or mask.shape[1] != (n + 63) // 64:
+        raise ValueError(f"mask: expected shape [{n}, {(n + 63) // 64}], got {tuple(mask.shape)}")
+    cap = _nbr_check(nbr_count, nbr_idx, n, dev)
     status = torch.empty(n, dtype=torch.uint8, device=dev) if status is None else status
     keep = torch.empty(n, dtype=torch.uint8, device=dev) if keep is None else keep
+    _plane(status, "status", torch.uint8, n, dev)
+    _plane(keep, "keep", torch.uint8, n, dev)
     scratch = torch.empty(2, dtype=torch.int32, device=dev) if grid else None
     call("dgal_nms_keep", n, _ptr(mask), mask.shape[1], _ptr(nbr_count), _ptr(nbr_idx), cap, _ptr(status),
          _ptr(keep), _ptr(scratch), _stream(dev))

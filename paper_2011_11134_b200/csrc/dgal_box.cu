@@ -18,6 +18,7 @@
 #include "dgal_core.cuh"
 #include "dgal_internal.h"
 #include "dgal_pipe.cuh"
+#include "dgal_refine.cuh"
 
 namespace dgal {
 
@@ -30,10 +31,10 @@ namespace {
 #define DGAL_BOX_BWD_TILE 128
 #endif
 #ifndef DGAL_BOX_BWD2_MINB
-#define DGAL_BOX_BWD2_MINB 7
+#define DGAL_BOX_BWD2_MINB 6   // 80 registers (the thin-pair redo, dgal_exact.cuh; 7 CTAs spill)
 #endif
 #ifndef DGAL_BOX_BWD3_MINB
-#define DGAL_BOX_BWD3_MINB 6
+#define DGAL_BOX_BWD3_MINB 5   // 96 registers (6 CTAs spill with the thin-pair redo)
 #endif
 #ifndef DGAL_BOX_FUSED_PK
 #define DGAL_BOX_FUSED_PK true   // 2D: gradient part in paired FP32 (A/B: 0.593 -> 0.584 ms; 3D 0.674 -> 0.683, not used)
@@ -265,6 +266,7 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
     constexpr int T = kBoxFwdT;
     constexpr bool PF = DGAL_BOX_PF;
     __shared__ float sq[8 * T];   // per-thread p2 vertex table (kP2Smem), [k][thread]
+    __shared__ float sp1[DGAL_THIN ? 8 * T : 1];   // p1 corners of a thin pair (dgal_exact.cuh), [k][thread]
     __shared__ WalkLut4 wlut;     // flag-walk tables
     __shared__ __align__(16) BoxRing<DIMS, PF ? T : 1> ring;   // tile t+1 in flight while tile t computes
     const int tid = threadIdx.x;
@@ -279,6 +281,7 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
     }
     load_walk_lut4(wlut, tid, T);
     __syncthreads();
+    uint32_t thinmask = 0;   // tiles whose pair is thin (R^2 > kThinRatio A_u)
 #pragma unroll 1
     for (int t = 0; t < kBoxFwdNT; ++t) {
         const int64_t k = k0 + (int64_t)t * T;
@@ -300,15 +303,17 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
             sq[q * T + threadIdx.x] = Q.x[q];
             sq[(4 + q) * T + threadIdx.x] = Q.y[q];
         }
-        const FwdOut<4, true> r = iou_fwd<4, true, kP2Smem>(P, Q, QTable{sq + threadIdx.x, sq + 4 * T + threadIdx.x, T},
-                                                            &wlut);
+        const FwdOut<4, true> r = iou_fwd<4, true, kP2Smem, DGAL_THIN>(
+            P, Q, QTable{sq + threadIdx.x, sq + 4 * T + threadIdx.x, T}, &wlut);
+        thinmask |= (uint32_t)r.thin << t;   // thin pair: fixed after the loop
         float v = r.iou;
         int m = r.nx;
         uint64_t seq = r.seq.w[0];
+        const float A1x2 = r.A1x2, A2x2 = r.A2x2, Aix2 = r.Aix2;
         if (DIMS == 3) {
             const ZOver z = z_overlap<DIMS>(a, b);
-            const float Vix2 = r.Aix2 * z.dz;
-            const float Vux2 = (r.A1x2 * a.d + r.A2x2 * b.d) - Vix2;
+            const float Vix2 = Aix2 * z.dz;
+            const float Vux2 = (A1x2 * a.d + A2x2 * b.d) - Vix2;
             const bool ok = m > 0 && Vix2 > 0.f && Vux2 > 0.f;
             v = ok ? fminf(Vix2 / Vux2, 1.f) : 0.f;
             m = ok ? m : 0;
@@ -317,6 +322,37 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
         __stcs(iou + k, v);
         nx[k] = (uint8_t)m;
         __stcs(reinterpret_cast<unsigned long long *>(xflags) + k, (unsigned long long)seq);
+    }
+    // thin pairs (rare; dgal_exact.cuh): the areas of the stored record in double from
+    // the float corners (rebuilt from the parameters: bitwise the same), IoU / volumes
+#pragma unroll 1
+    while (thinmask) {
+        const int t = __ffs(thinmask) - 1;
+        thinmask &= thinmask - 1u;
+        const int64_t k = k0 + (int64_t)t * T;
+        const Box<DIMS> a = load_box<DIMS>(b1, k, sk, sp), b = load_box<DIMS>(b2, k, sk, sp);
+        Poly<4> P, Q;
+        box_pair_polys<DIMS>(a, b, P, Q);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            sp1[q * T + tid] = P.x[q]; sp1[(4 + q) * T + tid] = P.y[q];
+            sq[q * T + tid] = Q.x[q]; sq[(4 + q) * T + tid] = Q.y[q];
+        }
+        Seq<4> s2;
+        s2.w[0] = reinterpret_cast<const unsigned long long *>(xflags)[k];
+        int m = nx[k];
+        float v;
+        AreasX2 e;
+        fwd_thin_fix<4>(StridedVerts{sp1 + tid, sp1 + 4 * T + tid, sq + tid, sq + 4 * T + tid, T}, s2, m, v, &e);
+        if (DIMS == 3 && m > 0) {
+            const ZOver z = z_overlap<DIMS>(a, b);
+            const double Vi = e.ai * z.dz, Vu = (e.a1 * a.d + e.a2 * b.d) - Vi;
+            v = (Vi > 0.0 && Vu > 0.0) ? (float)fmin(Vi / Vu, 1.0) : 0.f;
+            if (!(Vi > 0.0 && Vu > 0.0)) { m = 0; s2.w[0] = 0ull; }
+        }
+        iou[k] = v;
+        nx[k] = (uint8_t)m;
+        reinterpret_cast<unsigned long long *>(xflags)[k] = s2.w[0];
     }
 }
 
@@ -329,6 +365,10 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
 // box parameters, as the oracle does: cos / sin by sincospi (exact
 // reduction, no local memory), frame = box 1's centre.
 struct BoxGeometry {
+    // the float corners carry ~2-3 ulp of rounding (sin / cos, products), which a
+    // crossing amplifies ~1/sin: at |sin| ~ 2^-10 that was up to 4e-4 relative in the
+    // parameter gradients, so box crossings are redone in double below 2^-7
+    static constexpr float kRefine = 0.0078125f;
     const float *p;   // staged parameters [param][pair]: cx1, cy1, w1, h1, th1, cx2, cy2, w2, h2, th2
     __device__ __forceinline__ static void corner(double dcx, double dcy, double w, double h, double th, int k,
                                                   double &x, double &y)
@@ -406,13 +446,29 @@ box_bwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
     Poly<4> G1, G2;
     VolCoef co;
     const BoxGeometry geo{S.bp};
-    bwd_tile_pair<4, kBoxTile, BoxGeometry>(S.x1, S.y1, S.x2, S.y2, sq, m, g, live, S.scr, S.queue[tid >> 5], S.lut,
-                                            G1, G2, Extrude{z.dz, a.d, b.d}, &co, &geo);
+    const bool thin = bwd_tile_pair<4, kBoxTile, BoxGeometry>(S.x1, S.y1, S.x2, S.y2, sq, m, g, live, S.scr,
+                                                              S.queue[tid >> 5], S.lut, G1, G2,
+                                                              Extrude{z.dz, a.d, b.d}, &co, &geo);
     if (!live) return;
     float gcz1, gd1, gcz2, gd2;
     z_grads<DIMS>(co, z, gcz1, gd1, gcz2, gd2);
     store_box_grad<DIMS>(gb1, k, sk, sp, box_vjp(a.w, a.h, t.c1, t.s1, G1), gcz1, gd1);
     store_box_grad<DIMS>(gb2, k, sk, sp, box_vjp(b.w, b.h, t.c2, t.s2, G2), gcz2, gd2);
+    if (thin) {   // thin pair: intersection area in double from the corner tile, gradients again (rare)
+        // everything re-read (the first pass's values are dead: no register pressure on the common path)
+        const Box<DIMS> a2 = load_box<DIMS>(b1, k, sk, sp), b2_ = load_box<DIMS>(b2, k, sk, sp);
+        const ZOver z2 = z_overlap<DIMS>(a2, b2_);
+        Seq<4> s2;
+        s2.w[0] = __ldcs(reinterpret_cast<const unsigned long long *>(xflags) + k);
+        bwd_thin_redo<4, kBoxTile>(S.x1, S.y1, S.x2, S.y2, s2, nx[k], __ldcs(grad + k), S.scr, S.lut, G1, G2,
+                                   Extrude{z2.dz, a2.d, b2_.d}, &co);
+        Trig t2;
+        box_sincos(a2.th, t2.s1, t2.c1);
+        box_sincos(b2_.th, t2.s2, t2.c2);
+        z_grads<DIMS>(co, z2, gcz1, gd1, gcz2, gd2);
+        store_box_grad<DIMS>(gb1, k, sk, sp, box_vjp(a2.w, a2.h, t2.c1, t2.s1, G1), gcz1, gd1);
+        store_box_grad<DIMS>(gb2, k, sk, sp, box_vjp(b2_.w, b2_.h, t2.c2, t2.s2, G2), gcz2, gd2);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -422,7 +478,7 @@ template <int DIMS>
 __global__ void __launch_bounds__(kBoxFusedT, DIMS == 2 ? DGAL_BOX_FUSED2_MINB : DGAL_BOX_FUSED3_MINB)
 box_fused_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict__ b2, int64_t sk, int64_t sp,
                  const float *__restrict__ grad, float scale, float *__restrict__ iou, float *__restrict__ gb1,
-                 float *__restrict__ gb2)
+                 float *__restrict__ gb2, uint32_t *__restrict__ refine)
 {
     constexpr int T = kBoxFusedT;
     constexpr bool PF = DGAL_BOX_PF;
@@ -457,13 +513,118 @@ box_fused_kernel(int64_t n, const float *__restrict__ b1, const float *__restric
         const Trig t = box_pair_polys<DIMS>(a, b, P, Q);
         const ZOver z = z_overlap<DIMS>(a, b);
         VolCoef co;
+        bool need;
         const float v = iou_fused<4, kP2PiecesSmem, DIMS == 2 && DGAL_BOX_FUSED_PK>(P, Q, g, G1, G2, Extrude{z.dz, a.d, b.d},
-                                                    &co, QTable{pt + tid, pt + 8 * T + tid, T});
+                                                    &co, QTable{pt + tid, pt + 8 * T + tid, T}, &need);
+        refine_mark(refine, k, need);   // redone exactly by box_fused_refine_kernel
         if (iou) __stcs(iou + k, v);
         float gcz1, gd1, gcz2, gd2;
         z_grads<DIMS>(co, z, gcz1, gd1, gcz2, gd2);
         store_box_grad<DIMS>(gb1, k, sk, sp, box_vjp(a.w, a.h, t.c1, t.s1, G1), gcz1, gd1);
         store_box_grad<DIMS>(gb2, k, sk, sp, box_vjp(b.w, b.h, t.c2, t.s2, G2), gcz2, gd2);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Refine pass of the fused box kernel (dgal_refine.cuh): the marked pairs redone
+// with the split path's arithmetic — box_fwd's clip with flags (+ the thin-pair
+// areas in double), then box_bwd's phases (crossings refined in double from the
+// box parameters, BoxGeometry), the extrusion and box_to_polygon_grad.
+// ---------------------------------------------------------------------------
+static_assert(kRefT == kBoxTile, "the refine tile is the backward tile (BoxGeometry strides)");
+struct BoxRefineSmem {
+    uint16_t q[kRefChunkPairs];
+    BoxBwdSmem b;
+    int qn;
+};
+
+template <int DIMS>
+__global__ void __launch_bounds__(kRefT, 4)
+box_fused_refine_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict__ b2, int64_t sk,
+                        int64_t sp, const float *__restrict__ grad, float scale, float *__restrict__ iou,
+                        float *__restrict__ gb1, float *__restrict__ gb2, uint32_t *__restrict__ refine)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BoxRefineSmem &R = *reinterpret_cast<BoxRefineSmem *>(smem_raw);
+    BoxBwdSmem &S = R.b;
+    const int tid = threadIdx.x;
+    fill_flag_lut(S.lut, tid, kRefT);
+    if (tid == 0) R.qn = 0;
+    __syncthreads();
+    const int64_t nwords = refine_words(n);
+    const int64_t nchunks = (nwords + kRefChunkWords - 1) / kRefChunkWords;
+#pragma unroll 1
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        refine_gather(refine, nwords, c, R.q, &R.qn);
+        __syncthreads();
+        const int total = R.qn;
+#pragma unroll 1
+        for (int base = 0; base < total; base += kRefT) {
+            const int e = base + tid;
+            const bool live = e < total;
+            const int64_t k = live ? c * kRefChunkPairs + R.q[e] : 0;
+            Box<DIMS> a{}, b{};
+            Poly<4> P, Q;
+            Trig t{1.f, 0.f, 1.f, 0.f};
+            if (live) {
+                a = load_box<DIMS>(b1, k, sk, sp);
+                b = load_box<DIMS>(b2, k, sk, sp);
+                t = box_pair_polys<DIMS>(a, b, P, Q);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) { P.x[q] = P.y[q] = Q.x[q] = Q.y[q] = 0.f; }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                S.x1[tid * 4 + q] = P.x[q]; S.y1[tid * 4 + q] = P.y[q];
+                S.x2[tid * 4 + q] = Q.x[q]; S.y2[tid * 4 + q] = Q.y[q];
+            }
+            {
+                const float bv[10] = {a.cx, a.cy, a.w, a.h, a.th, b.cx, b.cy, b.w, b.h, b.th};
+#pragma unroll
+                for (int q = 0; q < 10; ++q) S.bp[q * kBoxTile + tid] = bv[q];
+            }
+            const ZOver z = z_overlap<DIMS>(a, b);
+            FwdOut<4, true> r = iou_fwd<4, true, kP2Regs, true>(P, Q);
+            float A1x2 = r.A1x2, A2x2 = r.A2x2, Aix2 = r.Aix2;
+            if (r.thin) {
+                AreasX2 e;
+                fwd_thin_fix<4>(RawPolyVerts{S.x1 + tid * 4, S.y1 + tid * 4, S.x2 + tid * 4, S.y2 + tid * 4}, r.seq,
+                                r.nx, r.iou, &e);
+                A1x2 = (float)e.a1; A2x2 = (float)e.a2; Aix2 = (float)e.ai;
+            }
+            int m = r.nx;
+            float v = r.iou;
+            if (DIMS == 3) {
+                const float Vix2 = Aix2 * z.dz;
+                const float Vux2 = (A1x2 * a.d + A2x2 * b.d) - Vix2;
+                const bool ok = m > 0 && Vix2 > 0.f && Vux2 > 0.f;
+                v = ok ? fminf(Vix2 / Vux2, 1.f) : 0.f;
+                m = ok ? m : 0;
+            }
+            if (live && iou) iou[k] = v;
+            const float g = live ? (grad ? grad[k] : scale) : 0.f;
+            __syncwarp();   // the warp's tile is staged
+            Poly<4> G1, G2;
+            VolCoef co;
+            const BoxGeometry geo{S.bp};
+            const bool thin = bwd_tile_pair<4, kBoxTile, BoxGeometry>(S.x1, S.y1, S.x2, S.y2, r.seq, live ? m : 0, g,
+                                                                      live, S.scr, S.queue[tid >> 5], S.lut, G1, G2,
+                                                                      Extrude{z.dz, a.d, b.d}, &co, &geo);
+            if (thin)
+                bwd_thin_redo<4, kBoxTile>(S.x1, S.y1, S.x2, S.y2, r.seq, m, g, S.scr, S.lut, G1, G2,
+                                           Extrude{z.dz, a.d, b.d}, &co);
+            if (live) {
+                float gcz1, gd1, gcz2, gd2;
+                z_grads<DIMS>(co, z, gcz1, gd1, gcz2, gd2);
+                store_box_grad<DIMS>(gb1, k, sk, sp, box_vjp(a.w, a.h, t.c1, t.s1, G1), gcz1, gd1);
+                store_box_grad<DIMS>(gb2, k, sk, sp, box_vjp(b.w, b.h, t.c2, t.s2, G2), gcz2, gd2);
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        if (tid == 0) R.qn = 0;
+        __syncthreads();
     }
 }
 
@@ -506,16 +667,28 @@ cudaError_t launch_box_bwd(int dims, int layout, int64_t n, const float *b1, con
 }
 
 cudaError_t launch_box_fused(int dims, int layout, int64_t n, const float *b1, const float *b2, const float *grad,
-                             float scale, float *iou, float *gb1, float *gb2, cudaStream_t st)
+                             float scale, float *iou, float *gb1, float *gb2, uint32_t *refine, cudaStream_t st)
 {
     int64_t sk, sp;
     box_strides(dims, layout, n, sk, sp);
     constexpr int64_t per = (int64_t)(DGAL_BOX_PF ? DGAL_BOX_FUSED_NT : 1) * kBoxFusedT;
     const unsigned grid = (unsigned)((n + per - 1) / per);
-    if (dims == 3)
-        box_fused_kernel<3><<<grid, kBoxFusedT, 0, st>>>(n, b1, b2, sk, sp, grad, scale, iou, gb1, gb2);
-    else
-        box_fused_kernel<2><<<grid, kBoxFusedT, 0, st>>>(n, b1, b2, sk, sp, grad, scale, iou, gb1, gb2);
+    static DeviceCache c2, c3;
+    const int a = (dims == 3 ? c3 : c2).get([&](int) {
+        return dims == 3 ? set_smem_attr(box_fused_refine_kernel<3>, sizeof(BoxRefineSmem))
+                         : set_smem_attr(box_fused_refine_kernel<2>, sizeof(BoxRefineSmem));
+    });
+    if (a <= 0) return (cudaError_t)(-a);
+    const unsigned rg = (unsigned)refine_grid_for(n);
+    if (dims == 3) {
+        box_fused_kernel<3><<<grid, kBoxFusedT, 0, st>>>(n, b1, b2, sk, sp, grad, scale, iou, gb1, gb2, refine);
+        box_fused_refine_kernel<3><<<rg, kRefT, sizeof(BoxRefineSmem), st>>>(n, b1, b2, sk, sp, grad, scale, iou,
+                                                                            gb1, gb2, refine);
+    } else {
+        box_fused_kernel<2><<<grid, kBoxFusedT, 0, st>>>(n, b1, b2, sk, sp, grad, scale, iou, gb1, gb2, refine);
+        box_fused_refine_kernel<2><<<rg, kRefT, sizeof(BoxRefineSmem), st>>>(n, b1, b2, sk, sp, grad, scale, iou,
+                                                                            gb1, gb2, refine);
+    }
     return cudaGetLastError();
 }
 

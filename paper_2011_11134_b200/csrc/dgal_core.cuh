@@ -3,7 +3,7 @@
 // fully unrolled over the compile-time vertex count K ("templated
 // with options for precision and size ... fix-size allocated memory"), so no
 // array is ever dynamically indexed and nothing spills to local memory
-// (checked on the SASS by tests/test_build_artifacts.py).
+// (checked on the SASS by tests/test_abi_cpu.py::test_sass_is_sm100a_register_resident).
 //
 // Method.  The paper's `intersect(p1, p2, xflags)` is
 // realised as an edge-interval clip: every edge of p1 is clipped against the
@@ -199,12 +199,39 @@ struct Seq {
     uint64_t w[NW];
 };
 
+// the number of non-zero bytes of a record = its nx (0x00 is the padding, never a flag: R2)
+template <int K>
+__device__ __forceinline__ int record_len(const Seq<K> &s)
+{
+    int c = 0;
+#pragma unroll
+    for (int q = 0; q < K / 4; ++q) {
+        uint64_t t = s.w[q] | (s.w[q] >> 4);
+        t |= t >> 2;
+        t |= t >> 1;
+        c += __popcll(t & 0x0101010101010101ull);
+    }
+    return c;
+}
+
 template <int K>
 __device__ __forceinline__ uint32_t seq_byte(const Seq<K> &s, int p)  // p static
 {
     const uint64_t w = s.w[p >> 3];
     return (uint32_t)(w >> (8 * (p & 7))) & 0xFFu;
 }
+
+}  // namespace dgal
+
+#ifndef DGAL_THIN
+#define DGAL_THIN 1     // thin / sliver pairs: areas of the recorded intersection in double (dgal_exact.cuh)
+#endif
+#ifndef DGAL_THIN_BWD
+#define DGAL_THIN_BWD DGAL_THIN   // ... also in the backward's S:303 coefficients
+#endif
+#include "dgal_exact.cuh"   // double-precision area of the recorded intersection (thin pairs)
+
+namespace dgal {
 
 // ---------------------------------------------------------------------------
 // forward: intersect + area + IoU
@@ -215,6 +242,7 @@ struct FwdOut {
     int nx;
     Seq<K> seq;
     float A1x2, A2x2, Aix2;  // twice the areas (the 3D box forward extrudes them)
+    bool thin;               // THIN: a thin pair, its record kept for fwd_thin_fix (iou_fwd)
 };
 
 // Extrusion of the footprints for the yaw-only 3D IoU:
@@ -230,6 +258,45 @@ __device__ __forceinline__ Extrude flat() { return Extrude{1.f, 1.f, 1.f}; }
 struct VolCoef {
     float cvi, cvu, ai, a1, a2;
 };
+
+// R^2 / A_u above which a pair's float area is recomputed in double: the float
+// error is ~c eps R^2 with c of a few (measured: aspect-10 triangles at scene
+// coordinates, R^2/A_u ~ 10, max IoU error 2.3e-6 against the 1e-5 tolerance);
+// flagged pairs in the benchmark workloads: cfg3 4e-5 (nonempty), cfg4 0.
+constexpr float kThinRatio = 8.f;
+
+// squared extent of the pair about p1.v0 (the polygons recentred on it)
+template <int K>
+__device__ __forceinline__ float pair_extent2(const Poly<K> &P, const Poly<K> &Q)
+{
+    // p2's vertices two per paired instruction, in the (2q, 2q+1) pairs the decision
+    // rows pack (no register moves); p1's scalar (P.x[0] = P.y[0] = 0 after recentring)
+    float r = 0.f;
+#pragma unroll
+    for (int q = 0; q < K / 2; ++q) {
+        const uint64_t qx = f2pack(Q.x[2 * q], Q.x[2 * q + 1]), qy = f2pack(Q.y[2 * q], Q.y[2 * q + 1]);
+        float a, b;
+        f2unpack(f2fma(qx, qx, f2mul(qy, qy)), a, b);
+        r = fmaxf(r, fmaxf(a, b));
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) r = fmaxf(r, fmaf(P.x[k], P.x[k], P.y[k] * P.y[k]));
+    return r;
+}
+
+// thin: R^2 > kThinRatio A_u, with twice the union area aux2 = A1x2 + A2x2 - Aix2
+__device__ __forceinline__ bool pair_is_thin(float R2, float aux2)
+{
+    return R2 > (0.5f * kThinRatio) * aux2;
+}
+
+// the backward's form (its area is a sum of piece terms about p1.v0, not the forward's
+// per-event terms): sum |terms| = A1x2 + sum_j |C2_j| over twice the union area,
+// against the same ratio (<= 2 for two overlapping fat polygons: 2 A_1 + 2 A_2 <= 4 A_u)
+__device__ __forceinline__ bool pair_is_thin_sum(float absx2, float aux2)
+{
+    return absx2 > (0.5f * kThinRatio) * aux2;
+}
 
 // ---------------------------------------------------------------------------
 // Walk tables for K = 4 (the flag walk of iou_fwd and the p2 inside mask of
@@ -355,7 +422,15 @@ struct Clip {
     uint32_t in2;                      // p2 vertices inside p1 (consistent with the events)
     float A1x2, A2x2, Aix2;            // twice the areas
     bool nonempty;
+    bool sep;                          // a p2 edge line separates p1 (strictly): empty for sure
+    bool ill;                          // ILL: some (p1 edge, p2 line) has |sin| < kIllSin
 };
+
+// |sin| of the angle between a p1 edge and a p2 edge below which the fused kernels
+// hand the pair to their refine pass (crossing parameters in float are conditioned
+// by 1/sin: ~6e-8 / sin relative; the split backward refines |sin| < 2^-10 in double,
+// DESIGN.md §4.2b)
+constexpr float kIllSin = 0.001953125f;   // 2^-9
 
 // p1, p2 must already be recentred (coordinates near 0; p1.v0 or a box centre).
 // How the p2 side of Green's sum is formed (§4.1 of DESIGN.md):
@@ -377,7 +452,10 @@ struct QTable {
     int stride;
 };
 
-template <int K, int MODE>
+// ILL: also report whether any (p1 edge i, p2 line j) pair is nearly parallel,
+// |g_i x f_j| < kIllSin |g_i| |f_j| (c.ill; the Cyrus-Beck denominators are exactly
+// these cross products) — a superset of the pairs with an ill-conditioned crossing.
+template <int K, int MODE, bool ILL = false>
 __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &Q, Clip<K> &c,
                                                QTable qt = QTable{nullptr, nullptr, 0},
                                                const WalkLut4 *wl = nullptr)
@@ -453,6 +531,22 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     float *t0 = c.t0, *t1 = c.t1;
     uint32_t jin = 0, jout = 0, valid = 0, enter = 0, leave = 0;
     const float hi0 = __int_as_float(0x3F800008);
+    // ILL: min over (i, j) of den^2 - sin^2 |g_i|^2 |f_j|^2 (negative: nearly parallel)
+    // (K = 4: inside the edge loop, from its Cyrus-Beck denominators, with the
+    // per-line factors -sin^2 |f_j|^2 precomputed; K = 8: in a separate pass over
+    // the edge vectors after the loop — inside it, 8 more live registers spill)
+    float illm = 1.f;
+    constexpr bool ILL_LOOP = ILL && (K == 4);
+    uint64_t nsf[ILL ? K / 2 : 1];
+    const uint64_t ns2 = f2pack(-kIllSin * kIllSin, -kIllSin * kIllSin);
+    auto nsf_q = [&](int q) {
+        const uint64_t fx2 = f2pack(fx[2 * q], fx[2 * q + 1]), fy2 = f2pack(fy[2 * q], fy[2 * q + 1]);
+        return f2mul(f2fma(fx2, fx2, f2mul(fy2, fy2)), ns2);
+    };
+    if (ILL_LOOP) {
+#pragma unroll
+        for (int q = 0; q < K / 2; ++q) nsf[q] = nsf_q(q);
+    }
     // Events (same pass).  An exit of p1 edge i through p2 line j_out starts the p2
     // piece on edge j_out at X_out = v_i + t1 g_i; an entry through line j_in ends
     // the piece on edge j_in at X_in = v_i + t0 g_i.  Green's term of such a piece,
@@ -496,6 +590,12 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
             for (int j = 0; j < K; ++j) dn[j] = d0[j];
         }
         float lo = 0.f, hi = hi0;
+        uint64_t g2 = 0ull;
+        float gg = 0.f;
+        if (ILL_LOOP) {
+            gg = fmaf(gx[i], gx[i], gy[i] * gy[i]);
+            g2 = f2pack(gg, gg);
+        }
         if (DGAL_F32X2 & 2) {   // lines 2q, 2q+1 in one register pair (same arithmetic as below)
             const uint64_t tiny2 = f2pack(kTiny, kTiny), big2 = f2pack(kBig, kBig);
 #pragma unroll
@@ -504,6 +604,11 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
                 const uint64_t den = f2add(f2sub(a, f2pack(dn[2 * q], dn[2 * q + 1])), tiny2);
                 float d0_, d1_;
                 f2unpack(den, d0_, d1_);
+                if (ILL_LOOP) {
+                    float x0, x1;
+                    f2unpack(f2fma(den, den, f2mul(g2, nsf[q])), x0, x1);
+                    illm = fminf(illm, fminf(x0, x1));
+                }
                 const uint64_t r = f2pack(rcp_approx(d0_), rcp_approx(d1_));
                 const uint64_t m = f2pack(__saturatef(-d0_ * kBig), __saturatef(-d1_ * kBig));
                 float u0, u1;
@@ -520,6 +625,11 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
             for (int j = 0; j < K; ++j) {
                 const float a = dc[j], b = dn[j];
                 const float den = (a - b) + kTiny;
+                if (ILL_LOOP) {
+                    float nf0, nf1;
+                    f2unpack(nsf[j / 2], nf0, nf1);
+                    illm = fminf(illm, fmaf(den, den, gg * ((j & 1) ? nf1 : nf0)));
+                }
                 const float r = rcp_approx(den);
                 const float m = __saturatef(-den * kBig);  // 1: bounds below
                 const float ve = enc_idx(a * r, j);
@@ -593,6 +703,23 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     bool separated = false;
 #pragma unroll
     for (int j = 0; j < K; ++j) separated |= (m1[j] < kTiny);
+    if (ILL && !ILL_LOOP) {   // (g_i x f_j)^2 - sin^2 |g_i|^2 |f_j|^2 over all (i, j), lines paired
+#pragma unroll
+        for (int q = 0; q < K / 2; ++q) nsf[q] = nsf_q(q);
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const float gg = fmaf(gx[i], gx[i], gy[i] * gy[i]);
+            const uint64_t g2 = f2pack(gg, gg), GX = f2pack(gx[i], gx[i]), NGY = f2pack(-gy[i], -gy[i]);
+#pragma unroll
+            for (int q = 0; q < K / 2; ++q) {
+                const uint64_t fx2 = f2pack(fx[2 * q], fx[2 * q + 1]), fy2 = f2pack(fy[2 * q], fy[2 * q + 1]);
+                const uint64_t cr = f2fma(GX, fy2, f2mul(NGY, fx2));
+                float x0, x1;
+                f2unpack(f2fma(cr, cr, f2mul(g2, nsf[q])), x0, x1);
+                illm = fminf(illm, fminf(x0, x1));
+            }
+        }
+    }
     c.jin = jin; c.jout = jout; c.valid = valid; c.enter = enter; c.leave = leave;
     if (PSMEM) {
 #pragma unroll
@@ -651,10 +778,20 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     c.on2 = on2;
     c.in2 = in2;
     c.nonempty = !separated && (Aix2 > 0.f);
+    c.sep = separated;
+    c.ill = ILL && (illm < 0.f);
 }
 
 // p1, p2 must already be recentred on o = p1.v0 (p1.x[0] == p1.y[0] == 0).
-template <int K, bool FLAGS, int MODE = (K == 4 ? kP2Pieces : kP2Regs)>
+// THIN (FLAGS only): detect thin pairs, R^2 > kThinRatio A_u (pair_is_thin).  A thin
+// pair's float area sum — including the sign test that decides an empty
+// intersection — is not accurate enough: out.thin is set and out.seq / out.nx hold
+// the walk's record whatever the sign of the float area (when the pair is not
+// separated and the walk has 3..2K vertices), so the caller can recompute the areas
+// of p1, p2 and of that record in double (areas_exact, dgal_exact.cuh) and decide
+// emptiness and the IoU from them (fwd_thin_fix).  The kernels do that after their
+// tile loop (rare; keeps the double-precision code out of the hot loop).
+template <int K, bool FLAGS, int MODE = (K == 4 ? kP2Pieces : kP2Regs), bool THIN = false>
 __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly<K> &Q,
                                                     QTable qt = QTable{nullptr, nullptr, 0},
                                                     const WalkLut4 *wl = nullptr)
@@ -662,6 +799,8 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
     constexpr uint32_t KMASK = (1u << K) - 1u;
     Clip<K> c;
     clip_intervals<K, MODE>(P, Q, c, qt, wl);
+    // (after the clip, which keeps P and Q live to its end anyway: one register through the walk)
+    const float R2 = (FLAGS && THIN) ? pair_extent2<K>(P, Q) : 0.f;
     const float *t0 = c.t0, *t1 = c.t1;
     const float A1x2 = c.A1x2, A2x2 = c.A2x2, Aix2 = c.Aix2;
     bool nonempty = c.nonempty;
@@ -674,6 +813,7 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
     out.A1x2 = A1x2;
     out.A2x2 = A2x2;
     out.Aix2 = 0.f;
+    out.thin = false;
 
     if (FLAGS) {
         // p2 vertices inside p1, consistent with the crossings (clip_intervals)
@@ -753,8 +893,10 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
         }
         // The walk from p1's edge 0 IS the canonical order (R3: start at the first
         // vertex along p1's boundary from v0; FromP2(0) when p2 lies inside p1).
-        nonempty = nonempty && pos >= 3 && pos <= 2 * K;
-        if (nonempty) {
+        const bool cand = !c.sep && pos >= 3 && pos <= 2 * K;
+        out.thin = THIN && cand && pair_is_thin(R2, (A1x2 + A2x2) - Aix2);
+        nonempty = nonempty && cand;
+        if (nonempty || out.thin) {
             out.seq = s;
             out.nx = pos;
         }
@@ -775,17 +917,30 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
 // trip, no crossing recomputation): dA_i/dv_i += n_i ∫(1-t)dt, dA_i/dv_i+1 +=
 // n_i ∫t dt over each boundary piece, then the S:303 chain.
 // p1, p2 recentred on p1.v0.  Returns IoU (identical to the pairwise path).
+// need (when given): the float result may miss the tolerance — a nearly parallel
+// (p1 edge, p2 edge) pair (crossing parameters conditioned by 1/sin) or a thin pair
+// (area sum conditioned by R^2 / A_u) — and the caller must have the pair redone by
+// the exact split path (the fused kernels' refine pass).
 template <int K, int MODE = kP2Pieces, bool PK = false>
 __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, float g, Poly<K> &G1,
                                            Poly<K> &G2, const Extrude ex = flat(), VolCoef *co = nullptr,
-                                           QTable qt = QTable{nullptr, nullptr, 0})
+                                           QTable qt = QTable{nullptr, nullptr, 0}, bool *need = nullptr)
 {
 #pragma unroll
     for (int k = 0; k < K; ++k) { G1.x[k] = 0.f; G1.y[k] = 0.f; G2.x[k] = 0.f; G2.y[k] = 0.f; }
     if (co) *co = VolCoef{0.f, 0.f, 0.f, 0.f, 0.f};
+    const float R2 = need ? pair_extent2<K>(P, Q) : 0.f;
+    if (need) *need = false;
     Clip<K> c;
-    clip_intervals<K, MODE>(P, Q, c, qt);
-    if (!c.nonempty) return 0.f;
+    if (need) clip_intervals<K, MODE, true>(P, Q, c, qt);
+    else clip_intervals<K, MODE, false>(P, Q, c, qt);
+    if (!c.nonempty) {
+        // a thin pair's float area may be <= 0 although p1 and p2 overlap: the refine
+        // pass decides (when the pair is not separated and has a boundary piece)
+        if (need) *need = !c.sep && (c.valid | c.in2) != 0u && pair_is_thin(R2, (c.A1x2 + c.A2x2) - c.Aix2);
+        return 0.f;
+    }
+    if (need) *need = c.ill || pair_is_thin(R2, (c.A1x2 + c.A2x2) - c.Aix2);
     // V = A d (2D: d = 1); IoU = V_i / V_u
     const float Vix2 = c.Aix2 * ex.dz;
     const float Vux2 = (c.A1x2 * ex.d1 + c.A2x2 * ex.d2) - Vix2;
@@ -939,7 +1094,8 @@ constexpr float kRefineSin = 0.0009765625f;   // 2^-10: float t error ~6e-8/sin 
 
 template <int K, int TILE>
 __device__ __forceinline__ bool bwd_crossing(const float *sPx, const float *sPy, const float *sQx,
-                                             const float *sQy, uint32_t b, float *scr)
+                                             const float *sQy, uint32_t b, float *scr,
+                                             float refine_sin = kRefineSin)
 {
     const int i = (b >> 3) & (K - 1), j = b & (K - 1);
     const int i1 = (i + 1) & (K - 1), j1 = (j + 1) & (K - 1);
@@ -956,7 +1112,7 @@ __device__ __forceinline__ bool bwd_crossing(const float *sPx, const float *sPy,
     const bool enter = den < 0.f;
     DGAL_ASSERT(i >= 0 && i < K && j >= 0 && j < K);
     // ill-conditioned (den^2 < sin^2 |e|^2 |h|^2): left to bwd_crossing_exact
-    const bool need = DGAL_BWD_REFINE && (den * den < (kRefineSin * kRefineSin) * fmaf(ex, ex, ey * ey) * hh);
+    const bool need = DGAL_BWD_REFINE && (den * den < (refine_sin * refine_sin) * fmaf(ex, ex, ey * ey) * hh);
     if (!need) {
         scr[(enter ? i : K + i) * TILE] = t;
         scr[(enter ? 3 * K + j : 2 * K + j) * TILE] = s;
@@ -969,6 +1125,7 @@ __device__ __forceinline__ bool bwd_crossing(const float *sPx, const float *sPy,
 // the input, so its values are exact.
 template <int K>
 struct TileGeometry {
+    static constexpr float kRefine = kRefineSin;   // |sin| below which a crossing is redone in double
     const float *x1, *y1, *x2, *y2;   // tile bases, [pair][k]
     __device__ __forceinline__ void get(int pt, int i, int i1, int j, int j1, double &vx, double &vy,
                                         double &v1x, double &v1y, double &wx, double &wy, double &w1x,
@@ -976,6 +1133,11 @@ struct TileGeometry {
     {
         vx = x1[pt * K + i]; vy = y1[pt * K + i]; v1x = x1[pt * K + i1]; v1y = y1[pt * K + i1];
         wx = x2[pt * K + j]; wy = y2[pt * K + j]; w1x = x2[pt * K + j1]; w1y = y2[pt * K + j1];
+    }
+    // all vertices of the pair, for the exact area of a thin pair (dgal_exact.cuh)
+    __device__ __forceinline__ RawPolyVerts verts(int pt) const
+    {
+        return RawPolyVerts{x1 + pt * K, y1 + pt * K, x2 + pt * K, y2 + pt * K};
     }
 };
 
@@ -1017,16 +1179,22 @@ __device__ __forceinline__ void bwd_crossing_exact(const float *sPx, const float
 }
 
 // V = OR of the flag table over the recorded bytes (vertex / crossing provenance).
+// Returns whether the pair is thin (pair_is_thin on its float areas): then the
+// caller recomputes the intersection's area in double and calls again with twice
+// it in *ovr, which replaces the float sum in the S:303 coefficients (the piece
+// weights stay the float ones: they need ~1e-7, not 1e-16; so do A_1, A_2, whose
+// float sums are accurate to ~eps R^2 / A — only a sliver intersection's is not).
 template <int K, int TILE, bool PK = false>
-__device__ __forceinline__ void bwd_epilogue(const float *sPx, const float *sPy, const float *sQx,
+__device__ __forceinline__ bool bwd_epilogue(const float *sPx, const float *sPy, const float *sQx,
                                              const float *sQy, float g, uint32_t V, const float *scr,
                                              Poly<K> &G1, Poly<K> &G2, const Extrude ex = flat(),
-                                             VolCoef *co = nullptr)
+                                             VolCoef *co = nullptr, const float *ovr = nullptr)
 {
 #pragma unroll
     for (int k = 0; k < K; ++k) { G1.x[k] = 0.f; G1.y[k] = 0.f; G2.x[k] = 0.f; G2.y[k] = 0.f; }
     if (co) *co = VolCoef{0.f, 0.f, 0.f, 0.f, 0.f};
-    if (V == 0) return;  // nx == 0: zero subgradient
+    if (V == 0) return false;  // nx == 0: zero subgradient
+    bool thin = false;
 
     if constexpr (PK && (DGAL_F32X2 & 4)) {
     // paired FP32 along (p1, p2): X[k] = (v_k.x, w_k.x), Y[k] = (v_k.y, w_k.y) recentred
@@ -1077,13 +1245,27 @@ __device__ __forceinline__ void bwd_epilogue(const float *sPx, const float *sPy,
     }
     float ai1, ai2;
     f2unpack(AIX, ai1, ai2);
-    const float Aix2 = ai1 + ai2;
+    float Aix2 = ai1 + ai2;
+    if (ovr) {
+        Aix2 = *ovr;
+    } else if (DGAL_THIN_BWD) {
+        // the piece sum's rounding: ~eps (sum |L C1| + sum |L C2|) <= eps (A1x2 + sum |C2|)
+        // (C1 >= 0: o = p1.v0 lies in p1); C2 terms are large when p2 is far from o
+        float c2abs = 0.f;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            float c1_, c2_;
+            f2unpack(C[i], c1_, c2_);
+            c2abs += fabsf(c2_);
+        }
+        thin = pair_is_thin_sum(A1x2 + c2abs, (A1x2 + A2x2) - Aix2);
+    }
 
     // dIoU/dV_i = (V_u + V_i)/V_u^2, dIoU/dV_1,2 = -V_i/V_u^2; V = A d (2D: d = 1)
     const float Ai = 0.5f * Aix2;
     const float Vi = Ai * ex.dz;
     const float Vu = 0.5f * ((A1x2 * ex.d1 + A2x2 * ex.d2) - Aix2 * ex.dz);
-    if (!(Vu > 0.f) || !(Vi > 0.f)) return;  // R10 guard
+    if (!(Vu > 0.f) || !(Vi > 0.f)) return thin;  // R10 guard
     const float inv = 1.f / Vu;
     const float q = Vi * inv;
     const float cvi = g * ((1.f + q) * inv);
@@ -1152,12 +1334,20 @@ __device__ __forceinline__ void bwd_epilogue(const float *sPx, const float *sPy,
         Aix2 = fmaf(l1, C1[i], Aix2);
         Aix2 = fmaf(l2, C2[i], Aix2);
     }
+    if (ovr) {
+        Aix2 = *ovr;
+    } else if (DGAL_THIN_BWD) {
+        float c2abs = 0.f;
+#pragma unroll
+        for (int i = 0; i < K; ++i) c2abs += fabsf(C2[i]);
+        thin = pair_is_thin_sum(A1x2 + c2abs, (A1x2 + A2x2) - Aix2);
+    }
 
     // dIoU/dV_i = (V_u + V_i)/V_u^2, dIoU/dV_1,2 = -V_i/V_u^2; V = A d (2D: d = 1)
     const float Ai = 0.5f * Aix2;
     const float Vi = Ai * ex.dz;
     const float Vu = 0.5f * ((A1x2 * ex.d1 + A2x2 * ex.d2) - Aix2 * ex.dz);
-    if (!(Vu > 0.f) || !(Vi > 0.f)) return;  // R10 guard
+    if (!(Vu > 0.f) || !(Vi > 0.f)) return thin;  // R10 guard
     const float inv = 1.f / Vu;
     const float q = Vi * inv;
     const float cvi = g * ((1.f + q) * inv);
@@ -1180,6 +1370,7 @@ __device__ __forceinline__ void bwd_epilogue(const float *sPx, const float *sPy,
         G2.y[k] = -fmaf(wa2, fx[k], wb2 * fx[km]);
     }
     }
+    return thin;
 }
 
 // One backward tile: thread tid owns pair tid of a tile of TILE pairs whose
@@ -1188,7 +1379,7 @@ __device__ __forceinline__ void bwd_epilogue(const float *sPx, const float *sPy,
 // (warp prefix sum), evaluates the warp's crossings 32 at a time (full SIMT
 // width), then runs the epilogue.  Must be called by all 32 lanes of the warp.
 template <int K, int TILE, class GEO = TileGeometry<K>, bool PK = false>
-__device__ __forceinline__ void bwd_tile_pair(const float *tx1, const float *ty1, const float *tx2,
+__device__ __forceinline__ bool bwd_tile_pair(const float *tx1, const float *ty1, const float *tx2,
                                               const float *ty2, const Seq<K> &sq, int m, float g, bool live,
                                               float *scr, uint16_t *queue, const FlagLut &lut,
                                               Poly<K> &G1, Poly<K> &G2, const Extrude ex = flat(),
@@ -1243,7 +1434,7 @@ __device__ __forceinline__ void bwd_tile_pair(const float *tx1, const float *ty1
             DGAL_ASSERT((int)(ent >> 8) < 32);
             const int pt = warp * 32 + (int)(ent >> 8);
             need = bwd_crossing<K, TILE>(tx1 + pt * K, ty1 + pt * K, tx2 + pt * K, ty2 + pt * K, ent & 0xFFu,
-                                         scr + pt);
+                                         scr + pt, GEO::kRefine);
         }
         const unsigned bal = __ballot_sync(0xFFFFFFFFu, need);
         if (bal) {
@@ -1269,9 +1460,76 @@ __device__ __forceinline__ void bwd_tile_pair(const float *tx1, const float *ty1
         }
     }
     __syncwarp();
+    bool thin = false;
     if (live)
-        bwd_epilogue<K, TILE, PK>(tx1 + tid * K, ty1 + tid * K, tx2 + tid * K, ty2 + tid * K, g, V, scr + tid, G1,
-                                  G2, ex, co);
+        thin = bwd_epilogue<K, TILE, PK>(tx1 + tid * K, ty1 + tid * K, tx2 + tid * K, ty2 + tid * K, g, V, scr + tid,
+                                         G1, G2, ex, co);
+    return DGAL_THIN_BWD && thin;
+}
+
+// the recorded bytes masked to the first m, and their provenance bits (the flag table)
+template <int K>
+__device__ __forceinline__ uint32_t masked_record(Seq<K> &w, int m, const FlagLut &lut)
+{
+#pragma unroll
+    for (int q = 0; q < Seq<K>::NW; ++q) {
+        const int rem = m - 8 * q;
+        w.w[q] &= (rem >= 8) ? ~0ull : ((rem <= 0) ? 0ull : (shl64(1ull, 8u * (uint32_t)rem) - 1ull));
+    }
+    uint32_t V = 0;
+#pragma unroll
+    for (int p = 0; p < 2 * K; ++p) V |= lut.v[seq_byte<K>(w, p)];
+    return V;
+}
+
+// The whole backward of ONE pair by its own thread, every crossing in double and the
+// intersection's area in double (areas_exact): the thin-pair redo of the per-thread
+// backward kernel, run after its tile loop with the pair re-staged at tile slot pt
+// (no warp cooperation, so it runs for the thin lanes only).
+template <int K, int TILE, bool PK = false>
+__device__ __forceinline__ void bwd_pair_exact(const float *tx1, const float *ty1, const float *tx2,
+                                               const float *ty2, int pt, Seq<K> w, int m, float g, float *scr,
+                                               const FlagLut &lut, Poly<K> &G1, Poly<K> &G2)
+{
+    const uint32_t V = masked_record<K>(w, m, lut);
+    bwd_prologue<K, TILE>(scr + pt);
+    const TileGeometry<K> geo{tx1, ty1, tx2, ty2};
+#pragma unroll 1
+    for (int p = 0; p < m && p < 2 * K; ++p) {
+        const uint64_t ww = (K == 8 && p >= 8) ? w.w[Seq<K>::NW - 1] : w.w[0];
+        const uint32_t b = (uint32_t)(ww >> (8 * (p & 7))) & 0xFFu;
+        if (b >= 0xC0u)
+            bwd_crossing_exact<K, TILE, TileGeometry<K>>(tx1 + pt * K, ty1 + pt * K, tx2 + pt * K, ty2 + pt * K, b,
+                                                         scr + pt, geo, pt);
+    }
+    const AreasX2 a = areas_exact<K, false>(geo.verts(pt), w, m);
+    const float ovr = (float)a.ai;
+    bwd_epilogue<K, TILE, PK>(tx1 + pt * K, ty1 + pt * K, tx2 + pt * K, ty2 + pt * K, g, V, scr + pt, G1, G2, flat(),
+                              nullptr, &ovr);
+}
+
+
+// A thin pair (bwd_tile_pair returned true; rare): the area of the recorded
+// intersection in double (dgal_exact.cuh), then the epilogue again with it.
+// Called by the kernels AFTER they stored the first gradients (so those are dead
+// here: no register pressure on the common path), before the tile's shared memory
+// (vertices, interval scratch) is reused; the record is re-read by the caller
+// (sq, m: as given to bwd_tile_pair).  Overwrites G1, G2 (and co).
+// The vertices are the tile's floats (for boxes: the float corners; their rounding,
+// ~eps L, moves a sliver's area by ~eps L W — relative ~eps; it is the float SUM,
+// ~eps R^2, that is not accurate enough).
+template <int K, int TILE, bool PK = false>
+__device__ __forceinline__ void bwd_thin_redo(const float *tx1, const float *ty1, const float *tx2,
+                                              const float *ty2, Seq<K> w, int m, float g, const float *scr,
+                                              const FlagLut &lut, Poly<K> &G1, Poly<K> &G2,
+                                              const Extrude ex = flat(), VolCoef *co = nullptr)
+{
+    const int tid = threadIdx.x;
+    const uint32_t V = masked_record<K>(w, m, lut);
+    const AreasX2 a = areas_exact<K, false>(TileGeometry<K>{tx1, ty1, tx2, ty2}.verts(tid), w, m);
+    const float ovr = (float)a.ai;
+    bwd_epilogue<K, TILE, PK>(tx1 + tid * K, ty1 + tid * K, tx2 + tid * K, ty2 + tid * K, g, V, scr + tid, G1, G2,
+                              ex, co, &ovr);
 }
 
 }  // namespace dgal

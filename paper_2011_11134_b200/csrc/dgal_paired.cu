@@ -3,6 +3,7 @@
 #include "dgal_core.cuh"
 #include "dgal_internal.h"
 #include "dgal_pipe.cuh"
+#include "dgal_refine.cuh"
 
 namespace dgal {
 
@@ -103,6 +104,7 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
         __syncthreads();
     }
     QTable qt{sq + threadIdx.x, sq + K * T + threadIdx.x, T};
+    uint32_t thinmask = 0;   // tiles whose pair is thin (R^2 > kThinRatio A_u)
 #pragma unroll 1
     for (int t = 0; t < NT; ++t) {
         const int64_t k = k0 + (int64_t)t * T;
@@ -132,7 +134,8 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
 #pragma unroll
             for (int q = 0; q < K; ++q) { sq[q * T + threadIdx.x] = Q.x[q]; sq[(K + q) * T + threadIdx.x] = Q.y[q]; }
         }
-        const FwdOut<K, true> r = iou_fwd<K, true, DGAL_FWD_P2MODE>(P, Q, qt, WL ? &wlut[0] : nullptr);
+        const FwdOut<K, true> r = iou_fwd<K, true, DGAL_FWD_P2MODE, DGAL_THIN>(P, Q, qt, WL ? &wlut[0] : nullptr);
+        thinmask |= (uint32_t)r.thin << t;   // thin pair: fixed after the loop
         __stcs(iou + k, r.iou);
         nx[k] = (uint8_t)r.nx;
         if (K == 4) {
@@ -142,6 +145,33 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
             v.x = r.seq.w[0];
             v.y = r.seq.w[Seq<K>::NW - 1];
             __stcs(reinterpret_cast<ulonglong2 *>(xflags) + k, v);
+        }
+    }
+    // thin pairs (rare; dgal_exact.cuh): the areas of the record this thread stored, in
+    // double from the raw inputs, decide emptiness and the IoU (out of the hot loop)
+#ifdef DGAL_THIN_NOPOST
+    if (thinmask) iou[k0] = -1.f;
+    thinmask = 0;
+#endif
+#pragma unroll 1
+    while (thinmask) {
+        const int t = __ffs(thinmask) - 1;
+        thinmask &= thinmask - 1u;
+        const int64_t k = k0 + (int64_t)t * T;
+        Seq<K> sq2;
+        int m = nx[k];
+        if (K == 4) sq2.w[0] = reinterpret_cast<const unsigned long long *>(xflags)[k];
+        else {
+            const ulonglong2 v = reinterpret_cast<const ulonglong2 *>(xflags)[k];
+            sq2.w[0] = v.x; sq2.w[Seq<K>::NW - 1] = v.y;
+        }
+        float v;
+        fwd_thin_fix<K>(RawPolyVerts{x1 + k * K, y1 + k * K, x2 + k * K, y2 + k * K}, sq2, m, v);
+        iou[k] = v;
+        if (m == 0) {
+            nx[k] = 0;
+            if (K == 4) reinterpret_cast<unsigned long long *>(xflags)[k] = 0ull;
+            else reinterpret_cast<ulonglong2 *>(xflags)[k] = make_ulonglong2(0ull, 0ull);
         }
     }
 }
@@ -274,9 +304,19 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
         for (int q = 0; q < K / 4; ++q) sq.w[q] = live ? T.xf[tid * (K / 4) + q] : 0ull;
         const int m = live ? T.nx[tid] : 0;
         Poly<K> G1, G2;
-        bwd_tile_pair<K, kTile>(T.x1, T.y1, T.x2, T.y2, sq, m, live ? T.g[tid] : 0.f, live, S.scr,
-                                S.queue[tid >> 5], S.lut, G1, G2);
+        const bool thin = bwd_tile_pair<K, kTile>(T.x1, T.y1, T.x2, T.y2, sq, m, live ? T.g[tid] : 0.f, live, S.scr,
+                                                  S.queue[tid >> 5], S.lut, G1, G2);
         if (live) {
+            store_plane<K>(gx1, k, G1.x);
+            store_plane<K>(gy1, k, G1.y);
+            store_plane<K>(gx2, k, G2.x);
+            store_plane<K>(gy2, k, G2.y);
+        }
+        if (thin) {   // thin pair: area in double, gradients again (rare); the record re-read
+            Seq<K> s2;
+#pragma unroll
+            for (int q = 0; q < K / 4; ++q) s2.w[q] = T.xf[tid * (K / 4) + q];
+            bwd_thin_redo<K, kTile>(T.x1, T.y1, T.x2, T.y2, s2, T.nx[tid], T.g[tid], S.scr, S.lut, G1, G2);
             store_plane<K>(gx1, k, G1.x);
             store_plane<K>(gy1, k, G1.y);
             store_plane<K>(gx2, k, G2.x);
@@ -330,6 +370,7 @@ struct BwdPtSmem {
     float scr[4 * K * T];
     uint16_t queue[T / 32][32 * 2 * K];
     FlagLut lut;
+    uint32_t thinm[T];   // per thread: tiles whose pair is thin (kept here, not in a register: the loop is at 72)
 };
 
 template <int K>
@@ -365,25 +406,23 @@ paired_bwd_pt_kernel(int64_t n, const float *__restrict__ x1, const float *__res
         if (K == 4) cp_async8(D.xf + tid, xflags + k * 8);
         else cp_async16(D.xf + 2 * tid, xflags + k * 16);
     };
-    int m_next = 0;
-    if (tile_base(0) + tid < n) {
-        prefetch(0, tile_base(0) + tid);
-        m_next = nx[tile_base(0) + tid];
-    }
+    // nx is not loaded: a forward record's bytes past nx are the 0x00 padding (R2),
+    // which the phases ignore (no flag-table bits, no crossing), so the record is
+    // read whole (m = 2K; the thin redo counts its bytes) — one load and one live
+    // register less per pair (the loop is at its 72-register budget)
+    if (tile_base(0) + tid < n) prefetch(0, tile_base(0) + tid);
     cp_async_commit();
     fill_flag_lut(S.lut, tid, T);
     __syncthreads();
+    S.thinm[tid] = 0u;
 #pragma unroll 1
     for (int t = 0; t < nv; ++t) {
         const int64_t k = tile_base(t) + tid;
         const bool live = k < n;
-        const int m = live ? m_next : 0;
+        const int m = live ? 2 * K : 0;
         if (t + 1 < nv) {
             const int64_t kn = tile_base(t + 1) + tid;
-            if (kn < n) {
-                prefetch((t + 1) & 1, kn);
-                m_next = nx[kn];
-            }
+            if (kn < n) prefetch((t + 1) & 1, kn);
         }
         cp_async_commit();
         cp_async_wait<1>();                      // this thread's copies of tile t landed
@@ -393,15 +432,52 @@ paired_bwd_pt_kernel(int64_t n, const float *__restrict__ x1, const float *__res
 #pragma unroll
         for (int q = 0; q < K / 4; ++q) sq.w[q] = live ? D.xf[tid * (K / 4) + q] : 0ull;
         Poly<K> G1, G2;
-        bwd_tile_pair<K, T, TileGeometry<K>, K == 4>(D.x1, D.y1, D.x2, D.y2, sq, m, live ? D.g[tid] : 0.f, live,
-                                                     S.scr, S.queue[tid >> 5], S.lut, G1, G2);
+        const bool thin = bwd_tile_pair<K, T, TileGeometry<K>, K == 4>(D.x1, D.y1, D.x2, D.y2, sq, m,
+                                                                       live ? D.g[tid] : 0.f, live, S.scr,
+                                                                       S.queue[tid >> 5], S.lut, G1, G2);
         if (live) {
             store_plane<K>(gx1, k, G1.x);
             store_plane<K>(gy1, k, G1.y);
             store_plane<K>(gx2, k, G2.x);
             store_plane<K>(gy2, k, G2.y);
         }
+        if (thin) S.thinm[tid] |= 1u << t;      // thin pair: redone after the loop
         __syncwarp();                            // stage t & 1 is refilled next iteration
+    }
+    // thin pairs (rare; dgal_exact.cuh), out of the hot loop: each thread redoes its own,
+    // re-staged at its slot of stage 0 from global memory, every crossing and the
+    // intersection's area in double (bwd_pair_exact; no warp cooperation)
+    if (!DGAL_THIN_BWD) return;
+    cp_async_wait<0>();
+    uint32_t thinmask = S.thinm[tid];
+    typename BwdPtSmem<K>::Stage &D = S.st[0];
+    // the chunk's first pair recomputed from the CTA index (volatile: not kept live
+    // through the loop, which is at its register budget)
+    uint32_t cta, ncta;
+    asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(cta));
+    asm volatile("mov.u32 %0, %%nctaid.x;" : "=r"(ncta));
+    const int64_t base2 = (int64_t)(DGAL_BWD_REV ? (ncta - 1u - cta) : cta) * (NT * T);
+    const int nv2 = (int)min((int64_t)NT, (n - base2 + T - 1) / T);
+#pragma unroll 1
+    while (thinmask) {
+        const int t = __ffs(thinmask) - 1;
+        thinmask &= thinmask - 1u;
+        const int64_t k = base2 + (int64_t)(DGAL_BWD_REV ? (nv2 - 1 - t) : t) * T + tid;
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+            D.x1[tid * K + q] = x1[k * K + q]; D.y1[tid * K + q] = y1[k * K + q];
+            D.x2[tid * K + q] = x2[k * K + q]; D.y2[tid * K + q] = y2[k * K + q];
+        }
+        Seq<K> sq;
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q) sq.w[q] = reinterpret_cast<const uint64_t *>(xflags)[k * (K / 4) + q];
+        Poly<K> G1, G2;
+        bwd_pair_exact<K, T, K == 4>(D.x1, D.y1, D.x2, D.y2, tid, sq, record_len<K>(sq), grad[k], S.scr, S.lut, G1,
+                                     G2);
+        store_plane<K>(gx1, k, G1.x);
+        store_plane<K>(gy1, k, G1.y);
+        store_plane<K>(gx2, k, G2.x);
+        store_plane<K>(gy2, k, G2.y);
     }
 }
 
@@ -515,7 +591,7 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
                     const float *__restrict__ x2, const float *__restrict__ y2,
                     const float *__restrict__ grad, float scale, float *__restrict__ iou,
                     float *__restrict__ gx1, float *__restrict__ gy1,
-                    float *__restrict__ gx2, float *__restrict__ gy2)
+                    float *__restrict__ gx2, float *__restrict__ gy2, uint32_t *__restrict__ refine)
 {
 #ifndef DGAL_FUSED_PK
 #define DGAL_FUSED_PK true   // K = 4: gradient part in paired FP32 (K = 8 would spill)
@@ -581,8 +657,10 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
             if (grad) g = __ldcs(grad + k);
         }
         recentre<K>(P, Q);
+        bool need;
         const float v = iou_fused<K, DGAL_FUSED_P2MODE, K == 4 && DGAL_FUSED_PK>(P, Q, g, G1, G2, flat(), nullptr,
-                                                        QTable{pt + tid, pt + 2 * K * T + tid, T});
+                                                        QTable{pt + tid, pt + 2 * K * T + tid, T}, &need);
+        refine_mark(refine, k, need);   // redone exactly by paired_fused_refine_kernel
         if (iou) __stcs(iou + k, v);
         store_plane<K>(gx1, k, G1.x);
         store_plane<K>(gy1, k, G1.y);
@@ -590,6 +668,110 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
         store_plane<K>(gy2, k, G2.y);
     }
 }
+
+// ---------------------------------------------------------------------------
+// Refine pass of the fused kernel (dgal_refine.cuh): the marked pairs redone with
+// the split path's arithmetic — the forward clip with flags (+ the area of the
+// recorded intersection in double for a thin pair), then the backward phases
+// through those flags (ill-conditioned crossings refined in double).  Each CTA
+// gathers a chunk's marked pairs and works on them 128 at a time.
+// ---------------------------------------------------------------------------
+template <int K>
+struct RefineSmem {
+    uint16_t q[kRefChunkPairs];                             // marked pairs of the chunk
+    float x1[kRefT * K], y1[kRefT * K], x2[kRefT * K], y2[kRefT * K];   // raw tile, [pair][k]
+    float scr[4 * K * kRefT];                               // interval end points, [slot][pair]
+    uint16_t queue[kRefT / 32][32 * 2 * K];                 // per-warp crossing queue
+    float sq[2 * K * kRefT];                                // per-thread p2 vertex table (kP2Smem), [k][thread]
+    FlagLut lut;
+    int qn;
+};
+
+template <int K>
+__global__ void __launch_bounds__(kRefT, (K == 4) ? 4 : 2)
+paired_fused_refine_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
+                           const float *__restrict__ x2, const float *__restrict__ y2,
+                           const float *__restrict__ grad, float scale, float *__restrict__ iou,
+                           float *__restrict__ gx1, float *__restrict__ gy1, float *__restrict__ gx2,
+                           float *__restrict__ gy2, uint32_t *__restrict__ refine)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RefineSmem<K> &S = *reinterpret_cast<RefineSmem<K> *>(smem_raw);
+    const int tid = threadIdx.x;
+    fill_flag_lut(S.lut, tid, kRefT);
+    if (tid == 0) S.qn = 0;
+    __syncthreads();
+    const int64_t nwords = refine_words(n);
+    const int64_t nchunks = (nwords + kRefChunkWords - 1) / kRefChunkWords;
+#pragma unroll 1
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        refine_gather(refine, nwords, c, S.q, &S.qn);
+        __syncthreads();
+        const int total = S.qn;
+#pragma unroll 1
+        for (int base = 0; base < total; base += kRefT) {
+            const int e = base + tid;
+            const bool live = e < total;
+            const int64_t k = live ? c * kRefChunkPairs + S.q[e] : 0;
+            DGAL_ASSERT(!live || k < n);
+            Poly<K> P, Q;
+            if (live) {
+                load_poly<K>(x1, y1, k, P);
+                load_poly<K>(x2, y2, k, Q);
+            } else {
+#pragma unroll
+                for (int q = 0; q < K; ++q) { P.x[q] = P.y[q] = Q.x[q] = Q.y[q] = 0.f; }
+            }
+#pragma unroll
+            for (int q = 0; q < K; ++q) {
+                S.x1[tid * K + q] = P.x[q]; S.y1[tid * K + q] = P.y[q];
+                S.x2[tid * K + q] = Q.x[q]; S.y2[tid * K + q] = Q.y[q];
+            }
+            recentre<K>(P, Q);
+#pragma unroll
+            for (int q = 0; q < K; ++q) { S.sq[q * kRefT + tid] = Q.x[q]; S.sq[(K + q) * kRefT + tid] = Q.y[q]; }
+            FwdOut<K, true> r = iou_fwd<K, true, kP2Smem, true>(P, Q, QTable{S.sq + tid, S.sq + K * kRefT + tid, kRefT});
+            if (r.thin)
+                fwd_thin_fix<K>(RawPolyVerts{S.x1 + tid * K, S.y1 + tid * K, S.x2 + tid * K, S.y2 + tid * K}, r.seq,
+                                r.nx, r.iou);
+            if (live && iou) iou[k] = r.iou;
+            const float g = live ? (grad ? grad[k] : scale) : 0.f;
+            __syncwarp();   // the warp's tile is staged (the crossing queue reads other lanes' pairs)
+            Poly<K> G1, G2;
+            const bool thin = bwd_tile_pair<K, kRefT, TileGeometry<K>, false>(
+                S.x1, S.y1, S.x2, S.y2, r.seq, live ? r.nx : 0, g, live, S.scr, S.queue[tid >> 5], S.lut, G1, G2);
+            if (thin) bwd_thin_redo<K, kRefT, false>(S.x1, S.y1, S.x2, S.y2, r.seq, r.nx, g, S.scr, S.lut, G1, G2);
+            if (live) {
+                store_plane<K>(gx1, k, G1.x);
+                store_plane<K>(gy1, k, G1.y);
+                store_plane<K>(gx2, k, G2.x);
+                store_plane<K>(gy2, k, G2.y);
+            }
+            __syncwarp();   // the tile is restaged next round
+        }
+        __syncthreads();
+        if (tid == 0) S.qn = 0;
+        __syncthreads();
+    }
+}
+
+namespace {
+int refine_grid(int64_t n)
+{
+    static DeviceCache cache;
+    const int sms = cache.get([](int dev) {
+        int s = 0;
+        cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+        return s;
+    });
+    const int64_t nchunks = (refine_words(n) + kRefChunkWords - 1) / kRefChunkWords;
+    const int64_t g = (int64_t)(sms > 0 ? sms : 148) * 4;
+    return (int)(nchunks < g ? nchunks : g);
+}
+}  // namespace
+
+int refine_grid_for(int64_t n) { return refine_grid(n); }
+size_t refine_workspace_bytes(int64_t n) { return refine_mask_bytes(n); }
 
 namespace {
 template <int K>
@@ -602,27 +784,31 @@ constexpr size_t fused_smem_bytes()
 template <int K>
 cudaError_t launch_fused_k(int64_t n, const float *x1, const float *y1, const float *x2, const float *y2,
                            const float *grad, float scale, float *iou, float *gx1, float *gy1, float *gx2,
-                           float *gy2, cudaStream_t st)
+                           float *gy2, uint32_t *refine, cudaStream_t st)
 {
     constexpr int T = (K == 4) ? kFused4Threads : kFused8Threads;
     constexpr bool PF = (K == 4) ? DGAL_FUSED_PF : DGAL_FUSED8_PF;
     constexpr int64_t per = (int64_t)(PF ? ((K == 4) ? DGAL_FUSED4_NT : DGAL_FUSED8_NT) : 1) * T;
     constexpr size_t smem = fused_smem_bytes<K>();
-    static DeviceCache cache;
+    static DeviceCache cache, rcache;
     const int a = cache.get([&](int) { return set_smem_attr(paired_fused_kernel<K>, smem); });
     if (a <= 0) return (cudaError_t)(-a);
+    const int b = rcache.get([&](int) { return set_smem_attr(paired_fused_refine_kernel<K>, sizeof(RefineSmem<K>)); });
+    if (b <= 0) return (cudaError_t)(-b);
     paired_fused_kernel<K><<<(unsigned)((n + per - 1) / per), T, smem, st>>>(n, x1, y1, x2, y2, grad, scale, iou,
-                                                                               gx1, gy1, gx2, gy2);
+                                                                               gx1, gy1, gx2, gy2, refine);
+    paired_fused_refine_kernel<K><<<(unsigned)refine_grid(n), kRefT, sizeof(RefineSmem<K>), st>>>(
+        n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2, refine);
     return cudaGetLastError();
 }
 }  // namespace
 
 cudaError_t launch_paired_fused(int K, int64_t n, const float *x1, const float *y1, const float *x2,
                                 const float *y2, const float *grad, float scale, float *iou, float *gx1,
-                                float *gy1, float *gx2, float *gy2, cudaStream_t st)
+                                float *gy1, float *gx2, float *gy2, uint32_t *refine, cudaStream_t st)
 {
-    if (K == 4) return launch_fused_k<4>(n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2, st);
-    return launch_fused_k<8>(n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2, st);
+    if (K == 4) return launch_fused_k<4>(n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2, refine, st);
+    return launch_fused_k<8>(n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2, refine, st);
 }
 
 }  // namespace dgal

@@ -19,5 +19,6 @@ from .generators import (  # noqa: F401
     gen_cfg5_scene,
     gen_config,
     gen_quad_pairs,
+    gen_thin_pairs,
     seed_for,
 )

@@ -399,6 +399,47 @@ def gen_quad_pairs(n: int = 4096, seed: int | None = None) -> PairBatch:
 
 
 # ----------------------------------------------------------------------------
+# thin / sliver polygons (test workload: "numerical stability ... arbitrary
+# shape input"; the float conditioning of the area sum on high-aspect shapes)
+# ----------------------------------------------------------------------------
+def _thin_poly(rng, m, verts, c, a, b, phi):
+    """`verts`-gons inscribed in ellipses (semi-axes a >> b, orientation phi): angles
+    (k + U(-0.3, 0.3)) 2 pi / verts + phi0 — in angular order, so convex and CCW."""
+    phi0 = rng.uniform(0, 2 * math.pi, size=m)
+    k = np.arange(verts)[None, :]
+    alpha = (k + rng.uniform(-0.3, 0.3, size=(m, verts))) * (2 * math.pi / verts) + phi0[:, None]
+    ex, ey = a[:, None] * np.cos(alpha), b[:, None] * np.sin(alpha)
+    cp, sp = np.cos(phi)[:, None], np.sin(phi)[:, None]
+    return c[:, :1] + cp * ex - sp * ey, c[:, 1:] + sp * ex + cp * ey
+
+
+def gen_thin_pairs(n: int, K: int, verts: int, aspect: float, seed: int | None = None,
+                   extent: float = 354.0) -> PairBatch:
+    """Pairs of thin convex `verts`-gons (verts <= K; padded to K by repeating the last
+    vertex, include/dgal.h) of aspect ratio `aspect` (ellipse semi-axes a, a / aspect,
+    a ~ U[1, 30] m), centred anywhere in [-extent, extent]^2 (scene coordinates, the
+    nuScenes square of cfg5).  The partner's centre lies inside p1's ellipse; half the
+    pairs cross at a random angle (sliver intersections far from both polygons'
+    vertices), half overlap lengthwise (orientation N(0, 0.05^2)).  Tests only."""
+    seed = BASE_SEED + 61 + 1000 * K + 100 * verts + int(aspect) if seed is None else seed
+    rng = np.random.Generator(np.random.PCG64(seed))
+    c1 = rng.uniform(-extent, extent, size=(n, 2))
+    a1 = rng.uniform(1, 30, size=n)
+    phi1 = rng.uniform(-math.pi, math.pi, size=n)
+    x1, y1 = _thin_poly(rng, n, verts, c1, a1, a1 / aspect, phi1)
+    u, v = rng.uniform(-0.8, 0.8, size=n) * a1, rng.uniform(-0.5, 0.5, size=n) * (a1 / aspect)
+    c2 = c1 + np.stack([np.cos(phi1) * u - np.sin(phi1) * v, np.sin(phi1) * u + np.cos(phi1) * v], 1)
+    a2 = rng.uniform(1, 30, size=n)
+    cross_ = rng.uniform(size=n) < 0.5
+    phi2 = phi1 + np.where(cross_, rng.uniform(-math.pi, math.pi, size=n), rng.normal(0, 0.05, size=n))
+    x2, y2 = _thin_poly(rng, n, verts, c2, a2, a2 / aspect, phi2)
+    pad = lambda a: np.concatenate([a, np.repeat(a[:, -1:], K - verts, 1)], 1)  # noqa: E731
+    f = lambda a: np.ascontiguousarray(pad(a).astype(np.float32).reshape(-1))  # noqa: E731
+    g = rng.uniform(-1, 1, size=n).astype(np.float32)
+    return PairBatch(Polys(f(x1), f(y1), K), Polys(f(x2), f(y2), K), g)
+
+
+# ----------------------------------------------------------------------------
 # cfg5: nuScenes-like clustered proposals
 # ----------------------------------------------------------------------------
 # (share, length, width)

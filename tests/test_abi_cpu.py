@@ -26,7 +26,7 @@ def test_header_declares_the_boundary():
     names = _declared()
     assert names == sorted(["dgal_iou_paired_fwd", "dgal_iou_paired_bwd", "dgal_iou_paired_fused",
                             "dgal_box_iou_paired_fwd", "dgal_box_iou_paired_bwd", "dgal_box_iou_paired_fused",
-                            "dgal_iou_pairwise",
+                            "dgal_iou_pairwise", "dgal_fused_workspace_bytes",
                             "dgal_pairwise_workspace_bytes", "dgal_nms_round", "dgal_nms_keep",
                             "dgal_status_string", "dgal_build_info"])
 
@@ -65,13 +65,24 @@ def test_host_side_validation_without_gpu():
     assert L.dgal_iou_paired_fwd(4, 8, P(a + 4), P(a), P(a), P(a), P(a), P(a), P(a), None) == 3
     # misaligned xflags for K=8 (needs 16 B)
     assert L.dgal_iou_paired_fwd(8, 8, P(a), P(a), P(a), P(a), P(a), P(a), P(a + 8), None) == 3
-    # fused: misaligned dL/dIoU or IoU output (4 B), misaligned gradient plane (16 B)
-    assert L.dgal_iou_paired_fused(4, 8, P(a), P(a), P(a), P(a), P(a + 2), ctypes.c_float(1.0), None,
-                                   P(a), P(a), P(a), P(a), None) == 3
-    assert L.dgal_iou_paired_fused(4, 8, P(a), P(a), P(a), P(a), None, ctypes.c_float(1.0), P(a + 1),
-                                   P(a), P(a), P(a), P(a), None) == 3
-    assert L.dgal_iou_paired_fused(8, 8, P(a), P(a), P(a), P(a), None, ctypes.c_float(1.0), None,
-                                   P(a), P(a + 8), P(a), P(a), None) == 3
+    # fused: misaligned dL/dIoU or IoU output (4 B), misaligned gradient plane (16 B),
+    # refine workspace missing / too small / misaligned
+    ws = L.dgal_fused_workspace_bytes(8)
+    assert ws == 8 and L.dgal_fused_workspace_bytes(1 << 24) == 4 * (1 << 19)
+    assert L.dgal_fused_workspace_bytes(65) == 16        # 3 words -> two 8-byte vectors
+    F1 = ctypes.c_float(1.0)
+    assert L.dgal_iou_paired_fused(4, 8, P(a), P(a), P(a), P(a), P(a + 2), F1, None,
+                                   P(a), P(a), P(a), P(a), P(a), ws, None) == 3
+    assert L.dgal_iou_paired_fused(4, 8, P(a), P(a), P(a), P(a), None, F1, P(a + 1),
+                                   P(a), P(a), P(a), P(a), P(a), ws, None) == 3
+    assert L.dgal_iou_paired_fused(8, 8, P(a), P(a), P(a), P(a), None, F1, None,
+                                   P(a), P(a + 8), P(a), P(a), P(a), ws, None) == 3
+    assert L.dgal_iou_paired_fused(4, 8, P(a), P(a), P(a), P(a), None, F1, None,
+                                   P(a), P(a), P(a), P(a), None, ws, None) == 1
+    assert L.dgal_iou_paired_fused(4, 8, P(a), P(a), P(a), P(a), None, F1, None,
+                                   P(a), P(a), P(a), P(a), P(a), ws - 1, None) == 1
+    assert L.dgal_iou_paired_fused(4, 8, P(a), P(a), P(a), P(a), None, F1, None,
+                                   P(a), P(a), P(a), P(a), P(a + 4), ws, None) == 3
     # n == 0 is a no-op
     assert L.dgal_iou_paired_fwd(4, 0, None, None, None, None, None, None, None, None) == 0
     assert L.dgal_iou_paired_bwd(4, 0, *([None] * 11), None) == 0
@@ -83,7 +94,9 @@ def test_host_side_validation_without_gpu():
     assert L.dgal_box_iou_paired_fwd(2, 0, 8, P(a), P(a), P(a), P(a), P(a + 4), None) == 3
     assert L.dgal_box_iou_paired_fwd(2, 0, 0, None, None, None, None, None, None) == 0
     assert L.dgal_box_iou_paired_bwd(3, 0, 8, P(a), P(a), None, P(a), P(a), P(a), P(a), None) == 1
-    assert L.dgal_box_iou_paired_fused(2, 0, 8, P(a), P(a), None, 1.0, None, None, P(a), None) == 1
+    assert L.dgal_box_iou_paired_fused(2, 0, 8, P(a), P(a), None, 1.0, None, None, P(a), P(a), 8, None) == 1
+    assert L.dgal_box_iou_paired_fused(2, 0, 8, P(a), P(a), None, 1.0, None, P(a), P(a), None, 8, None) == 1
+    assert L.dgal_box_iou_paired_fused(2, 0, 8, P(a), P(a), None, 1.0, None, P(a), P(a), P(a + 4), 8, None) == 3
     # pairwise: nothing requested, negative threshold with a mask, short mask rows
     args = [4, 8, P(a), P(a), 8, P(a), P(a), 0]
     assert L.dgal_iou_pairwise(*args, None, 0.5, None, 0, None, None, 0, None, 0, None) == 1

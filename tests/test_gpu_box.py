@@ -213,11 +213,11 @@ def test_near_coincident_boxes_iou(scale):
     assert_iou_close(iou3, ref3)
 
 
-@pytest.mark.parametrize("scale", [1e-6, 1e-5, 1e-4])
+@pytest.mark.parametrize("scale", [1e-6, 1e-5, 1e-4, 1e-3, 1e-2])
 def test_near_coincident_box_gradients(scale):
     """Prediction ~ target boxes: on the pairs whose flags equal the oracle's, the box
-    parameter gradients match it (the ill-conditioned crossings are refined on corners
-    rebuilt in double from the parameters)."""
+    parameter gradients match it (the ill-conditioned crossings, |sin| < 2^-7, are
+    refined on corners rebuilt in double from the parameters)."""
     from test_gpu_paired import _near_coincident_boxes
     b1, b2 = _near_coincident_boxes(50_000, scale, seed=40 + int(-math.log10(scale)))
     g = np.random.default_rng(6).uniform(-1, 1, b1.shape[1]).astype(np.float32)
@@ -227,3 +227,31 @@ def test_near_coincident_box_gradients(scale):
     assert same.mean() > 0.8          # the rest sit within rounding of a flag change (exact ties at 1e-6)
     assert_grad_close(g1.T[same], ref["gb1"][same])
     assert_grad_close(g2.T[same], ref["gb2"][same])
+
+
+@pytest.mark.parametrize("dims", [2, 3])
+@pytest.mark.parametrize("scale", [1e-6, 1e-5, 1e-4, 1e-3, 1e-2])
+def test_box_fused_near_coincident(dims, scale):
+    """The fused box loss kernel on prediction ~ target pairs: IoU within 1e-5 on every
+    pair, parameter gradients at the north_star tolerance wherever the split forward's
+    flags equal the oracle's (nearly parallel edge pairs are redone by the refine pass
+    with the box split path's exact crossings, include/dgal.h)."""
+    from test_gpu_paired import _near_coincident_boxes
+    n = 40_000
+    b1, b2 = _near_coincident_boxes(n, scale, seed=60 + dims + int(-math.log10(scale)))
+    rng = np.random.default_rng(dims)
+    if dims == 3:
+        z = rng.normal(-1, 0.4, n); d = rng.uniform(1.4, 1.9, n)
+        dz = scale * rng.normal(size=n) + 0.05 * rng.uniform(0.5, 1, n)   # z extents away from ties
+        b1 = np.concatenate([b1[:2], z[None], b1[2:4], d[None], b1[4:]]).astype(np.float32)
+        b2 = np.concatenate([b2[:2], (z + dz)[None], b2[2:4], d[None], b2[4:]]).astype(np.float32)
+    g = rng.uniform(-1, 1, n).astype(np.float32)
+    B1, B2 = torch.from_numpy(np.ascontiguousarray(b1)).to(dev()), torch.from_numpy(np.ascontiguousarray(b2)).to(dev())
+    _, nx, xf = dgal.box_iou_paired_fwd(B1, B2)
+    iou, g1, g2 = dgal.box_iou_paired_fused(B1, B2, grad=torch.from_numpy(g).to(dev()))
+    ref = oracle.box_iou_paired(b1.T.astype(np.float64), b2.T.astype(np.float64), g.astype(np.float64))
+    assert_iou_close(iou.cpu().numpy(), ref["iou"])
+    same = (nx.cpu().numpy() == ref["nx"]) & np.all(xf.cpu().numpy() == ref["xflags"], 1)
+    assert same.mean() > 0.8
+    assert_grad_close(g1.cpu().numpy().T[same], ref["gb1"][same])
+    assert_grad_close(g2.cpu().numpy().T[same], ref["gb2"][same])

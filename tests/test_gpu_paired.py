@@ -253,11 +253,15 @@ def test_fused_consistent_with_split_and_pairwise():
     assert torch.allclose(iou_f, iou_s, atol=2e-6, rtol=0)
     for a, c in zip(gf, gs):
         assert torch.allclose(a, c, atol=1e-4, rtol=1e-3)
-    # the fused IoU is bitwise the pairwise (flag-free) IoU of the same pairs
+    # the fused IoU is bitwise the pairwise (flag-free) IoU of the same pairs, except on
+    # the pairs the refine pass redid with the split forward (include/dgal.h)
     m = 256
     pw, _, _, _ = dgal.iou_pairwise(x1[:m].contiguous(), y1[:m].contiguous(), x2[:m].contiguous(),
                                     y2[:m].contiguous(), want_mask=False)
-    assert torch.equal(pw.diagonal(), iou_f[:m])
+    d = pw.diagonal() != iou_f[:m]
+    assert int(d.sum()) <= m // 10
+    assert torch.allclose(pw.diagonal(), iou_f[:m], atol=2e-6, rtol=0)
+    assert torch.equal(iou_f[:m][d], iou_s[:m][d])
     # scalar mode == constant array; bitwise linearity in dL/dIoU
     s = -1.0 / 4096
     _, *ga = dgal.iou_paired_fused(x1, y1, x2, y2, scale=s)
@@ -415,3 +419,67 @@ def test_padded_polygons(m, K):
         folded = got[:, :m].copy()
         folded[:, m - 1] += got[:, m:].sum(1)
         assert_grad_close(folded, want)
+
+
+def _near_octagons(n, scale, seed):
+    """Convex octagons (ellipse-inscribed, as cfg4) and a copy with EVERY vertex moved by
+    ~scale x size (convex at these scales; no exactly shared vertex, so the flags are
+    those of nearly parallel crossings, not of exact ties)."""
+    rng = np.random.default_rng(seed)
+    c = rng.uniform(-10, 10, (n, 2))
+    a = rng.uniform(1, 3, n)
+    b = a * rng.uniform(0.6, 1.0, n)
+    phi = rng.uniform(-np.pi, np.pi, n)
+    ang = (np.arange(8)[None, :] + rng.uniform(-0.3, 0.3, (n, 8))) * np.pi / 4
+    ex, ey = a[:, None] * np.cos(ang), b[:, None] * np.sin(ang)
+    x1 = c[:, :1] + np.cos(phi)[:, None] * ex - np.sin(phi)[:, None] * ey
+    y1 = c[:, 1:] + np.sin(phi)[:, None] * ex + np.cos(phi)[:, None] * ey
+    x2 = x1 + rng.normal(size=x1.shape) * scale * a[:, None]
+    y2 = y1 + rng.normal(size=y1.shape) * scale * a[:, None]
+    return tuple(np.ascontiguousarray(v.astype(np.float32)) for v in (x1, y1, x2, y2))
+
+
+@pytest.mark.parametrize("K", [4, 8])
+@pytest.mark.parametrize("scale", [1e-6, 1e-5, 1e-4, 1e-3, 1e-2])
+def test_fused_near_coincident_gradients(K, scale):
+    """The fused loss kernel on prediction ~ target pairs (the regime an IoU loss ends
+    training in): IoU within 1e-5 on every pair, and wherever the split forward's flags
+    equal the oracle's, the fused vertex gradients match the oracle at the north_star
+    tolerance — nearly parallel edge pairs are marked and redone by the refine pass with
+    the split path's exact crossings (include/dgal.h)."""
+    seed = 40 + int(-math.log10(scale)) + K
+    if K == 4:
+        b1, b2 = _near_coincident_boxes(50_000, scale, seed=seed)
+        x1, y1 = oracle.box_corners(b1.T.astype(np.float64))
+        x2, y2 = oracle.box_corners(b2.T.astype(np.float64))
+        x1, y1, x2, y2 = (np.ascontiguousarray(a.astype(np.float32)) for a in (x1, y1, x2, y2))
+    else:
+        x1, y1, x2, y2 = _near_octagons(30_000, scale, seed)
+    n = x1.shape[0]
+    g = np.random.default_rng(seed).uniform(-1, 1, n).astype(np.float32)
+    T = lambda a: torch.from_numpy(a).to(dev())  # noqa: E731
+    X = (T(x1), T(y1), T(x2), T(y2))
+    _, nx, xf = dgal.iou_paired_fwd(*X)
+    iou_f, *gf = dgal.iou_paired_fused(*X, grad=T(g))
+    rf = oracle.iou_paired_fwd((x1, y1), (x2, y2))
+    assert_iou_close(iou_f.cpu().numpy(), rf["iou"])
+    same = (nx.cpu().numpy() == rf["nx"]) & np.all(xf.cpu().numpy() == rf["xflags"], 1)
+    assert same.mean() > 0.8
+    ref = oracle.iou_paired_bwd((x1, y1), (x2, y2), g)
+    for got, want in zip(gf, ref):
+        assert_grad_close(got.cpu().numpy()[same], want[same])
+
+
+def test_fused_workspace_stays_zero_and_reusable():
+    """The refine mask is left all-zero by every call (include/dgal.h), so one workspace
+    serves consecutive calls; results are bitwise repeatable."""
+    b1, b2 = _near_coincident_boxes(20_000, 1e-4, seed=7)
+    x1, y1 = oracle.box_corners(b1.T.astype(np.float64))
+    x2, y2 = oracle.box_corners(b2.T.astype(np.float64))
+    X = [torch.from_numpy(np.ascontiguousarray(a.astype(np.float32))).to(dev()) for a in (x1, y1, x2, y2)]
+    ws = torch.zeros(dgal.lib().dgal_fused_workspace_bytes(20_000), dtype=torch.uint8, device=dev())
+    r1 = dgal.iou_paired_fused(*X, scale=0.25, workspace=ws)
+    assert int(ws.count_nonzero()) == 0
+    r2 = dgal.iou_paired_fused(*X, scale=0.25, workspace=ws)
+    for a_, b_ in zip(r1, r2):
+        assert torch.equal(a_, b_)

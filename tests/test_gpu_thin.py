@@ -1,0 +1,72 @@
+"""GPU parity on thin / sliver polygons (§V: "improve the numerical stability
+... arbitrary shape input"; north_star tolerances): synth.gen_thin_pairs, aspect
+30-300, scene coordinates up to +-354 m, padded triangles / quads for K=4 and
+octagon / pentagon slivers for K=8.  The float area sum of such pairs is
+ill-conditioned (~eps R^2 against an area ~R^2 / aspect); the kernels detect them
+(R^2 > kThinRatio A_u) and redo the area of the recorded intersection in double
+(csrc/dgal_exact.cuh).  IoU is compared on EVERY pair (R18), flags and vertex
+gradients on the margin pairs (R13); padded vertices' gradients are folded onto
+the last real vertex (include/dgal.h)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2011_11134_b200 as dgal
+import synth
+from gpu_util import assert_flags_exact, assert_grad_close, assert_iou_close, dev
+
+pytestmark = pytest.mark.gpu
+
+CASES = [(K, v, a) for K, v in ((4, 3), (4, 4), (8, 8), (8, 5)) for a in (30.0, 100.0, 300.0)]
+N = 20000
+
+
+def _case(K, verts, aspect):
+    b = synth.gen_thin_pairs(N, K, verts, aspect)
+    X = [torch.from_numpy(a.reshape(N, K)).to(dev()) for a in (b.p1.x, b.p1.y, b.p2.x, b.p2.y)]
+    un = lambda a: a.reshape(N, K)[:, :verts].astype(np.float64)  # noqa: E731
+    p1, p2 = (un(b.p1.x), un(b.p1.y)), (un(b.p2.x), un(b.p2.y))
+    return b, X, p1, p2
+
+
+def _fold(g, verts):
+    g = g.cpu().numpy().astype(np.float64)
+    f = g[:, :verts].copy()
+    f[:, verts - 1] += g[:, verts:].sum(1)
+    return f
+
+
+@pytest.mark.parametrize("K,verts,aspect", CASES)
+def test_thin_split_path(K, verts, aspect):
+    b, X, p1, p2 = _case(K, verts, aspect)
+    iou, nx, xf = dgal.iou_paired_fwd(*X)
+    g = torch.from_numpy(b.grad).to(dev())
+    gr = dgal.iou_paired_bwd(*X, g, nx, xf)
+    ref = oracle.iou_paired_fwd(p1, p2)
+    assert (ref["iou"] > 0).mean() > 0.85             # the workload does overlap
+    assert_iou_close(iou.cpu().numpy(), ref["iou"])
+    ok = oracle.margin_ok(p1, p2)
+    assert ok.mean() > 0.5
+    # flags of the padded polygons: indices of the real vertices / edges are the same
+    # (the repeated vertex's zero-length edge never carries a crossing)
+    nxk = nx.cpu().numpy()
+    xfk = xf.cpu().numpy()
+    if verts == K:
+        assert_flags_exact(nxk[ok], xfk[ok], {"nx": ref["nx"][ok], "xflags": ref["xflags"][ok]})
+    rg = oracle.iou_paired_bwd(p1, p2, b.grad)
+    for got, want in zip(gr, rg):
+        assert_grad_close(_fold(got, verts)[ok], want[ok])
+
+
+@pytest.mark.parametrize("K,verts,aspect", CASES)
+def test_thin_fused(K, verts, aspect):
+    b, X, p1, p2 = _case(K, verts, aspect)
+    g = torch.from_numpy(b.grad).to(dev())
+    iou, *gr = dgal.iou_paired_fused(*X, grad=g)
+    ref = oracle.iou_paired_fwd(p1, p2)
+    assert_iou_close(iou.cpu().numpy(), ref["iou"])
+    ok = oracle.margin_ok(p1, p2)
+    rg = oracle.iou_paired_bwd(p1, p2, b.grad)
+    for got, want in zip(gr, rg):
+        assert_grad_close(_fold(got, verts)[ok], want[ok])

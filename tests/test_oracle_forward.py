@@ -374,6 +374,22 @@ def test_canonical_start_convention(cfg):
         assert a > 0
 
 
+CANON = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "canonical_start.json")))
+
+
+@pytest.mark.parametrize("case", CANON["cases"], ids=lambda c: c["name"])
+def test_canonical_start_hand_derived(case):
+    """R3 pinned to hand-derived sequences (tests/golden/canonical_start.json): the
+    start is the smallest position i + t along p1's boundary, with t measured on
+    p1's edge (case 1 would start elsewhere with t taken on p2's edge), not the
+    smallest byte (cases 2, 3), wrapping through p1's closing edge (case 3)."""
+    P, Q = np.array(case["p1"], float), np.array(case["p2"], float)
+    iou, nx, fl, ai = fwd1(P, Q)
+    assert nx == case["nx"] and fl == case["xflags"]
+    assert abs(ai - case["area_i"][0] / case["area_i"][1]) < 1e-14
+    assert abs(iou - case["iou"][0] / case["iou"][1]) < 1e-14
+
+
 # --- degenerate geometry pinned to closed forms (R5 boundary-inclusive) --------
 def test_nested_collinear_boxes_closed_form():
     """Same centre, height and yaw, widths w and w(1 - delta): p2 inside p1 with two
