@@ -290,12 +290,13 @@ __device__ __forceinline__ bool pair_is_thin(float R2, float aux2)
     return R2 > (0.5f * kThinRatio) * aux2;
 }
 
-// the backward's form (its area is a sum of piece terms about p1.v0, not the forward's
-// per-event terms): sum |terms| = A1x2 + sum_j |C2_j| over twice the union area,
-// against the same ratio (<= 2 for two overlapping fat polygons: 2 A_1 + 2 A_2 <= 4 A_u)
-__device__ __forceinline__ bool pair_is_thin_sum(float absx2, float aux2)
+// the backward's form (its area is a sum of piece terms about p1.v0, whose rounding
+// is bounded by ~2 eps S, S = sum over the 2K vertices of |v|^2 <= 2K R^2): thin when
+// S > 2K kThinRatio A_u (= 4 K kThinRatio / 2 aux2; cfg3 box pairs have S / aux2 ~ 2-6)
+template <int K>
+__device__ __forceinline__ bool pair_is_thin_sum(float S, float aux2)
 {
-    return absx2 > (0.5f * kThinRatio) * aux2;
+    return S > (float)(K * kThinRatio) * aux2;
 }
 
 // ---------------------------------------------------------------------------
@@ -423,7 +424,7 @@ struct Clip {
     float A1x2, A2x2, Aix2;            // twice the areas
     bool nonempty;
     bool sep;                          // a p2 edge line separates p1 (strictly): empty for sure
-    bool ill;                          // ILL: some (p1 edge, p2 line) has |sin| < kIllSin
+    bool ill;                          // ILL: some p1 edge crosses a p2 line at |sin| < kIllSin
 };
 
 // |sin| of the angle between a p1 edge and a p2 edge below which the fused kernels
@@ -452,13 +453,24 @@ struct QTable {
     int stride;
 };
 
-// ILL: also report whether any (p1 edge i, p2 line j) pair is nearly parallel,
-// |g_i x f_j| < kIllSin |g_i| |f_j| (c.ill; the Cyrus-Beck denominators are exactly
-// these cross products) — a superset of the pairs with an ill-conditioned crossing.
+// Per-thread shared-memory table of the ILL test's per-line factors for K = 8 (in
+// registers they spill the K = 8 fused kernel): the pair (2q, 2q+1) at p[q * st].
+struct IllTab {
+    uint64_t *p;
+    int st;
+    float sin = kIllSin;   // the |sin| threshold (boxes: their corners' rounding needs a larger one)
+};
+
+// ILL: also report whether some p1 edge i CROSSES some p2 line j (its end points on
+// opposite sides: a candidate crossing of the Cyrus-Beck update) while being nearly
+// parallel to it, |g_i x f_j| < kIllSin |g_i| |f_j| (c.ill; the Cyrus-Beck
+// denominators are exactly these cross products) — a superset of the pairs with an
+// ill-conditioned crossing (nearly parallel edges that do not cross — the opposite
+// sides of two nearly aligned boxes — do not count: ~100x fewer pairs marked).
 template <int K, int MODE, bool ILL = false>
 __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &Q, Clip<K> &c,
                                                QTable qt = QTable{nullptr, nullptr, 0},
-                                               const WalkLut4 *wl = nullptr)
+                                               const WalkLut4 *wl = nullptr, IllTab it = IllTab{nullptr, 0})
 {
     const bool LUT = (K == 4) && wl != nullptr;   // in2 from the table (wl in shared memory)
     constexpr bool PIECES = (MODE == kP2Pieces || MODE == kP2PiecesSmem);
@@ -531,21 +543,33 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     float *t0 = c.t0, *t1 = c.t1;
     uint32_t jin = 0, jout = 0, valid = 0, enter = 0, leave = 0;
     const float hi0 = __int_as_float(0x3F800008);
-    // ILL: min over (i, j) of den^2 - sin^2 |g_i|^2 |f_j|^2 (negative: nearly parallel)
-    // (K = 4: inside the edge loop, from its Cyrus-Beck denominators, with the
-    // per-line factors -sin^2 |f_j|^2 precomputed; K = 8: in a separate pass over
-    // the edge vectors after the loop — inside it, 8 more live registers spill)
-    float illm = 1.f;
-    constexpr bool ILL_LOOP = ILL && (K == 4);
-    uint64_t nsf[ILL ? K / 2 : 1];
-    const uint64_t ns2 = f2pack(-kIllSin * kIllSin, -kIllSin * kIllSin);
-    auto nsf_q = [&](int q) {
-        const uint64_t fx2 = f2pack(fx[2 * q], fx[2 * q + 1]), fy2 = f2pack(fy[2 * q], fy[2 * q + 1]);
-        return f2mul(f2fma(fx2, fx2, f2mul(fy2, fy2)), ns2);
-    };
-    if (ILL_LOOP) {
+    // ILL, inside the edge loop from its Cyrus-Beck denominators: candidate (i, j) is
+    // ill when x = den^2 - sin^2 |g_i|^2 |f_j|^2 < 0 AND p = d[i][j] d[i+1][j] < 0 (a
+    // crossing, or an end point exactly on the line); both signs AND-ed into one accumulator (one LOP3 per candidate).  The
+    // per-line factors -sin^2 |f_j|^2 live in registers (K = 4) or in the caller's
+    // shared-memory table it (K = 8).
+    // (K = 8 folds the longest p1 edge's |g|^2 into the table instead of each edge's:
+    // one register pair less in the loop, which is at its budget; conservative — a
+    // shorter edge is tested against a larger |sin| threshold)
+    uint32_t illacc = 0u;
+    constexpr bool NSF_REG = (K == 4) || !ILL;
+    uint64_t nsf[(ILL && NSF_REG) ? K / 2 : 1];
+    if (ILL) {
+        float gmax = 1.f;
+        if (!NSF_REG) {
+            gmax = 0.f;
 #pragma unroll
-        for (int q = 0; q < K / 2; ++q) nsf[q] = nsf_q(q);
+            for (int i = 0; i < K; ++i) gmax = fmaxf(gmax, fmaf(gx[i], gx[i], gy[i] * gy[i]));
+        }
+        const float ns = -it.sin * it.sin * gmax;
+        const uint64_t ns2 = f2pack(ns, ns);
+#pragma unroll
+        for (int q = 0; q < K / 2; ++q) {
+            const uint64_t fx2 = f2pack(fx[2 * q], fx[2 * q + 1]), fy2 = f2pack(fy[2 * q], fy[2 * q + 1]);
+            const uint64_t v = f2mul(f2fma(fx2, fx2, f2mul(fy2, fy2)), ns2);
+            if (NSF_REG) nsf[NSF_REG ? q : 0] = v;
+            else it.p[q * it.st] = v;
+        }
     }
     // Events (same pass).  An exit of p1 edge i through p2 line j_out starts the p2
     // piece on edge j_out at X_out = v_i + t1 g_i; an entry through line j_in ends
@@ -591,8 +615,8 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
         }
         float lo = 0.f, hi = hi0;
         uint64_t g2 = 0ull;
-        float gg = 0.f;
-        if (ILL_LOOP) {
+        float gg = 1.f;
+        if (ILL && NSF_REG) {
             gg = fmaf(gx[i], gx[i], gy[i] * gy[i]);
             g2 = f2pack(gg, gg);
         }
@@ -601,13 +625,18 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
 #pragma unroll
             for (int q = 0; q < K / 2; ++q) {
                 const uint64_t a = f2pack(dc[2 * q], dc[2 * q + 1]);
-                const uint64_t den = f2add(f2sub(a, f2pack(dn[2 * q], dn[2 * q + 1])), tiny2);
+                const uint64_t bq = f2pack(dn[2 * q], dn[2 * q + 1]);
+                const uint64_t den = f2add(f2sub(a, bq), tiny2);
                 float d0_, d1_;
                 f2unpack(den, d0_, d1_);
-                if (ILL_LOOP) {
-                    float x0, x1;
-                    f2unpack(f2fma(den, den, f2mul(g2, nsf[q])), x0, x1);
-                    illm = fminf(illm, fminf(x0, x1));
+                if (ILL) {
+                    const uint64_t thr = NSF_REG ? f2mul(g2, nsf[NSF_REG ? q : 0]) : it.p[q * it.st];
+                    float x0, x1, p0, p1;
+                    f2unpack(f2fma(den, den, thr), x0, x1);
+                    // (- 1e-26: an end point exactly on the line, d = +tiny = 1e-30, counts as a
+                    // crossing for |d| of the other end up to 1e4)
+                    f2unpack(f2fma(a, bq, f2pack(-1e-26f, -1e-26f)), p0, p1);
+                    illacc |= (__float_as_uint(x0) & __float_as_uint(p0)) | (__float_as_uint(x1) & __float_as_uint(p1));
                 }
                 const uint64_t r = f2pack(rcp_approx(d0_), rcp_approx(d1_));
                 const uint64_t m = f2pack(__saturatef(-d0_ * kBig), __saturatef(-d1_ * kBig));
@@ -625,10 +654,11 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
             for (int j = 0; j < K; ++j) {
                 const float a = dc[j], b = dn[j];
                 const float den = (a - b) + kTiny;
-                if (ILL_LOOP) {
+                if (ILL) {
                     float nf0, nf1;
-                    f2unpack(nsf[j / 2], nf0, nf1);
-                    illm = fminf(illm, fmaf(den, den, gg * ((j & 1) ? nf1 : nf0)));
+                    f2unpack(NSF_REG ? nsf[NSF_REG ? j / 2 : 0] : it.p[(j / 2) * it.st], nf0, nf1);
+                    illacc |= __float_as_uint(fmaf(den, den, gg * ((j & 1) ? nf1 : nf0))) &
+                              __float_as_uint(fmaf(a, b, -1e-26f));
                 }
                 const float r = rcp_approx(den);
                 const float m = __saturatef(-den * kBig);  // 1: bounds below
@@ -703,23 +733,6 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     bool separated = false;
 #pragma unroll
     for (int j = 0; j < K; ++j) separated |= (m1[j] < kTiny);
-    if (ILL && !ILL_LOOP) {   // (g_i x f_j)^2 - sin^2 |g_i|^2 |f_j|^2 over all (i, j), lines paired
-#pragma unroll
-        for (int q = 0; q < K / 2; ++q) nsf[q] = nsf_q(q);
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            const float gg = fmaf(gx[i], gx[i], gy[i] * gy[i]);
-            const uint64_t g2 = f2pack(gg, gg), GX = f2pack(gx[i], gx[i]), NGY = f2pack(-gy[i], -gy[i]);
-#pragma unroll
-            for (int q = 0; q < K / 2; ++q) {
-                const uint64_t fx2 = f2pack(fx[2 * q], fx[2 * q + 1]), fy2 = f2pack(fy[2 * q], fy[2 * q + 1]);
-                const uint64_t cr = f2fma(GX, fy2, f2mul(NGY, fx2));
-                float x0, x1;
-                f2unpack(f2fma(cr, cr, f2mul(g2, nsf[q])), x0, x1);
-                illm = fminf(illm, fminf(x0, x1));
-            }
-        }
-    }
     c.jin = jin; c.jout = jout; c.valid = valid; c.enter = enter; c.leave = leave;
     if (PSMEM) {
 #pragma unroll
@@ -779,7 +792,7 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     c.in2 = in2;
     c.nonempty = !separated && (Aix2 > 0.f);
     c.sep = separated;
-    c.ill = ILL && (illm < 0.f);
+    c.ill = ILL && (illacc >> 31) != 0u;
 }
 
 // p1, p2 must already be recentred on o = p1.v0 (p1.x[0] == p1.y[0] == 0).
@@ -924,16 +937,17 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
 template <int K, int MODE = kP2Pieces, bool PK = false>
 __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, float g, Poly<K> &G1,
                                            Poly<K> &G2, const Extrude ex = flat(), VolCoef *co = nullptr,
-                                           QTable qt = QTable{nullptr, nullptr, 0}, bool *need = nullptr)
+                                           QTable qt = QTable{nullptr, nullptr, 0}, bool *need = nullptr,
+                                           IllTab it = IllTab{nullptr, 0})
 {
 #pragma unroll
     for (int k = 0; k < K; ++k) { G1.x[k] = 0.f; G1.y[k] = 0.f; G2.x[k] = 0.f; G2.y[k] = 0.f; }
     if (co) *co = VolCoef{0.f, 0.f, 0.f, 0.f, 0.f};
-    const float R2 = need ? pair_extent2<K>(P, Q) : 0.f;
     if (need) *need = false;
     Clip<K> c;
-    if (need) clip_intervals<K, MODE, true>(P, Q, c, qt);
+    if (need) clip_intervals<K, MODE, true>(P, Q, c, qt, nullptr, it);
     else clip_intervals<K, MODE, false>(P, Q, c, qt);
+    const float R2 = need ? pair_extent2<K>(P, Q) : 0.f;   // (after the clip: not live through it)
     if (!c.nonempty) {
         // a thin pair's float area may be <= 0 although p1 and p2 overlap: the refine
         // pass decides (when the pair is not separated and has a boundary piece)
@@ -1184,7 +1198,8 @@ __device__ __forceinline__ void bwd_crossing_exact(const float *sPx, const float
 // it in *ovr, which replaces the float sum in the S:303 coefficients (the piece
 // weights stay the float ones: they need ~1e-7, not 1e-16; so do A_1, A_2, whose
 // float sums are accurate to ~eps R^2 / A — only a sliver intersection's is not).
-template <int K, int TILE, bool PK = false>
+// OVR3: *ovr holds {A_i, A_1, A_2} (twice each), all three replacing the float sums.
+template <int K, int TILE, bool PK = false, bool OVR3 = false>
 __device__ __forceinline__ bool bwd_epilogue(const float *sPx, const float *sPy, const float *sQx,
                                              const float *sQy, float g, uint32_t V, const float *scr,
                                              Poly<K> &G1, Poly<K> &G2, const Extrude ex = flat(),
@@ -1247,18 +1262,17 @@ __device__ __forceinline__ bool bwd_epilogue(const float *sPx, const float *sPy,
     f2unpack(AIX, ai1, ai2);
     float Aix2 = ai1 + ai2;
     if (ovr) {
-        Aix2 = *ovr;
+        Aix2 = ovr[0];
+        if (OVR3) { A1x2 = ovr[1]; A2x2 = ovr[2]; }
     } else if (DGAL_THIN_BWD) {
-        // the piece sum's rounding: ~eps (sum |L C1| + sum |L C2|) <= eps (A1x2 + sum |C2|)
-        // (C1 >= 0: o = p1.v0 lies in p1); C2 terms are large when p2 is far from o
-        float c2abs = 0.f;
+        // the piece sum's rounding is bounded by ~2 eps sum_k (|v_k|^2 + |w_k|^2)
+        // (|x y'| <= (x^2 + y'^2) / 2 for each product of each shoelace term)
+        uint64_t S2 = 0ull;
 #pragma unroll
-        for (int i = 0; i < K; ++i) {
-            float c1_, c2_;
-            f2unpack(C[i], c1_, c2_);
-            c2abs += fabsf(c2_);
-        }
-        thin = pair_is_thin_sum(A1x2 + c2abs, (A1x2 + A2x2) - Aix2);
+        for (int k = 0; k < K; ++k) S2 = f2fma(X[k], X[k], f2fma(Y[k], Y[k], S2));
+        float s1_, s2_;
+        f2unpack(S2, s1_, s2_);
+        thin = pair_is_thin_sum<K>(s1_ + s2_, (A1x2 + A2x2) - Aix2);
     }
 
     // dIoU/dV_i = (V_u + V_i)/V_u^2, dIoU/dV_1,2 = -V_i/V_u^2; V = A d (2D: d = 1)
@@ -1335,12 +1349,13 @@ __device__ __forceinline__ bool bwd_epilogue(const float *sPx, const float *sPy,
         Aix2 = fmaf(l2, C2[i], Aix2);
     }
     if (ovr) {
-        Aix2 = *ovr;
+        Aix2 = ovr[0];
+        if (OVR3) { A1x2 = ovr[1]; A2x2 = ovr[2]; }
     } else if (DGAL_THIN_BWD) {
-        float c2abs = 0.f;
+        float sq = 0.f;
 #pragma unroll
-        for (int i = 0; i < K; ++i) c2abs += fabsf(C2[i]);
-        thin = pair_is_thin_sum(A1x2 + c2abs, (A1x2 + A2x2) - Aix2);
+        for (int k = 0; k < K; ++k) sq = fmaf(P.x[k], P.x[k], fmaf(P.y[k], P.y[k], fmaf(Q.x[k], Q.x[k], fmaf(Q.y[k], Q.y[k], sq))));
+        thin = pair_is_thin_sum<K>(sq, (A1x2 + A2x2) - Aix2);
     }
 
     // dIoU/dV_i = (V_u + V_i)/V_u^2, dIoU/dV_1,2 = -V_i/V_u^2; V = A d (2D: d = 1)
@@ -1371,6 +1386,63 @@ __device__ __forceinline__ bool bwd_epilogue(const float *sPx, const float *sPy,
     }
     }
     return thin;
+}
+
+// The 2D epilogue in double, for a thin pair (bwd_pair_exact): its vertex gradients
+// are small differences of the intersection and union terms, each ~g L / A_u (L the
+// pair's extent), which float rounds to ~eps g L^2 / A_u — up to 1e-4 absolute at
+// aspect 300.  Same formulas as bwd_epilogue, every quantity in double (the interval
+// end points are the float ones, exact in double); the areas are the exact ones.
+template <int K, int TILE>
+__device__ __forceinline__ void bwd_epilogue_exact(const float *sPx, const float *sPy, const float *sQx,
+                                                   const float *sQy, float g, uint32_t V, const float *scr,
+                                                   const AreasX2 &ar, Poly<K> &G1, Poly<K> &G2)
+{
+#pragma unroll
+    for (int k = 0; k < K; ++k) { G1.x[k] = 0.f; G1.y[k] = 0.f; G2.x[k] = 0.f; G2.y[k] = 0.f; }
+    if (V == 0) return;
+    constexpr uint32_t KMASK = (1u << K) - 1u;
+    const uint32_t v1 = V & KMASK, v2 = (V >> 8) & KMASK;
+    const uint32_t on1m = v1 | ((v1 >> 1) | (v1 << (K - 1))) | (V >> 16);
+    const uint32_t on2m = v2 | ((v2 >> 1) | (v2 << (K - 1))) | (V >> 24);
+    const double Ai = 0.5 * ar.ai, Au = 0.5 * ((ar.a1 + ar.a2) - ar.ai);
+    if (!(Au > 0.0) || !(Ai > 0.0)) return;  // R10 guard
+    const double inv = 1.0 / Au, q = Ai * inv;
+    const double ci = (double)g * ((1.0 + q) * inv);    // dL/dA_i
+    const double hu = 0.5 * ((double)g * (-q * inv));  // dL/dA_1,2 times 1/2 (area_grad)
+    // piece weights of edge i: alpha = l (1 - h), beta = l h (p1: which = 0, p2: 1),
+    // recomputed per use (no arrays: the caller's loop is at its register budget)
+    auto wts = [&](int which, int i, double &alpha, double &beta) {
+        const double t0 = scr[(2 * K * which + i) * TILE], t1 = scr[(2 * K * which + K + i) * TILE];
+        const uint32_t on = which ? on2m : on1m;
+        const double l = ((on >> i) & 1u) ? fmax(t1 - t0, 0.0) : 0.0;
+        beta = l * (0.5 * (t0 + t1));
+        alpha = l - beta;
+    };
+#pragma unroll 1
+    for (int k = 0; k < K; ++k) {
+        const int km = (k + K - 1) % K, k1 = (k + 1) % K;
+        double al, be, bem, alm;
+        // p1 vertex k: edge k (as its start, alpha) and edge k-1 (as its end, beta)
+        wts(0, k, al, be);
+        wts(0, km, alm, bem);
+        const double gxk = (double)sPx[k1] - sPx[k], gyk = (double)sPy[k1] - sPy[k];
+        const double gxm = (double)sPx[k] - sPx[km], gym = (double)sPy[k] - sPy[km];
+        double wa = ci * al + hu, wb = ci * bem + hu;
+        const float g1x = (float)(wa * gyk + wb * gym), g1y = (float)(-(wa * gxk + wb * gxm));
+        wts(1, k, al, be);
+        wts(1, km, alm, bem);
+        const double fxk = (double)sQx[k1] - sQx[k], fyk = (double)sQy[k1] - sQy[k];
+        const double fxm = (double)sQx[k] - sQx[km], fym = (double)sQy[k] - sQy[km];
+        wa = ci * al + hu;
+        wb = ci * bem + hu;
+        const float g2x = (float)(wa * fyk + wb * fym), g2y = (float)(-(wa * fxk + wb * fxm));
+        // (a dynamic k: write through the unrolled selects of the register arrays)
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+            if (q == k) { G1.x[q] = g1x; G1.y[q] = g1y; G2.x[q] = g2x; G2.y[q] = g2y; }
+        }
+    }
 }
 
 // One backward tile: thread tid owns pair tid of a tile of TILE pairs whose
@@ -1502,10 +1574,8 @@ __device__ __forceinline__ void bwd_pair_exact(const float *tx1, const float *ty
             bwd_crossing_exact<K, TILE, TileGeometry<K>>(tx1 + pt * K, ty1 + pt * K, tx2 + pt * K, ty2 + pt * K, b,
                                                          scr + pt, geo, pt);
     }
-    const AreasX2 a = areas_exact<K, false>(geo.verts(pt), w, m);
-    const float ovr = (float)a.ai;
-    bwd_epilogue<K, TILE, PK>(tx1 + pt * K, ty1 + pt * K, tx2 + pt * K, ty2 + pt * K, g, V, scr + pt, G1, G2, flat(),
-                              nullptr, &ovr);
+    const AreasX2 a = areas_exact<K, true>(geo.verts(pt), w, m);
+    bwd_epilogue_exact<K, TILE>(tx1 + pt * K, ty1 + pt * K, tx2 + pt * K, ty2 + pt * K, g, V, scr + pt, a, G1, G2);
 }
 
 

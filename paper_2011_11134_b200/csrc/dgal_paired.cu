@@ -316,7 +316,7 @@ paired_bwd_kernel(int64_t n, const float *__restrict__ x1, const float *__restri
             Seq<K> s2;
 #pragma unroll
             for (int q = 0; q < K / 4; ++q) s2.w[q] = T.xf[tid * (K / 4) + q];
-            bwd_thin_redo<K, kTile>(T.x1, T.y1, T.x2, T.y2, s2, T.nx[tid], T.g[tid], S.scr, S.lut, G1, G2);
+            bwd_pair_exact<K, kTile>(T.x1, T.y1, T.x2, T.y2, tid, s2, T.nx[tid], T.g[tid], S.scr, S.lut, G1, G2);
             store_plane<K>(gx1, k, G1.x);
             store_plane<K>(gy1, k, G1.y);
             store_plane<K>(gx2, k, G2.x);
@@ -611,6 +611,7 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
     float *ring = fsm;
     float *gring = ring + (PF ? 2 * 4 * T * K : 0);
     float *pt = gring + (PF ? 2 * T : 0);
+    uint64_t *illt = reinterpret_cast<uint64_t *>(pt + 4 * K * T);   // K = 8: ILL factors, [q][thread]
     const int tid = threadIdx.x;
     const int64_t k0 = (int64_t)blockIdx.x * (NT * T) + tid;
     auto prefetch = [&](int stage, int64_t k) {
@@ -658,8 +659,9 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
         }
         recentre<K>(P, Q);
         bool need;
-        const float v = iou_fused<K, DGAL_FUSED_P2MODE, K == 4 && DGAL_FUSED_PK>(P, Q, g, G1, G2, flat(), nullptr,
-                                                        QTable{pt + tid, pt + 2 * K * T + tid, T}, &need);
+        const float v = iou_fused<K, DGAL_FUSED_P2MODE, K == 4 && DGAL_FUSED_PK>(
+            P, Q, g, G1, G2, flat(), nullptr, QTable{pt + tid, pt + 2 * K * T + tid, T}, &need,
+            IllTab{illt + tid, T});
         refine_mark(refine, k, need);   // redone exactly by paired_fused_refine_kernel
         if (iou) __stcs(iou + k, v);
         store_plane<K>(gx1, k, G1.x);
@@ -740,7 +742,7 @@ paired_fused_refine_kernel(int64_t n, const float *__restrict__ x1, const float 
             Poly<K> G1, G2;
             const bool thin = bwd_tile_pair<K, kRefT, TileGeometry<K>, false>(
                 S.x1, S.y1, S.x2, S.y2, r.seq, live ? r.nx : 0, g, live, S.scr, S.queue[tid >> 5], S.lut, G1, G2);
-            if (thin) bwd_thin_redo<K, kRefT, false>(S.x1, S.y1, S.x2, S.y2, r.seq, r.nx, g, S.scr, S.lut, G1, G2);
+            if (thin) bwd_pair_exact<K, kRefT>(S.x1, S.y1, S.x2, S.y2, tid, r.seq, r.nx, g, S.scr, S.lut, G1, G2);
             if (live) {
                 store_plane<K>(gx1, k, G1.x);
                 store_plane<K>(gy1, k, G1.y);
@@ -779,7 +781,7 @@ constexpr size_t fused_smem_bytes()
 {
     constexpr int T = (K == 4) ? kFused4Threads : kFused8Threads;
     constexpr bool PF = (K == 4) ? DGAL_FUSED_PF : DGAL_FUSED8_PF;
-    return sizeof(float) * ((PF ? 2 * 4 * T * K + 2 * T : 0) + 4 * K * T);
+    return sizeof(float) * ((PF ? 2 * 4 * T * K + 2 * T : 0) + 4 * K * T) + (K == 8 ? 8 * (K / 2) * T : 0);
 }
 template <int K>
 cudaError_t launch_fused_k(int64_t n, const float *x1, const float *y1, const float *x2, const float *y2,
