@@ -161,6 +161,47 @@ def cpu_oracle_rate(sample, seconds=10.0):
     return sample.n * reps / dt, nt, reps, dt
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_baseline_extra(cfg3_batch, nt):
+    """SURVEY §8(d) oracle timings beside the GPU ones (~10 s of CPU work): the CPU
+    model, a single-thread cfg3 rate, cfg1 and cfg4 in full, and cfg5's plain
+    all-pairs oracle on a 1 % row sample (1,000 rows x 100,000 columns, extrapolated
+    linearly to the whole matrix)."""
+    import oracle
+    import synth
+    out = {"cpu_model": cpu_model(), "host_threads": nt}
+    s1 = cfg3_batch.take(np.arange(1 << 16))
+    t = time.perf_counter()
+    oracle.iou_paired_fwd(s1.p1, s1.p2, nthreads=1)
+    oracle.iou_paired_bwd(s1.p1, s1.p2, s1.grad, nthreads=1)
+    out["cfg3_1_thread_pairs_per_s"] = s1.n / (time.perf_counter() - t)
+    for cfg in (1, 4):
+        b = synth.gen_config(cfg)
+        t = time.perf_counter()
+        oracle_fwdbwd(b, nt)
+        dt = time.perf_counter() - t
+        out[f"cfg{cfg}_full"] = {"pairs": b.n, "s": dt, "pairs_per_s": b.n / dt}
+    sc = synth.gen_cfg5_scene()
+    rows = sc.polys.take(np.arange(0, sc.polys.n, 100))      # 1 % of the rows, spread over the ranking
+    t = time.perf_counter()
+    oracle.iou_pairwise(rows, sc.polys, nthreads=nt)
+    dt = time.perf_counter() - t
+    npairs = rows.n * sc.polys.n
+    out["cfg5_1pct_rows"] = {"rows": rows.n, "cols": sc.polys.n, "s": dt, "pairs_per_s": npairs / dt,
+                             "extrapolated_full_matrix_s": dt * sc.polys.n / rows.n}
+    return out
+
+
 def run_reference(args, rank):
     if rank != 0:
         return 0
@@ -203,17 +244,31 @@ def run_reference(args, rank):
 # GPU arm
 # ---------------------------------------------------------------------------
 class Ctx:
-    def __init__(self, world, rank, local):
+    """One process per GPU (torchrun env).  backend "nccl" (the product path, one GPU
+    per rank) or "gloo" (several ranks may share a GPU — the functional check of
+    the multi-rank code on a one-GPU box; its timings are not scaling numbers)."""
+
+    def __init__(self, world, rank, local, backend="nccl"):
         import torch
         self.torch = torch
         self.world, self.rank, self.local = world, rank, local
-        torch.cuda.set_device(local)
-        self.dev = torch.device("cuda", local)
+        ndev = torch.cuda.device_count()
+        self.shared_gpu = world > ndev
+        if self.shared_gpu and backend == "nccl" and world > 1:
+            raise SystemExit(f"{world} ranks on {ndev} GPU(s): NCCL needs one GPU per rank "
+                             f"(use --dist-backend gloo to run the ranks on a shared GPU)")
+        torch.cuda.set_device(local % ndev)
+        self.dev = torch.device("cuda", local % ndev)
         self.dist = None
+        self.backend = backend if world > 1 else None
         if world > 1:
             import torch.distributed as dist
-            dist.init_process_group("nccl", device_id=self.dev)
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=self.dev)
+            else:
+                dist.init_process_group("gloo")
             self.dist = dist
+            assert dist.get_world_size() == world
 
     def barrier(self):
         if self.dist:
@@ -222,9 +277,22 @@ class Ctx:
     def max_over_ranks(self, v):
         if not self.dist:
             return v
-        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        dev = self.dev if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
+
+    def all_equal(self, t):
+        """Whether tensor t is bitwise the same on every rank (checksum all-gather)."""
+        if not self.dist:
+            return True
+        torch = self.torch
+        h = torch.tensor([int(t.to(torch.int64).sum().item()), int((t.to(torch.int64) * torch.arange(
+            t.numel(), device=t.device) % 1000003).sum().item())], dtype=torch.int64)
+        dev = self.dev if self.backend == "nccl" else "cpu"
+        parts = [torch.empty_like(h, device=dev) for _ in range(self.world)]
+        self.dist.all_gather(parts, h.to(dev))
+        return all(torch.equal(parts[0].cpu(), q.cpu()) for q in parts)
 
 
 def paired_inputs(ctx, cfg, n):
@@ -238,22 +306,36 @@ def paired_inputs(ctx, cfg, n):
     return K, (x1, y1, x2, y2), g, b
 
 
-def time_paired(ctx, K, planes, g, steps, warmup, sampler=None):
-    """CUDA-event timing of `steps` fwd+bwd steps on the current stream; per-kernel
-    averages from events around each launch.  Returns (ms_total, fwd_ms, bwd_ms, t0, t1)."""
+def time_paired(ctx, K, planes, g, steps, warmup, sampler=None, extra=False):
+    """CUDA-event timing of `steps` fwd+bwd steps on the current stream.
+
+    The timed steps alternate between two copies of the input planes (step s reads
+    set s % 2), so no step finds the previous step's inputs in L2 (the backward walks
+    its tiles in descending order to reuse the forward's L2 lines WITHIN a step; across
+    steps a training loop would not get that reuse).  Per-kernel averages come from a
+    separate pass with events around each launch.  extra=True also measures the same
+    steps on ONE buffer set, with the 126 MB L2 flushed (a 256 MB memset outside each
+    step's events) before every step, and a sustained run of max(200, steps) steps.
+    Returns (ms_total, fwd_ms, bwd_ms, t0, t1, (iou, grads), extras)."""
     import paper_2011_11134_b200 as dgal
     torch = ctx.torch
     n = g.numel()
+    sets = [planes, tuple(t.clone() for t in planes)]
     iou = torch.empty(n, dtype=torch.float32, device=ctx.dev)
     nx = torch.empty(n, dtype=torch.uint8, device=ctx.dev)
     xf = torch.empty((n, 2 * K), dtype=torch.uint8, device=ctx.dev)
     grads = tuple(torch.empty((n, K), dtype=torch.float32, device=ctx.dev) for _ in range(4))
-    for _ in range(warmup):
-        dgal.iou_paired_fwd(*planes, out=(iou, nx, xf))
-        dgal.iou_paired_bwd(*planes, g, nx, xf, out=grads)
+
+    def step(pl):
+        dgal.iou_paired_fwd(*pl, out=(iou, nx, xf))
+        dgal.iou_paired_bwd(*pl, g, nx, xf, out=grads)
+
+    for s in range(warmup):
+        step(sets[s % 2])
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream(ctx.dev)
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    start, end = E(), E()
     # (1) the timed steps: fwd + bwd back to back, events only around the region
     #     (an event between two kernels drains the first before the second starts)
     ctx.barrier()
@@ -261,8 +343,7 @@ def time_paired(ctx, K, planes, g, steps, warmup, sampler=None):
     t0 = time.perf_counter()
     start.record(stream)
     for s in range(steps):
-        dgal.iou_paired_fwd(*planes, out=(iou, nx, xf))
-        dgal.iou_paired_bwd(*planes, g, nx, xf, out=grads)
+        step(sets[s % 2])
     end.record(stream)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
@@ -271,18 +352,51 @@ def time_paired(ctx, K, planes, g, steps, warmup, sampler=None):
     # (2) per-kernel split for the roofline: the same steps with an event around
     #     each launch (a separate pass, not part of the timed value)
     ns = min(steps, 50)
-    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(ns)]
+    ev = [tuple(E() for _ in range(3)) for _ in range(ns)]
     for s in range(ns):
         e0, e1, e2 = ev[s]
+        pl = sets[s % 2]
         e0.record(stream)
-        dgal.iou_paired_fwd(*planes, out=(iou, nx, xf))
+        dgal.iou_paired_fwd(*pl, out=(iou, nx, xf))
         e1.record(stream)
-        dgal.iou_paired_bwd(*planes, g, nx, xf, out=grads)
+        dgal.iou_paired_bwd(*pl, g, nx, xf, out=grads)
         e2.record(stream)
     torch.cuda.synchronize()
     fwd_ms = sum(a.elapsed_time(b) for a, b, _ in ev) / ns
     bwd_ms = sum(b.elapsed_time(c) for _, b, c in ev) / ns
-    return ctx.max_over_ranks(ms), fwd_ms, bwd_ms, t0, t1, (iou, grads)
+    extras = {}
+    if extra:
+        # same buffers every step (L2 carry-over between steps allowed)
+        a, z = E(), E()
+        a.record(stream)
+        for s in range(steps):
+            step(planes)
+        z.record(stream)
+        torch.cuda.synchronize()
+        extras["same_buffers_ms_per_step"] = ctx.max_over_ranks(a.elapsed_time(z)) / steps
+        # cold L2: a 256 MB memset (2 x the 126 MB L2) before every step, outside its events
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=ctx.dev)
+        evs = [(E(), E()) for _ in range(steps)]
+        for s in range(steps):
+            flush.zero_()
+            evs[s][0].record(stream)
+            step(planes)
+            evs[s][1].record(stream)
+        torch.cuda.synchronize()
+        extras["l2_flushed_ms_per_step"] = ctx.max_over_ranks(sum(x.elapsed_time(y) for x, y in evs) / steps)
+        del flush
+        # sustained: a long back-to-back run (power / clock steady state)
+        ns2 = max(200, steps)
+        a, z = E(), E()
+        a.record(stream)
+        for s in range(ns2):
+            step(sets[s % 2])
+        z.record(stream)
+        torch.cuda.synchronize()
+        extras["sustained_steps"] = ns2
+        extras["sustained_ms_per_step"] = ctx.max_over_ranks(a.elapsed_time(z)) / ns2
+    del sets
+    return ctx.max_over_ranks(ms), fwd_ms, bwd_ms, t0, t1, (iou, grads), extras
 
 
 def bench_e2e(ctx, K, planes, g, iou_dev, steps):
@@ -539,12 +653,27 @@ def bench_cfg5(ctx, steps, warmup, peak):
     mat_ms, tot_ms = mat_ms / steps, tot_ms / steps
     mat_max = ctx.max_over_ranks(mat_ms)
     tot_max = ctx.max_over_ranks(tot_ms)
-    kept = int((keep if ctx.world == 1 else (status[:n] == 1)).sum().item())
+    keep_vec = keep if ctx.world == 1 else (status[:n] == 1).to(torch.uint8)
+    kept = int(keep_vec.sum().item())
     bytes_local = nr * n * 4 + nr * words * 8
     del out
     torch.cuda.empty_cache()
+    extra = {}
+    if ctx.world > 1:
+        # S:509 / S:525: the sharded greedy keep is bitwise the single-GPU one — every rank
+        # holds the same vector, and rank 0 recomputes the whole problem on its GPU
+        # (mask + lists only, one kernel for all rounds) to compare
+        extra["keep_same_on_all_ranks"] = ctx.all_equal(keep_vec)
+        if ctx.rank == 0:
+            _, m1, c1, i1 = dgal.iou_pairwise(x, y, x, y, thr=sc.thr, want_iou=False, nbr_cap=cap, workspace=ws)
+            k1 = dgal.nms_keep(m1, c1, i1)
+            extra["keep_equal_single_gpu"] = bool(torch.equal(k1, keep_vec))
+            del m1, c1, i1
+            torch.cuda.empty_cache()
+        extra["nms_ms_per_round"] = (tot_max - mat_max) / max(rounds, 1)
+        extra["nms_check_every"] = 8
     return {"workload": "cfg5: pairwise IoU 100k x 100k nuScenes-like boxes + NMS mask + greedy keep (thr 0.7)",
-            "scaling": "strong (rows sharded)", "n_gpus": ctx.world,
+            "scaling": "strong (rows sharded)", "n_gpus": ctx.world, **extra,
             "pairs_per_s_matrix": n * n / (mat_max * 1e-3),
             "ms_matrix": mat_max, "ms_matrix_plus_nms": tot_max, "nms_rounds": rounds, "kept": kept,
             "path": "indexed: streaming zero fill + circle-grid candidates (include/dgal.h)",
@@ -565,16 +694,33 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: several ranks may share one GPU (functional multi-rank check)")
+    raw_argv = list(sys.argv[1:] if argv is None else argv)
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # started as `python bench.py --gpus N`: re-exec one process per GPU under
+        # torch.distributed.run (the driver's own N > 1 launch sets WORLD_SIZE itself)
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *raw_argv]
+        os.execv(sys.executable, cmd)
 
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one process per GPU")
     if args.impl == "reference":
         return run_reference(args, rank)
 
-    ctx = Ctx(world, rank, local)
+    ctx = Ctx(world, rank, local, args.dist_backend)
     torch = ctx.torch
     peak, peak_src = measured_peaks()
 
@@ -584,7 +730,8 @@ def main(argv=None):
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.05)
-    ms, fwd_ms, bwd_ms, t0, t1, (iou_dev, _) = time_paired(ctx, K, planes, g, args.steps, args.warmup)
+    ms, fwd_ms, bwd_ms, t0, t1, (iou_dev, _), hyg = time_paired(ctx, K, planes, g, args.steps, args.warmup)
+    _, _, _, _, _, _, hyg = time_paired(ctx, K, planes, g, args.steps, args.warmup, extra=True)
     time.sleep(0.02)
     sampler.stop()
     value = n * args.steps * world / (ms * 1e-3)
@@ -600,7 +747,7 @@ def main(argv=None):
     if not args.no_secondary:
         n4 = 1 << 22
         K4, planes4, g4, _ = paired_inputs(ctx, 4, n4)
-        ms4, f4, b4, _, _, _ = time_paired(ctx, K4, planes4, g4, max(10, args.steps // 4), args.warmup)
+        ms4, f4, b4, _, _, _, _ = time_paired(ctx, K4, planes4, g4, max(10, args.steps // 4), args.warmup)
         fb4, bb4 = algorithmic_bytes(K4)
         secondary["cfg4"] = {
             "workload": "cfg4: paired IoU fwd+bwd, 2^22 convex octagon pairs Poly2<float,8> per GPU",
@@ -633,7 +780,8 @@ def main(argv=None):
         rate, nt, reps, dt = cpu_oracle_rate(sample, seconds=10.0)
         cpu = {"value": rate, "unit": UNIT, "cores": nt, "kind": "oracle",
                "sample": f"first {sample.n} pairs of this cfg3 batch, fwd+bwd in float64, repeated {reps}x "
-                         f"({dt:.1f} s, {nt} OpenMP threads)"}
+                         f"({dt:.1f} s, {nt} OpenMP threads)",
+               **cpu_baseline_extra(batch, nt)}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -642,7 +790,14 @@ def main(argv=None):
         "config": {"workload": "cfg3: paired IoU loss fwd+bwd, KITTI-like rotated-box pairs, Poly2<float,4>",
                    "pairs_per_gpu": n, "global_pairs": n * world, "K": K,
                    "parallelism": f"dp{world} (contiguous pair shards, no collective)",
-                   "l2": "inputs 1.07 GB/GPU > 126 MB L2, no flush needed"},
+                   "dist_backend": ctx.backend, "shared_gpu": ctx.shared_gpu,
+                   "l2": "inputs 1.07 GB/GPU > 126 MB L2; timed steps alternate between two copies of the "
+                         "inputs (no L2 carry-over between steps); see 'hygiene' for one buffer set, "
+                         "an L2 flush before every step and a sustained run"},
+        "hygiene": {k: v for k, v in hyg.items()} | {
+            "burst_ms_per_step": ms / args.steps, "burst_steps": args.steps,
+            "l2_flushed_pairs_per_s": n * world / (hyg["l2_flushed_ms_per_step"] * 1e-3),
+            "sustained_pairs_per_s": n * world / (hyg["sustained_ms_per_step"] * 1e-3)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": peak, "unit": "GB/s",
                      "frac": dom_gbs / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_pair": {"paired_fwd": fb, "paired_bwd": bb},

@@ -44,8 +44,29 @@ def iou_paired_shard(x1, y1, x2, y2, grad, world: int, rank: int):
 iou_paired_sharded = iou_paired_shard   # SURVEY §8(b) name
 
 
+def _backend(group=None) -> str:
+    return dist.get_backend(group) if dist.is_initialized() else "none"
+
+
+def gather_status(status: torch.Tensor, B: int, group=None) -> None:
+    """All-gather every rank's slice status[r*B:(r+1)*B] into every rank's copy, in
+    place (NCCL: all_gather_into_tensor on the device, enqueued on the current
+    stream, no host sync; gloo: through host memory — the CPU test / shared-GPU
+    path)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    mine = status[rank * B:(rank + 1) * B].clone()
+    if _backend(group) == "nccl":
+        dist.all_gather_into_tensor(status, mine, group=group)
+        return
+    parts = [torch.empty_like(mine, device="cpu") for _ in range(world)]
+    dist.all_gather(parts, mine.cpu(), group=group)
+    status.copy_(torch.cat(parts).to(status.device))
+
+
 def nms_rounds(n: int, lo: int, hi: int, round_fn: Callable[[torch.Tensor], None],
-               status: torch.Tensor, group=None, max_rounds: Optional[int] = None) -> int:
+               status: torch.Tensor, group=None, max_rounds: Optional[int] = None,
+               check_every: int = 8) -> int:
     """Run NMS rounds to convergence.
 
     status: this rank's copy of the padded global status vector, uint8
@@ -53,18 +74,24 @@ def nms_rounds(n: int, lo: int, hi: int, round_fn: Callable[[torch.Tensor], None
     round_fn(status): updates status[lo:hi] (this rank's boxes) in place from
             the whole vector (dgal_nms_round on the GPU).
     After every round the ranks all-gather their slices, so all copies agree.
-    Returns the number of rounds.
+    The host checks for convergence only every `check_every` rounds (one device
+    -> host read of "any box undecided" per check, not per round: rounds after
+    convergence change nothing, so over-running is harmless).  Every rank reads
+    the same gathered vector, so all take the same decision.
+    Returns the number of rounds run (a multiple of check_every, or fewer at the limit).
     """
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     B = status.numel() // world
     assert status.numel() == world * B and lo == min(n, rank * B)
     limit = max_rounds if max_rounds is not None else n + 1
-    for r in range(1, limit + 1):
-        round_fn(status)
-        if world > 1:
-            mine = status[rank * B:(rank + 1) * B].clone()
-            dist.all_gather_into_tensor(status, mine, group=group)
+    r = 0
+    while r < limit:
+        for _ in range(min(check_every, limit - r)):
+            round_fn(status)
+            if world > 1:
+                gather_status(status, B, group)
+            r += 1
         if not bool((status[:n] == 0).any()):
             return r
     raise RuntimeError("NMS rounds did not converge")  # impossible: >= 1 box decides per round
