@@ -113,24 +113,25 @@ dgal_status dgal_iou_paired_bwd(int K, int64_t n,
  *
  * Exactness (north_star tolerances on every input, like the split path): the
  * one-pass float arithmetic is not accurate enough for two rare kinds of pair —
- * a nearly parallel (p1 edge, p2 edge) pair (|sin| < 2^-9: float crossing
- * parameters are conditioned by 1/sin) and a thin pair (R^2 > 8 A_u, R the
- * pair's extent: the float area sum is conditioned by R^2 / A_u).  The first
- * kernel marks them in the refine mask `workspace` (one bit per pair) and a
+ * a nearly parallel crossing (a p1 edge crossing a p2 edge's line at |sin| <
+ * 2^-9, 2^-7 for boxes: float crossing parameters are conditioned by 1/sin) and
+ * a thin pair (R^2 > 8 A_u, R the pair's extent: the float area sum is
+ * conditioned by R^2 / A_u).  The first kernel queues them in `workspace` and a
  * second kernel, enqueued right after it, recomputes exactly those pairs with
  * the split path's arithmetic (dgal_iou_paired_fwd + _bwd: crossings refined in
- * double, thin areas in double), overwriting their iou and gradients.  Unmarked
+ * double, thin areas in double), overwriting their iou and gradients.  Unqueued
  * pairs: IoU bit-identical to dgal_iou_pairwise, gradients equal to the split
  * path's up to rounding.
- *   workspace        >= dgal_fused_workspace_bytes(n) bytes of device memory,
+ *   workspace        >= dgal_fused_workspace_bytes(n) bytes of device memory
+ *                    (a queue: {count, done, pad[2], idx[n]} of uint32),
  *                    ZERO-FILLED by the caller before its first use; every call
- *                    leaves it zero-filled again (the refine pass clears the bits
- *                    it consumes), so it is reused across calls without clearing.
+ *                    leaves it zero-filled again (the refine kernel resets the
+ *                    counters), so it is reused across calls without clearing.
  *                    One workspace per stream: calls that may run concurrently
  *                    need separate workspaces.  NULL or too small ->
- *                    DGAL_ERR_INVALID_ARG.
+ *                    DGAL_ERR_INVALID_ARG.  n < 2^32 (32-bit queue entries).
  */
-size_t dgal_fused_workspace_bytes(int64_t n);   /* 4 * ceil(n / 32), rounded up to 8 */
+size_t dgal_fused_workspace_bytes(int64_t n);   /* 16 + 4 n, rounded up to 16 */
 
 dgal_status dgal_iou_paired_fused(int K, int64_t n,
                                   const float *x1, const float *y1,
@@ -177,9 +178,9 @@ dgal_status dgal_box_iou_paired_bwd(int dims, int layout, int64_t n,
                                     dgal_stream stream);
 
 /* fused forward + backward (f2 on boxes): dL/dIoU = grad_iou[k], or grad_scale
- * when grad_iou == NULL; iou nullable; workspace: the refine mask as for
+ * when grad_iou == NULL; iou nullable; workspace: the refine queue as for
  * dgal_iou_paired_fused (dgal_fused_workspace_bytes(n), zero-filled once; the
- * marked pairs are redone with the box split path's arithmetic). */
+ * queued pairs are redone with the box split path's arithmetic). */
 dgal_status dgal_box_iou_paired_fused(int dims, int layout, int64_t n,
                                       const float *b1, const float *b2,
                                       const float *grad_iou, float grad_scale,

@@ -75,7 +75,7 @@ _FUSED_WS = {}
 
 
 def fused_workspace(n: int, device=None, stream=None) -> torch.Tensor:
-    """Refine mask of the fused kernels (dgal_fused_workspace_bytes(n) bytes, zero-filled
+    """Refine queue of the fused kernels (dgal_fused_workspace_bytes(n) bytes, zero-filled
     once; every call leaves it zero-filled).  Cached per (device, stream) — one
     workspace per stream, as include/dgal.h requires — and grown on demand."""
     dev = torch.device(device or "cuda")
@@ -133,7 +133,7 @@ def iou_paired_fused(x1, y1, x2, y2, grad=None, scale: float = 1.0, K: int | Non
                      want_iou: bool = True, workspace: torch.Tensor | None = None):
     """Fused loss forward + backward (dgal_iou_paired_fused): dL/dIoU = grad[k] (a
     CUDA float tensor [n]) or the scalar `scale`.  Returns (iou | None, gx1, gy1, gx2, gy2).
-    workspace: the refine mask (fused_workspace(n), cached per stream when omitted)."""
+    workspace: the refine queue (fused_workspace(n), cached per stream when omitted)."""
     _plane(x1, "x1")
     K, n = _K_n(x1, K)
     dev = x1.device

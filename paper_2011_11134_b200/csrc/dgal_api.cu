@@ -70,12 +70,13 @@ dgal_status dgal_iou_paired_fused(int K, int64_t n, const float *x1, const float
     if (n == 0) return DGAL_OK;
     if (!x1 || !y1 || !x2 || !y2 || !gx1 || !gy1 || !gx2 || !gy2) return DGAL_ERR_INVALID_ARG;
     if (!workspace || workspace_bytes < dgal::refine_workspace_bytes(n)) return DGAL_ERR_INVALID_ARG;
+    if (n > dgal::kMaxFusedPairs) return DGAL_ERR_INVALID_ARG;
     if (!aligned(x1, 16) || !aligned(y1, 16) || !aligned(x2, 16) || !aligned(y2, 16) ||
         !aligned(gx1, 16) || !aligned(gy1, 16) || !aligned(gx2, 16) || !aligned(gy2, 16) ||
         (grad_iou && !aligned(grad_iou, 4)) || (iou && !aligned(iou, 4)) || !aligned(workspace, 16))
         return DGAL_ERR_MISALIGNED;
     return from_cuda(dgal::launch_paired_fused(K, n, x1, y1, x2, y2, grad_iou, grad_scale, iou, gx1, gy1, gx2,
-                                               gy2, static_cast<uint32_t *>(workspace), as_cuda(stream)));
+                                               gy2, workspace, as_cuda(stream)));
 }
 
 namespace {
@@ -121,11 +122,12 @@ dgal_status dgal_box_iou_paired_fused(int dims, int layout, int64_t n, const flo
     if (c != DGAL_OK || n == 0) return c;
     if (!grad_b1 || !grad_b2) return DGAL_ERR_INVALID_ARG;
     if (!workspace || workspace_bytes < dgal::refine_workspace_bytes(n)) return DGAL_ERR_INVALID_ARG;
+    if (n > dgal::kMaxFusedPairs) return DGAL_ERR_INVALID_ARG;
     if ((grad_iou && !aligned(grad_iou, 4)) || (iou && !aligned(iou, 4)) || !aligned(grad_b1, 4) ||
         !aligned(grad_b2, 4) || !aligned(workspace, 16))
         return DGAL_ERR_MISALIGNED;
     return from_cuda(dgal::launch_box_fused(dims, layout, n, b1, b2, grad_iou, grad_scale, iou, grad_b1, grad_b2,
-                                            static_cast<uint32_t *>(workspace), as_cuda(stream)));
+                                            workspace, as_cuda(stream)));
 }
 
 dgal_status dgal_iou_pairwise(int K, int64_t n_rows, const float *row_x, const float *row_y, int64_t m,

@@ -315,7 +315,7 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
             const float Vix2 = Aix2 * z.dz;
             const float Vux2 = (A1x2 * a.d + A2x2 * b.d) - Vix2;
             const bool ok = m > 0 && Vix2 > 0.f && Vux2 > 0.f;
-            v = ok ? fminf(Vix2 / Vux2, 1.f) : 0.f;
+            v = ok ? iou_div(Vix2, Vux2) : 0.f;
             m = ok ? m : 0;
             seq = ok ? seq : 0ull;
         }
@@ -478,7 +478,7 @@ template <int DIMS>
 __global__ void __launch_bounds__(kBoxFusedT, DIMS == 2 ? DGAL_BOX_FUSED2_MINB : DGAL_BOX_FUSED3_MINB)
 box_fused_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict__ b2, int64_t sk, int64_t sp,
                  const float *__restrict__ grad, float scale, float *__restrict__ iou, float *__restrict__ gb1,
-                 float *__restrict__ gb2, uint32_t *__restrict__ refine)
+                 float *__restrict__ gb2, RefineQueue *__restrict__ refine)
 {
     constexpr int T = kBoxFusedT;
     constexpr bool PF = DGAL_BOX_PF;
@@ -534,36 +534,30 @@ box_fused_kernel(int64_t n, const float *__restrict__ b1, const float *__restric
 // ---------------------------------------------------------------------------
 static_assert(kRefT == kBoxTile, "the refine tile is the backward tile (BoxGeometry strides)");
 struct BoxRefineSmem {
-    uint16_t q[kRefChunkPairs];
     BoxBwdSmem b;
-    int qn;
 };
 
 template <int DIMS>
 __global__ void __launch_bounds__(kRefT, 4)
 box_fused_refine_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict__ b2, int64_t sk,
                         int64_t sp, const float *__restrict__ grad, float scale, float *__restrict__ iou,
-                        float *__restrict__ gb1, float *__restrict__ gb2, uint32_t *__restrict__ refine)
+                        float *__restrict__ gb1, float *__restrict__ gb2, RefineQueue *__restrict__ refine)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BoxRefineSmem &R = *reinterpret_cast<BoxRefineSmem *>(smem_raw);
     BoxBwdSmem &S = R.b;
     const int tid = threadIdx.x;
-    fill_flag_lut(S.lut, tid, kRefT);
-    if (tid == 0) R.qn = 0;
-    __syncthreads();
-    const int64_t nwords = refine_words(n);
-    const int64_t nchunks = (nwords + kRefChunkWords - 1) / kRefChunkWords;
-#pragma unroll 1
-    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        refine_gather(refine, nwords, c, R.q, &R.qn);
+    const unsigned int total = refine_count(refine);
+    if ((unsigned int)blockIdx.x * kRefT < total) {
+        fill_flag_lut(S.lut, tid, kRefT);
         __syncthreads();
-        const int total = R.qn;
+    }
+    {
 #pragma unroll 1
-        for (int base = 0; base < total; base += kRefT) {
-            const int e = base + tid;
+        for (unsigned int base = blockIdx.x * kRefT; base < total; base += gridDim.x * kRefT) {
+            const unsigned int e = base + tid;
             const bool live = e < total;
-            const int64_t k = live ? c * kRefChunkPairs + R.q[e] : 0;
+            const int64_t k = live ? (int64_t)refine->idx[e] : 0;
             Box<DIMS> a{}, b{};
             Poly<4> P, Q;
             Trig t{1.f, 0.f, 1.f, 0.f};
@@ -600,7 +594,7 @@ box_fused_refine_kernel(int64_t n, const float *__restrict__ b1, const float *__
                 const float Vix2 = Aix2 * z.dz;
                 const float Vux2 = (A1x2 * a.d + A2x2 * b.d) - Vix2;
                 const bool ok = m > 0 && Vix2 > 0.f && Vux2 > 0.f;
-                v = ok ? fminf(Vix2 / Vux2, 1.f) : 0.f;
+                v = ok ? iou_div(Vix2, Vux2) : 0.f;
                 m = ok ? m : 0;
             }
             if (live && iou) iou[k] = v;
@@ -623,10 +617,9 @@ box_fused_refine_kernel(int64_t n, const float *__restrict__ b1, const float *__
             }
             __syncwarp();
         }
-        __syncthreads();
-        if (tid == 0) R.qn = 0;
-        __syncthreads();
     }
+    __syncthreads();
+    if (tid == 0) refine_finish(refine);
 }
 
 // ---------------------------------------------------------------------------
@@ -668,8 +661,9 @@ cudaError_t launch_box_bwd(int dims, int layout, int64_t n, const float *b1, con
 }
 
 cudaError_t launch_box_fused(int dims, int layout, int64_t n, const float *b1, const float *b2, const float *grad,
-                             float scale, float *iou, float *gb1, float *gb2, uint32_t *refine, cudaStream_t st)
+                             float scale, float *iou, float *gb1, float *gb2, void *refine_ws, cudaStream_t st)
 {
+    RefineQueue *refine = static_cast<RefineQueue *>(refine_ws);
     int64_t sk, sp;
     box_strides(dims, layout, n, sk, sp);
     constexpr int64_t per = (int64_t)(DGAL_BOX_PF ? DGAL_BOX_FUSED_NT : 1) * kBoxFusedT;

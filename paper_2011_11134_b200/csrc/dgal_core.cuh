@@ -73,6 +73,24 @@ __device__ __forceinline__ float rcp_approx(float x)
     return r;
 }
 
+// IoU = a / u (u > 0) by div.full (<= 2 ulp, no slow-path branch of the IEEE
+// division: a smaller loop body), clamped to 1; a == u (identical polygons) gives 1
+// exactly.  The one IoU division of every kernel (paired, fused, pairwise agree).
+__device__ __forceinline__ float iou_div(float a, float u)
+{
+    float q;
+    asm("div.full.f32 %0, %1, %2;" : "=f"(q) : "f"(a), "f"(u));
+    return (a == u) ? 1.f : fminf(q, 1.f);
+}
+
+// 1/x to ~1 ulp without the IEEE division's slow-path branch (x normal, > 0 here):
+// the approximate reciprocal and one Newton step
+__device__ __forceinline__ float rcp_refined(float x)
+{
+    const float r = rcp_approx(x);
+    return fmaf(r, fmaf(-x, r, 1.f), r);
+}
+
 // Paired FP32 (sm_100: FADD2 / FMUL2 / FFMA2 — two IEEE RN operations in one
 // instruction on a 64-bit register pair; no contraction across the asm).  The
 // kernels are issue-bound, so pairing the decision values and the Cyrus-Beck
@@ -269,6 +287,19 @@ constexpr float kThinRatio = 8.f;
 template <int K>
 __device__ __forceinline__ float pair_extent2(const Poly<K> &P, const Poly<K> &Q)
 {
+#ifdef DGAL_THIN_SUMSQ
+    // sum of the squared vertex norms (>= R^2; <= 2K R^2): paired accumulation, no max chain
+    uint64_t acc = 0ull;
+#pragma unroll
+    for (int q = 0; q < K / 2; ++q) {
+        const uint64_t qx = f2pack(Q.x[2 * q], Q.x[2 * q + 1]), qy = f2pack(Q.y[2 * q], Q.y[2 * q + 1]);
+        const uint64_t px = f2pack(P.x[2 * q], P.x[2 * q + 1]), py = f2pack(P.y[2 * q], P.y[2 * q + 1]);
+        acc = f2fma(qx, qx, f2fma(qy, qy, f2fma(px, px, f2fma(py, py, acc))));
+    }
+    float a, b;
+    f2unpack(acc, a, b);
+    return (a + b) * (1.f / (2 * K));
+#endif
     // p2's vertices two per paired instruction, in the (2q, 2q+1) pairs the decision
     // rows pack (no register moves); p1's scalar (P.x[0] = P.y[0] = 0 after recentring)
     float r = 0.f;
@@ -916,7 +947,7 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
     }
     if (nonempty) {
         const float Aux2 = (A1x2 + A2x2) - Aix2;
-        out.iou = (Aux2 > 0.f) ? fminf(Aix2 / Aux2, 1.f) : 0.f;
+        out.iou = (Aux2 > 0.f) ? iou_div(Aix2, Aux2) : 0.f;
         out.Aix2 = Aix2;
     }
     return out;
@@ -959,7 +990,7 @@ __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, f
     const float Vix2 = c.Aix2 * ex.dz;
     const float Vux2 = (c.A1x2 * ex.d1 + c.A2x2 * ex.d2) - Vix2;
     if (!(Vux2 > 0.f) || !(Vix2 > 0.f)) return 0.f;
-    const float iou = fminf(Vix2 / Vux2, 1.f);
+    const float iou = iou_div(Vix2, Vux2);
 
     if constexpr (PK && (DGAL_F32X2 & 4)) {
         // the same weights and gradients with (p1, p2) quantities in paired FP32
@@ -983,7 +1014,11 @@ __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, f
             AL[i] = f2sub(L, BE[i]);
         }
         const float Vi = 0.5f * Vix2, Vu = 0.5f * Vux2;
-        const float inv = 1.f / Vu;
+        #ifdef DGAL_FASTRCP
+    const float inv = rcp_refined(Vu);
+#else
+    const float inv = 1.f / Vu;
+#endif
         const float q = Vi * inv;
         const float cvi = g * ((1.f + q) * inv);
         const float cvu = g * (-q * inv);
@@ -1025,7 +1060,11 @@ __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, f
     }
     // dIoU/dV_i = (V_u + V_i)/V_u^2, dIoU/dV_1,2 = -V_i/V_u^2; dV/dA = d
     const float Vi = 0.5f * Vix2, Vu = 0.5f * Vux2;
+    #ifdef DGAL_FASTRCP
+    const float inv = rcp_refined(Vu);
+#else
     const float inv = 1.f / Vu;
+#endif
     const float q = Vi * inv;
     const float cvi = g * ((1.f + q) * inv);
     const float cvu = g * (-q * inv);
@@ -1280,7 +1319,11 @@ __device__ __forceinline__ bool bwd_epilogue(const float *sPx, const float *sPy,
     const float Vi = Ai * ex.dz;
     const float Vu = 0.5f * ((A1x2 * ex.d1 + A2x2 * ex.d2) - Aix2 * ex.dz);
     if (!(Vu > 0.f) || !(Vi > 0.f)) return thin;  // R10 guard
+    #ifdef DGAL_FASTRCP
+    const float inv = rcp_refined(Vu);
+#else
     const float inv = 1.f / Vu;
+#endif
     const float q = Vi * inv;
     const float cvi = g * ((1.f + q) * inv);
     const float cvu = g * (-q * inv);
@@ -1363,7 +1406,11 @@ __device__ __forceinline__ bool bwd_epilogue(const float *sPx, const float *sPy,
     const float Vi = Ai * ex.dz;
     const float Vu = 0.5f * ((A1x2 * ex.d1 + A2x2 * ex.d2) - Aix2 * ex.dz);
     if (!(Vu > 0.f) || !(Vi > 0.f)) return thin;  // R10 guard
+    #ifdef DGAL_FASTRCP
+    const float inv = rcp_refined(Vu);
+#else
     const float inv = 1.f / Vu;
+#endif
     const float q = Vi * inv;
     const float cvi = g * ((1.f + q) * inv);
     const float cvu = g * (-q * inv);

@@ -69,15 +69,16 @@ cudaError_t launch_paired_bwd(int K, int64_t n, const float *x1, const float *y1
                               cudaStream_t st);
 cudaError_t launch_paired_fused(int K, int64_t n, const float *x1, const float *y1, const float *x2,
                                 const float *y2, const float *grad, float scale, float *iou, float *gx1,
-                                float *gy1, float *gx2, float *gy2, uint32_t *refine, cudaStream_t st);
+                                float *gy1, float *gx2, float *gy2, void *refine, cudaStream_t st);
 int refine_grid_for(int64_t n);   // grid of the fused kernels' refine pass (dgal_refine.cuh)
+constexpr int64_t kMaxFusedPairs = 0xFFFFFFFFll;   // queue entries are 32-bit pair indices
 size_t refine_workspace_bytes(int64_t n);
 cudaError_t launch_box_fwd(int dims, int layout, int64_t n, const float *b1, const float *b2, float *iou,
                            uint8_t *nx, uint8_t *xflags, cudaStream_t st);
 cudaError_t launch_box_bwd(int dims, int layout, int64_t n, const float *b1, const float *b2, const float *grad,
                            const uint8_t *nx, const uint8_t *xflags, float *gb1, float *gb2, cudaStream_t st);
 cudaError_t launch_box_fused(int dims, int layout, int64_t n, const float *b1, const float *b2, const float *grad,
-                             float scale, float *iou, float *gb1, float *gb2, uint32_t *refine, cudaStream_t st);
+                             float scale, float *iou, float *gb1, float *gb2, void *refine, cudaStream_t st);
 cudaError_t launch_pairwise(int K, int64_t n_rows, const float *rx, const float *ry, int64_t m,
                             const float *cx, const float *cy, int64_t row_offset, float *iou,
                             float thr, uint64_t *mask, int64_t mask_words, int32_t *nbr_count,

@@ -448,6 +448,9 @@ paired_bwd_pt_kernel(int64_t n, const float *__restrict__ x1, const float *__res
     // re-staged at its slot of stage 0 from global memory, every crossing and the
     // intersection's area in double (bwd_pair_exact; no warp cooperation)
     if (!DGAL_THIN_BWD) return;
+#ifdef DGAL_NOPOSTBWD
+    return;
+#endif
     cp_async_wait<0>();
     uint32_t thinmask = S.thinm[tid];
     typename BwdPtSmem<K>::Stage &D = S.st[0];
@@ -591,7 +594,7 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
                     const float *__restrict__ x2, const float *__restrict__ y2,
                     const float *__restrict__ grad, float scale, float *__restrict__ iou,
                     float *__restrict__ gx1, float *__restrict__ gy1,
-                    float *__restrict__ gx2, float *__restrict__ gy2, uint32_t *__restrict__ refine)
+                    float *__restrict__ gx2, float *__restrict__ gy2, RefineQueue *__restrict__ refine)
 {
 #ifndef DGAL_FUSED_PK
 #define DGAL_FUSED_PK true   // K = 4: gradient part in paired FP32 (K = 8 would spill)
@@ -680,13 +683,11 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
 // ---------------------------------------------------------------------------
 template <int K>
 struct RefineSmem {
-    uint16_t q[kRefChunkPairs];                             // marked pairs of the chunk
     float x1[kRefT * K], y1[kRefT * K], x2[kRefT * K], y2[kRefT * K];   // raw tile, [pair][k]
     float scr[4 * K * kRefT];                               // interval end points, [slot][pair]
     uint16_t queue[kRefT / 32][32 * 2 * K];                 // per-warp crossing queue
     float sq[2 * K * kRefT];                                // per-thread p2 vertex table (kP2Smem), [k][thread]
     FlagLut lut;
-    int qn;
 };
 
 template <int K>
@@ -695,70 +696,63 @@ paired_fused_refine_kernel(int64_t n, const float *__restrict__ x1, const float 
                            const float *__restrict__ x2, const float *__restrict__ y2,
                            const float *__restrict__ grad, float scale, float *__restrict__ iou,
                            float *__restrict__ gx1, float *__restrict__ gy1, float *__restrict__ gx2,
-                           float *__restrict__ gy2, uint32_t *__restrict__ refine)
+                           float *__restrict__ gy2, RefineQueue *__restrict__ refine)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     RefineSmem<K> &S = *reinterpret_cast<RefineSmem<K> *>(smem_raw);
     const int tid = threadIdx.x;
-    fill_flag_lut(S.lut, tid, kRefT);
-    if (tid == 0) S.qn = 0;
-    __syncthreads();
-    const int64_t nwords = refine_words(n);
-    const int64_t nchunks = (nwords + kRefChunkWords - 1) / kRefChunkWords;
-#pragma unroll 1
-    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        refine_gather(refine, nwords, c, S.q, &S.qn);
-        __syncthreads();
-        const int total = S.qn;
-#pragma unroll 1
-        for (int base = 0; base < total; base += kRefT) {
-            const int e = base + tid;
-            const bool live = e < total;
-            const int64_t k = live ? c * kRefChunkPairs + S.q[e] : 0;
-            DGAL_ASSERT(!live || k < n);
-            Poly<K> P, Q;
-            if (live) {
-                load_poly<K>(x1, y1, k, P);
-                load_poly<K>(x2, y2, k, Q);
-            } else {
-#pragma unroll
-                for (int q = 0; q < K; ++q) { P.x[q] = P.y[q] = Q.x[q] = Q.y[q] = 0.f; }
-            }
-#pragma unroll
-            for (int q = 0; q < K; ++q) {
-                S.x1[tid * K + q] = P.x[q]; S.y1[tid * K + q] = P.y[q];
-                S.x2[tid * K + q] = Q.x[q]; S.y2[tid * K + q] = Q.y[q];
-            }
-            recentre<K>(P, Q);
-#pragma unroll
-            for (int q = 0; q < K; ++q) { S.sq[q * kRefT + tid] = Q.x[q]; S.sq[(K + q) * kRefT + tid] = Q.y[q]; }
-            FwdOut<K, true> r = iou_fwd<K, true, kP2Smem, true>(P, Q, QTable{S.sq + tid, S.sq + K * kRefT + tid, kRefT});
-            if (r.thin)
-                fwd_thin_fix<K>(RawPolyVerts{S.x1 + tid * K, S.y1 + tid * K, S.x2 + tid * K, S.y2 + tid * K}, r.seq,
-                                r.nx, r.iou);
-            if (live && iou) iou[k] = r.iou;
-            const float g = live ? (grad ? grad[k] : scale) : 0.f;
-            __syncwarp();   // the warp's tile is staged (the crossing queue reads other lanes' pairs)
-            Poly<K> G1, G2;
-            const bool thin = bwd_tile_pair<K, kRefT, TileGeometry<K>, false>(
-                S.x1, S.y1, S.x2, S.y2, r.seq, live ? r.nx : 0, g, live, S.scr, S.queue[tid >> 5], S.lut, G1, G2);
-            if (thin) bwd_pair_exact<K, kRefT>(S.x1, S.y1, S.x2, S.y2, tid, r.seq, r.nx, g, S.scr, S.lut, G1, G2);
-            if (live) {
-                store_plane<K>(gx1, k, G1.x);
-                store_plane<K>(gy1, k, G1.y);
-                store_plane<K>(gx2, k, G2.x);
-                store_plane<K>(gy2, k, G2.y);
-            }
-            __syncwarp();   // the tile is restaged next round
-        }
-        __syncthreads();
-        if (tid == 0) S.qn = 0;
+    const unsigned int total = refine_count(refine);
+    if ((unsigned int)blockIdx.x * kRefT < total) {
+        fill_flag_lut(S.lut, tid, kRefT);
         __syncthreads();
     }
+#pragma unroll 1
+    for (unsigned int base = blockIdx.x * kRefT; base < total; base += gridDim.x * kRefT) {
+        const unsigned int e = base + tid;
+        const bool live = e < total;
+        const int64_t k = live ? (int64_t)refine->idx[e] : 0;
+        DGAL_ASSERT(!live || k < n);
+        Poly<K> P, Q;
+        if (live) {
+            load_poly<K>(x1, y1, k, P);
+            load_poly<K>(x2, y2, k, Q);
+        } else {
+#pragma unroll
+            for (int q = 0; q < K; ++q) { P.x[q] = P.y[q] = Q.x[q] = Q.y[q] = 0.f; }
+        }
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+            S.x1[tid * K + q] = P.x[q]; S.y1[tid * K + q] = P.y[q];
+            S.x2[tid * K + q] = Q.x[q]; S.y2[tid * K + q] = Q.y[q];
+        }
+        recentre<K>(P, Q);
+#pragma unroll
+        for (int q = 0; q < K; ++q) { S.sq[q * kRefT + tid] = Q.x[q]; S.sq[(K + q) * kRefT + tid] = Q.y[q]; }
+        FwdOut<K, true> r = iou_fwd<K, true, kP2Smem, true>(P, Q, QTable{S.sq + tid, S.sq + K * kRefT + tid, kRefT});
+        if (r.thin)
+            fwd_thin_fix<K>(RawPolyVerts{S.x1 + tid * K, S.y1 + tid * K, S.x2 + tid * K, S.y2 + tid * K}, r.seq,
+                            r.nx, r.iou);
+        if (live && iou) iou[k] = r.iou;
+        const float g = live ? (grad ? grad[k] : scale) : 0.f;
+        __syncwarp();   // the warp's tile is staged (the crossing queue reads other lanes' pairs)
+        Poly<K> G1, G2;
+        const bool thin = bwd_tile_pair<K, kRefT, TileGeometry<K>, false>(
+            S.x1, S.y1, S.x2, S.y2, r.seq, live ? r.nx : 0, g, live, S.scr, S.queue[tid >> 5], S.lut, G1, G2);
+        if (thin) bwd_pair_exact<K, kRefT>(S.x1, S.y1, S.x2, S.y2, tid, r.seq, r.nx, g, S.scr, S.lut, G1, G2);
+        if (live) {
+            store_plane<K>(gx1, k, G1.x);
+            store_plane<K>(gy1, k, G1.y);
+            store_plane<K>(gx2, k, G2.x);
+            store_plane<K>(gy2, k, G2.y);
+        }
+        __syncwarp();   // the tile is restaged next round
+    }
+    __syncthreads();
+    if (tid == 0) refine_finish(refine);
 }
 
 namespace {
-int refine_grid(int64_t n)
+int refine_grid()
 {
     static DeviceCache cache;
     const int sms = cache.get([](int dev) {
@@ -766,14 +760,12 @@ int refine_grid(int64_t n)
         cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
         return s;
     });
-    const int64_t nchunks = (refine_words(n) + kRefChunkWords - 1) / kRefChunkWords;
-    const int64_t g = (int64_t)(sms > 0 ? sms : 148) * 4;
-    return (int)(nchunks < g ? nchunks : g);
+    return (sms > 0 ? sms : 148) * 2;
 }
 }  // namespace
 
-int refine_grid_for(int64_t n) { return refine_grid(n); }
-size_t refine_workspace_bytes(int64_t n) { return refine_mask_bytes(n); }
+int refine_grid_for(int64_t) { return refine_grid(); }
+size_t refine_workspace_bytes(int64_t n) { return refine_queue_bytes(n); }
 
 namespace {
 template <int K>
@@ -786,7 +778,7 @@ constexpr size_t fused_smem_bytes()
 template <int K>
 cudaError_t launch_fused_k(int64_t n, const float *x1, const float *y1, const float *x2, const float *y2,
                            const float *grad, float scale, float *iou, float *gx1, float *gy1, float *gx2,
-                           float *gy2, uint32_t *refine, cudaStream_t st)
+                           float *gy2, RefineQueue *refine, cudaStream_t st)
 {
     constexpr int T = (K == 4) ? kFused4Threads : kFused8Threads;
     constexpr bool PF = (K == 4) ? DGAL_FUSED_PF : DGAL_FUSED8_PF;
@@ -799,7 +791,7 @@ cudaError_t launch_fused_k(int64_t n, const float *x1, const float *y1, const fl
     if (b <= 0) return (cudaError_t)(-b);
     paired_fused_kernel<K><<<(unsigned)((n + per - 1) / per), T, smem, st>>>(n, x1, y1, x2, y2, grad, scale, iou,
                                                                                gx1, gy1, gx2, gy2, refine);
-    paired_fused_refine_kernel<K><<<(unsigned)refine_grid(n), kRefT, sizeof(RefineSmem<K>), st>>>(
+    paired_fused_refine_kernel<K><<<(unsigned)refine_grid(), kRefT, sizeof(RefineSmem<K>), st>>>(
         n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2, refine);
     return cudaGetLastError();
 }
@@ -807,10 +799,11 @@ cudaError_t launch_fused_k(int64_t n, const float *x1, const float *y1, const fl
 
 cudaError_t launch_paired_fused(int K, int64_t n, const float *x1, const float *y1, const float *x2,
                                 const float *y2, const float *grad, float scale, float *iou, float *gx1,
-                                float *gy1, float *gx2, float *gy2, uint32_t *refine, cudaStream_t st)
+                                float *gy1, float *gx2, float *gy2, void *refine, cudaStream_t st)
 {
-    if (K == 4) return launch_fused_k<4>(n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2, refine, st);
-    return launch_fused_k<8>(n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2, refine, st);
+    RefineQueue *q = static_cast<RefineQueue *>(refine);
+    if (K == 4) return launch_fused_k<4>(n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2, q, st);
+    return launch_fused_k<8>(n, x1, y1, x2, y2, grad, scale, iou, gx1, gy1, gx2, gy2, q, st);
 }
 
 }  // namespace dgal

@@ -68,8 +68,8 @@ def test_host_side_validation_without_gpu():
     # fused: misaligned dL/dIoU or IoU output (4 B), misaligned gradient plane (16 B),
     # refine workspace missing / too small / misaligned
     ws = L.dgal_fused_workspace_bytes(8)
-    assert ws == 8 and L.dgal_fused_workspace_bytes(1 << 24) == 4 * (1 << 19)
-    assert L.dgal_fused_workspace_bytes(65) == 16        # 3 words -> two 8-byte vectors
+    assert ws == 48 and L.dgal_fused_workspace_bytes(1 << 24) == 16 + 4 * (1 << 24)
+    assert L.dgal_fused_workspace_bytes(5) == 48        # 16 + 20 -> 48 (16-byte multiple)
     F1 = ctypes.c_float(1.0)
     assert L.dgal_iou_paired_fused(4, 8, P(a), P(a), P(a), P(a), P(a + 2), F1, None,
                                    P(a), P(a), P(a), P(a), P(a), ws, None) == 3
@@ -94,9 +94,10 @@ def test_host_side_validation_without_gpu():
     assert L.dgal_box_iou_paired_fwd(2, 0, 8, P(a), P(a), P(a), P(a), P(a + 4), None) == 3
     assert L.dgal_box_iou_paired_fwd(2, 0, 0, None, None, None, None, None, None) == 0
     assert L.dgal_box_iou_paired_bwd(3, 0, 8, P(a), P(a), None, P(a), P(a), P(a), P(a), None) == 1
-    assert L.dgal_box_iou_paired_fused(2, 0, 8, P(a), P(a), None, 1.0, None, None, P(a), P(a), 8, None) == 1
-    assert L.dgal_box_iou_paired_fused(2, 0, 8, P(a), P(a), None, 1.0, None, P(a), P(a), None, 8, None) == 1
-    assert L.dgal_box_iou_paired_fused(2, 0, 8, P(a), P(a), None, 1.0, None, P(a), P(a), P(a + 4), 8, None) == 3
+    assert L.dgal_box_iou_paired_fused(2, 0, 8, P(a), P(a), None, 1.0, None, None, P(a), P(a), 48, None) == 1
+    assert L.dgal_box_iou_paired_fused(2, 0, 8, P(a), P(a), None, 1.0, None, P(a), P(a), None, 48, None) == 1
+    assert L.dgal_box_iou_paired_fused(2, 0, 8, P(a), P(a), None, 1.0, None, P(a), P(a), P(a), 47, None) == 1
+    assert L.dgal_box_iou_paired_fused(2, 0, 8, P(a), P(a), None, 1.0, None, P(a), P(a), P(a + 4), 48, None) == 3
     # pairwise: nothing requested, negative threshold with a mask, short mask rows
     args = [4, 8, P(a), P(a), 8, P(a), P(a), 0]
     assert L.dgal_iou_pairwise(*args, None, 0.5, None, 0, None, None, 0, None, 0, None) == 1
