@@ -373,6 +373,45 @@ struct BwdPtSmem {
     uint32_t thinm[T];   // per thread: tiles whose pair is thin (kept here, not in a register: the loop is at 72)
 };
 
+// The per-thread backward's thin-pair redo (after its tile loop), out of line: its
+// code then does not enter the register allocation of the hot loop.
+template <int K>
+__device__ __noinline__ void bwd_pt_thin_redo(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
+                                              const float *__restrict__ x2, const float *__restrict__ y2,
+                                              const float *__restrict__ grad, const uint8_t *__restrict__ xflags,
+                                              float *__restrict__ gx1, float *__restrict__ gy1,
+                                              float *__restrict__ gx2, float *__restrict__ gy2, BwdPtSmem<K> &S)
+{
+    constexpr int T = kBwdPtThreads, NT = DGAL_BWDPT_NT;
+    const int tid = threadIdx.x;
+    uint32_t thinmask = S.thinm[tid];
+    typename BwdPtSmem<K>::Stage &D = S.st[0];
+    const int64_t chunk = DGAL_BWD_REV ? (int64_t)(gridDim.x - 1 - blockIdx.x) : (int64_t)blockIdx.x;
+    const int64_t base = chunk * (NT * T);
+    const int nv = (int)min((int64_t)NT, (n - base + T - 1) / T);
+#pragma unroll 1
+    while (thinmask) {
+        const int t = __ffs(thinmask) - 1;
+        thinmask &= thinmask - 1u;
+        const int64_t k = base + (int64_t)(DGAL_BWD_REV ? (nv - 1 - t) : t) * T + tid;
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+            D.x1[tid * K + q] = x1[k * K + q]; D.y1[tid * K + q] = y1[k * K + q];
+            D.x2[tid * K + q] = x2[k * K + q]; D.y2[tid * K + q] = y2[k * K + q];
+        }
+        Seq<K> sq;
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q) sq.w[q] = reinterpret_cast<const uint64_t *>(xflags)[k * (K / 4) + q];
+        Poly<K> G1, G2;
+        bwd_pair_exact<K, T, K == 4>(D.x1, D.y1, D.x2, D.y2, tid, sq, record_len<K>(sq), grad[k], S.scr, S.lut, G1,
+                                     G2);
+        store_plane<K>(gx1, k, G1.x);
+        store_plane<K>(gy1, k, G1.y);
+        store_plane<K>(gx2, k, G2.x);
+        store_plane<K>(gy2, k, G2.y);
+    }
+}
+
 template <int K>
 __global__ void __launch_bounds__(kBwdPtThreads, (K == 4) ? DGAL_BWDPT_MINB : DGAL_BWDPT8_MINB)
 paired_bwd_pt_kernel(int64_t n, const float *__restrict__ x1, const float *__restrict__ y1,
@@ -452,36 +491,7 @@ paired_bwd_pt_kernel(int64_t n, const float *__restrict__ x1, const float *__res
     return;
 #endif
     cp_async_wait<0>();
-    uint32_t thinmask = S.thinm[tid];
-    typename BwdPtSmem<K>::Stage &D = S.st[0];
-    // the chunk's first pair recomputed from the CTA index (volatile: not kept live
-    // through the loop, which is at its register budget)
-    uint32_t cta, ncta;
-    asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(cta));
-    asm volatile("mov.u32 %0, %%nctaid.x;" : "=r"(ncta));
-    const int64_t base2 = (int64_t)(DGAL_BWD_REV ? (ncta - 1u - cta) : cta) * (NT * T);
-    const int nv2 = (int)min((int64_t)NT, (n - base2 + T - 1) / T);
-#pragma unroll 1
-    while (thinmask) {
-        const int t = __ffs(thinmask) - 1;
-        thinmask &= thinmask - 1u;
-        const int64_t k = base2 + (int64_t)(DGAL_BWD_REV ? (nv2 - 1 - t) : t) * T + tid;
-#pragma unroll
-        for (int q = 0; q < K; ++q) {
-            D.x1[tid * K + q] = x1[k * K + q]; D.y1[tid * K + q] = y1[k * K + q];
-            D.x2[tid * K + q] = x2[k * K + q]; D.y2[tid * K + q] = y2[k * K + q];
-        }
-        Seq<K> sq;
-#pragma unroll
-        for (int q = 0; q < K / 4; ++q) sq.w[q] = reinterpret_cast<const uint64_t *>(xflags)[k * (K / 4) + q];
-        Poly<K> G1, G2;
-        bwd_pair_exact<K, T, K == 4>(D.x1, D.y1, D.x2, D.y2, tid, sq, record_len<K>(sq), grad[k], S.scr, S.lut, G1,
-                                     G2);
-        store_plane<K>(gx1, k, G1.x);
-        store_plane<K>(gy1, k, G1.y);
-        store_plane<K>(gx2, k, G2.x);
-        store_plane<K>(gy2, k, G2.y);
-    }
+    if (S.thinm[tid]) bwd_pt_thin_redo<K>(n, x1, y1, x2, y2, grad, xflags, gx1, gy1, gx2, gy2, S);
 }
 
 cudaError_t launch_paired_fwd(int K, int64_t n, const float *x1, const float *y1, const float *x2,
@@ -574,6 +584,9 @@ cudaError_t launch_paired_bwd(int K, int64_t n, const float *x1, const float *y1
 #endif
 constexpr int kFused4Threads = DGAL_FUSED4_THREADS, kFused8Threads = DGAL_FUSED8_THREADS;
 
+#ifndef DGAL_FUSED_NEED
+#define DGAL_FUSED_NEED 1     // mark nearly parallel crossings / thin pairs for the refine pass (A/B switch)
+#endif
 #ifndef DGAL_FUSED_PF
 #define DGAL_FUSED_PF 1       // NT consecutive tiles per CTA, tile t+1 copied (cp.async) while tile t computes
 #endif
@@ -661,10 +674,10 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
             if (grad) g = __ldcs(grad + k);
         }
         recentre<K>(P, Q);
-        bool need;
+        bool need = false;
         const float v = iou_fused<K, DGAL_FUSED_P2MODE, K == 4 && DGAL_FUSED_PK>(
-            P, Q, g, G1, G2, flat(), nullptr, QTable{pt + tid, pt + 2 * K * T + tid, T}, &need,
-            IllTab{illt + tid, T});
+            P, Q, g, G1, G2, flat(), nullptr, QTable{pt + tid, pt + 2 * K * T + tid, T},
+            DGAL_FUSED_NEED ? &need : nullptr, IllTab{illt + tid, T});
         refine_mark(refine, k, need);   // redone exactly by paired_fused_refine_kernel
         if (iou) __stcs(iou + k, v);
         store_plane<K>(gx1, k, G1.x);
