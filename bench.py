@@ -39,11 +39,12 @@ UNIT = "pairs/s"
 
 def algorithmic_bytes(K):
     """Per pair: fwd reads 2 polygons (16 K B) and writes iou 4 +
-    nx 1 + xflags 2K; bwd reads the polygons, g 4, nx 1, xflags 2K and writes the
-    two gradient polygons (16 K B)."""
+    nx 1 + xflags 2K; bwd reads the polygons, g 4, xflags 2K (and nx 1 for K = 8:
+    the K = 4 kernel takes nx from the record's zero padding) and writes the two
+    gradient polygons (16 K B)."""
     poly = 16 * K
     fwd = poly + 4 + 1 + 2 * K
-    bwd = poly + 4 + 1 + 2 * K + poly
+    bwd = poly + 4 + (0 if K == 4 else 1) + 2 * K + poly
     return fwd, bwd
 
 

@@ -17,6 +17,7 @@ KEYS = [  # (key, kernel regex); first match in launch order (the second pw_zero
     ("box_fwd_d2", r"box_fwd_kernel<2>"), ("box_bwd_d2", r"box_bwd_kernel<2>"), ("box_fused_d2", r"box_fused_kernel<2>"),
     ("box_fwd_d3", r"box_fwd_kernel<3>"), ("box_bwd_d3", r"box_bwd_kernel<3>"), ("box_fused_d3", r"box_fused_kernel<3>"),
     ("pw_zero_iou", r"pw_zero"), ("pw_candidates_k4", r"pw_candidates<4>"), ("nms_keep", r"nms_keep"),
+    ("paired_fused_refine_k4", r"paired_fused_refine_kernel<4>"), ("box_fused_refine_d2", r"box_fused_refine_kernel<2>"),
 ]
 
 
@@ -27,7 +28,7 @@ def main(path):
         d = next((d for d in launches if re.search(rx, d["kernel"])), None)
         if d is not None:
             out[f"{key}_bytes_per_launch"] = int(round((d["dram_read_GB"] + d["dram_write_GB"]) * 1e9, -3))
-    out["source"] = ("profiles/r01_ncu_full_summary.json (ncu --set full --clock-control none, "
+    out["source"] = (f"{sys.argv[2] if len(sys.argv) > 2 else path} (ncu --set full --clock-control none, "
                      "tools/prof_run.py --once, B200)")
     print(json.dumps(out, indent=1))
 

@@ -32,8 +32,7 @@ def main():
         for _ in range(reps):
             iou, nx, xf = dgal.iou_paired_fwd(x1, y1, x2, y2)
             dgal.iou_paired_bwd(x1, y1, x2, y2, g, nx, xf)
-            if cfg == 3:
-                dgal.iou_paired_fused(x1, y1, x2, y2, scale=-1.0 / n)
+            dgal.iou_paired_fused(x1, y1, x2, y2, scale=-1.0 / n)
         torch.cuda.synchronize()
         del x1, y1, x2, y2, g, iou, nx, xf
     if "box" in which:
