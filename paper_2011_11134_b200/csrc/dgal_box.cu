@@ -514,7 +514,7 @@ box_fused_kernel(int64_t n, const float *__restrict__ b1, const float *__restric
         const ZOver z = z_overlap<DIMS>(a, b);
         VolCoef co;
         bool need;
-        const float v = iou_fused<4, kP2PiecesSmem, DIMS == 2 && DGAL_BOX_FUSED_PK>(
+        const float v = iou_fused<4, kP2PiecesSmem, DIMS == 2 && DGAL_BOX_FUSED_PK, 0>(
             P, Q, g, G1, G2, Extrude{z.dz, a.d, b.d}, &co, QTable{pt + tid, pt + 8 * T + tid, T}, &need,
             IllTab{nullptr, 0, BoxGeometry::kRefine});
         refine_mark(refine, k, need);   // redone exactly by box_fused_refine_kernel

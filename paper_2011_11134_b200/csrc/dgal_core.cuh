@@ -241,6 +241,9 @@ __device__ __forceinline__ uint32_t seq_byte(const Seq<K> &s, int p)  // p stati
 
 }  // namespace dgal
 
+#ifndef DGAL_SEPT_FUSED
+#define DGAL_SEPT_FUSED 1   // the fused kernels keep the explicit separating-line test (A/B switch)
+#endif
 #ifndef DGAL_THIN
 #define DGAL_THIN 1     // thin / sliver pairs: areas of the recorded intersection in double (dgal_exact.cuh)
 #endif
@@ -287,8 +290,11 @@ constexpr float kThinRatio = 8.f;
 template <int K>
 __device__ __forceinline__ float pair_extent2(const Poly<K> &P, const Poly<K> &Q)
 {
-#ifdef DGAL_THIN_SUMSQ
-    // sum of the squared vertex norms (>= R^2; <= 2K R^2): paired accumulation, no max chain
+#ifndef DGAL_THIN_SUMSQ
+#define DGAL_THIN_SUMSQ 4   // the K for which R^2 is taken as (sum of squared norms) / 2K (A/B: K = 4 faster)
+#endif
+    if (K == DGAL_THIN_SUMSQ) {
+    // mean of the squared vertex norms (<= R^2 <= 2K x it): paired accumulation, no max chain
     uint64_t acc = 0ull;
 #pragma unroll
     for (int q = 0; q < K / 2; ++q) {
@@ -299,7 +305,7 @@ __device__ __forceinline__ float pair_extent2(const Poly<K> &P, const Poly<K> &Q
     float a, b;
     f2unpack(acc, a, b);
     return (a + b) * (1.f / (2 * K));
-#endif
+    }
     // p2's vertices two per paired instruction, in the (2q, 2q+1) pairs the decision
     // rows pack (no register moves); p1's scalar (P.x[0] = P.y[0] = 0 after recentring)
     float r = 0.f;
@@ -498,7 +504,7 @@ struct IllTab {
 // denominators are exactly these cross products) — a superset of the pairs with an
 // ill-conditioned crossing (nearly parallel edges that do not cross — the opposite
 // sides of two nearly aligned boxes — do not count: ~100x fewer pairs marked).
-template <int K, int MODE, bool ILL = false>
+template <int K, int MODE, bool ILL = false, int ILLG = -1>
 __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &Q, Clip<K> &c,
                                                QTable qt = QTable{nullptr, nullptr, 0},
                                                const WalkLut4 *wl = nullptr, IllTab it = IllTab{nullptr, 0})
@@ -510,7 +516,7 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     // the clip finds no piece and no p2 vertex inside.  Dropped (K^2 max operations:
     // cfg3 forward -2.4 %, cfg4 -6 %; the GPU suite is unchanged); the fused kernels
     // (ILL) keep it — without it ptxas spills the K = 4 one.
-    constexpr bool SEPT = ILL;
+    constexpr bool SEPT = DGAL_SEPT_FUSED && ILL;
     constexpr bool PIECES = (MODE == kP2Pieces || MODE == kP2PiecesSmem);
     constexpr bool PSMEM = (MODE == kP2PiecesSmem);
     constexpr uint32_t KMASK = (1u << K) - 1u;
@@ -590,10 +596,16 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     // standing in for each is conservative: a shorter edge is tested against a larger |sin|).
     uint32_t illacc = 0u;
     constexpr bool NSF_REG = (K == 4) || !ILL;
+#ifndef DGAL_ILL_GMAX
+#define DGAL_ILL_GMAX 1   // K = 4 too: max |g|^2 folded into the per-line factors (A/B: fused K=4 -1 %)
+#endif
+    // ILLG: 1 max|g|^2 folded in, 0 per-edge |g_i|^2 (boxes: their larger threshold would
+    // queue ~2x more pairs), -1 the build default
+    constexpr bool GMAX = !NSF_REG || (ILLG < 0 ? DGAL_ILL_GMAX : ILLG);
     uint64_t nsf[(ILL && NSF_REG) ? K / 2 : 1];
     if (ILL) {
         float gmax = 1.f;
-        if (!NSF_REG) {
+        if (GMAX) {
             gmax = 0.f;
 #pragma unroll
             for (int i = 0; i < K; ++i) gmax = fmaxf(gmax, fmaf(gx[i], gx[i], gy[i] * gy[i]));
@@ -654,7 +666,7 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
         // ILL, K = 4: this edge's |g|^2 (K = 8: folded into the table as max |g|^2)
         uint64_t g2 = 0ull;
         float gg = 1.f;
-        if (ILL && NSF_REG) {
+        if (ILL && !GMAX) {
             gg = fmaf(gx[i], gx[i], gy[i] * gy[i]);
             g2 = f2pack(gg, gg);
         }
@@ -668,7 +680,8 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
                 float d0_, d1_;
                 f2unpack(den, d0_, d1_);
                 if (ILL) {
-                    const uint64_t thr = NSF_REG ? f2mul(g2, nsf[NSF_REG ? q : 0]) : it.p[q * it.st];
+                    const uint64_t thr = !NSF_REG ? it.p[q * it.st]
+                                         : (GMAX ? nsf[NSF_REG ? q : 0] : f2mul(g2, nsf[NSF_REG ? q : 0]));
                     float x0, x1, p0, p1;
                     f2unpack(f2fma(den, den, thr), x0, x1);
                     // (- 1e-26: an end point exactly on the line, d = +tiny = 1e-30, counts as a
@@ -960,6 +973,28 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
     return out;
 }
 
+// The IoU of a thin pair for the pairwise evaluators (their clip records no flags):
+// out of line (rare; the evaluators are at their register budget) — the clip again
+// with the flag walk from the raw vertices (px[k], py[k]: p1 = the row, qx, qy: p2 =
+// the column; global or shared memory), then the areas of the recorded
+// intersection in double (dgal_exact.cuh), as the split forward does.
+template <int K>
+__device__ __noinline__ float pair_iou_exact(const float *px, const float *py, const float *qx, const float *qy)
+{
+    Poly<K> P, Q;
+    const float ox = px[0], oy = py[0];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        P.x[k] = __fsub_rn(px[k], ox); P.y[k] = __fsub_rn(py[k], oy);
+        Q.x[k] = __fsub_rn(qx[k], ox); Q.y[k] = __fsub_rn(qy[k], oy);
+    }
+    P.x[0] = 0.f;
+    P.y[0] = 0.f;
+    FwdOut<K, true> r = iou_fwd<K, true, kP2Regs, true>(P, Q);
+    if (r.thin || r.nx > 0) fwd_thin_fix<K>(RawPolyVerts{px, py, qx, qy}, r.seq, r.nx, r.iou);
+    return r.iou;
+}
+
 // ---------------------------------------------------------------------------
 // fused IoU forward + backward for a loss whose dL/dIoU is known up front
 // (e.g. L = mean(1 - IoU) has dL/dIoU = -1/n)
@@ -972,7 +1007,7 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
 // (p1 edge, p2 edge) pair (crossing parameters conditioned by 1/sin) or a thin pair
 // (area sum conditioned by R^2 / A_u) — and the caller must have the pair redone by
 // the exact split path (the fused kernels' refine pass).
-template <int K, int MODE = kP2Pieces, bool PK = false>
+template <int K, int MODE = kP2Pieces, bool PK = false, int ILLG = -1>
 __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, float g, Poly<K> &G1,
                                            Poly<K> &G2, const Extrude ex = flat(), VolCoef *co = nullptr,
                                            QTable qt = QTable{nullptr, nullptr, 0}, bool *need = nullptr,
@@ -983,7 +1018,7 @@ __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, f
     if (co) *co = VolCoef{0.f, 0.f, 0.f, 0.f, 0.f};
     if (need) *need = false;
     Clip<K> c;
-    if (need) clip_intervals<K, MODE, true>(P, Q, c, qt, nullptr, it);
+    if (need) clip_intervals<K, MODE, true, ILLG>(P, Q, c, qt, nullptr, it);
     else clip_intervals<K, MODE, false>(P, Q, c, qt);
     const float R2 = need ? pair_extent2<K>(P, Q) : 0.f;   // (after the clip: not live through it)
     if (!c.nonempty) {

@@ -115,7 +115,11 @@ pairwise_kernel(int64_t n_rows, const float *__restrict__ rxg, const float *__re
         }
         Pc.x[0] = 0.f;   // exact for finite input; lets the compiler fold it
         Pc.y[0] = 0.f;
-        const float v = iou_fwd<K, false>(Pc, Qc).iou;
+        const FwdOut<K, false> fo = iou_fwd<K, false>(Pc, Qc);
+        float v = fo.iou;
+        // thin pair (R^2 > kThinRatio A_u): the area of the recorded intersection in double
+        if (DGAL_THIN && pair_is_thin(pair_extent2<K>(Pc, Qc), (fo.A1x2 + fo.A2x2) - fo.Aix2))
+            v = pair_iou_exact<K>(px, py, qx, qy);
         const int64_t r = r0 + rl, c = c0 + cl;
         if (iou) iou[r * m + c] = v;
         const int64_t grow = row_offset + r;

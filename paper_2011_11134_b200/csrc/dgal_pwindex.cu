@@ -296,7 +296,11 @@ pw_candidates(int64_t n_rows, const float *__restrict__ rx, const float *__restr
         }
         P.x[0] = 0.f;   // exact for finite input; lets the compiler fold it
         P.y[0] = 0.f;
-        const float v = iou_fwd<K, false>(P, Q).iou;
+        const FwdOut<K, false> fo = iou_fwd<K, false>(P, Q);
+        float v = fo.iou;
+        // thin pair (R^2 > kThinRatio A_u): the area of the recorded intersection in double
+        if (DGAL_THIN && pair_is_thin(pair_extent2<K>(P, Q), (fo.A1x2 + fo.A2x2) - fo.Aix2))
+            v = pair_iou_exact<K>(rx + rr * K, ry + rr * K, cxg + (int64_t)c * K, cyg + (int64_t)c * K);
         if (iou && v != 0.f) iou[rr * m + c] = v;
         const int64_t grow = row_offset + rr;
         if (v > thr && c != grow) {

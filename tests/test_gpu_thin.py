@@ -70,3 +70,24 @@ def test_thin_fused(K, verts, aspect):
     rg = oracle.iou_paired_bwd(p1, p2, b.grad)
     for got, want in zip(gr, rg):
         assert_grad_close(_fold(got, verts)[ok], want[ok])
+
+
+@pytest.mark.parametrize("K,verts,aspect", [(4, 3, 300.0), (4, 4, 300.0), (8, 8, 300.0), (8, 5, 300.0),
+                                            (4, 3, 100.0), (8, 5, 100.0)])
+@pytest.mark.parametrize("indexed", [True, False])
+def test_thin_pairwise(K, verts, aspect, indexed):
+    """The pairwise evaluators (grid-indexed and tiled): rows = the thin p1 of 1024
+    pairs, columns = their p2 — the full 1024 x 1024 matrix against the oracle at
+    1e-5 (thin candidates recomputed from the recorded intersection in double)."""
+    b, X, p1, p2 = _case(K, verts, aspect)
+    m = 1024
+    x1, y1, x2, y2 = (t[:m].contiguous() for t in X)
+    got = dgal.iou_pairwise(x1, y1, x2, y2, want_mask=False, indexed=indexed)[0].cpu().numpy()
+    # the oracle on the padded polygons (a repeated vertex is a zero-length edge: same polygon)
+    P = synth.Polys(np.ascontiguousarray(b.p1.x.reshape(N, K)[:m].reshape(-1)),
+                    np.ascontiguousarray(b.p1.y.reshape(N, K)[:m].reshape(-1)), K)
+    Q = synth.Polys(np.ascontiguousarray(b.p2.x.reshape(N, K)[:m].reshape(-1)),
+                    np.ascontiguousarray(b.p2.y.reshape(N, K)[:m].reshape(-1)), K)
+    ref = oracle.iou_pairwise(P, Q)
+    assert (np.diag(ref) > 0).mean() > 0.85
+    assert np.abs(got - ref).max() <= 1e-5
