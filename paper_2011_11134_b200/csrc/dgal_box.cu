@@ -31,10 +31,10 @@ namespace {
 #define DGAL_BOX_BWD_TILE 128
 #endif
 #ifndef DGAL_BOX_BWD2_MINB
-#define DGAL_BOX_BWD2_MINB 6   // 80 registers (the thin-pair redo, dgal_exact.cuh; 7 CTAs spill)
+#define DGAL_BOX_BWD2_MINB 7
 #endif
 #ifndef DGAL_BOX_BWD3_MINB
-#define DGAL_BOX_BWD3_MINB 5   // 96 registers (6 CTAs spill with the thin-pair redo)
+#define DGAL_BOX_BWD3_MINB 6
 #endif
 #ifndef DGAL_BOX_FUSED_PK
 #define DGAL_BOX_FUSED_PK true   // 2D: gradient part in paired FP32 (A/B: 0.593 -> 0.584 ms; 3D 0.674 -> 0.683, not used)
@@ -402,6 +402,33 @@ struct BoxBwdSmem {
     FlagLut lut;
 };
 
+// A thin pair of the box backward (rare): the intersection area in double from the
+// corner tile, the gradients again — out of line, everything re-read, so its code
+// does not enter the hot path's register allocation.
+template <int DIMS>
+__device__ __noinline__ void box_bwd_thin_redo(const float *__restrict__ b1, const float *__restrict__ b2,
+                                               int64_t sk, int64_t sp, const float *__restrict__ grad,
+                                               const uint8_t *__restrict__ nx, const uint8_t *__restrict__ xflags,
+                                               float *__restrict__ gb1, float *__restrict__ gb2, int64_t k,
+                                               BoxBwdSmem &S)
+{
+    const Box<DIMS> a = load_box<DIMS>(b1, k, sk, sp), b = load_box<DIMS>(b2, k, sk, sp);
+    const ZOver z = z_overlap<DIMS>(a, b);
+    Seq<4> s2;
+    s2.w[0] = __ldcs(reinterpret_cast<const unsigned long long *>(xflags) + k);
+    Poly<4> G1, G2;
+    VolCoef co;
+    bwd_thin_redo<4, kBoxTile>(S.x1, S.y1, S.x2, S.y2, s2, nx[k], __ldcs(grad + k), S.scr, S.lut, G1, G2,
+                               Extrude{z.dz, a.d, b.d}, &co);
+    Trig t;
+    box_sincos(a.th, t.s1, t.c1);
+    box_sincos(b.th, t.s2, t.c2);
+    float gcz1, gd1, gcz2, gd2;
+    z_grads<DIMS>(co, z, gcz1, gd1, gcz2, gd2);
+    store_box_grad<DIMS>(gb1, k, sk, sp, box_vjp(a.w, a.h, t.c1, t.s1, G1), gcz1, gd1);
+    store_box_grad<DIMS>(gb2, k, sk, sp, box_vjp(b.w, b.h, t.c2, t.s2, G2), gcz2, gd2);
+}
+
 template <int DIMS>
 __global__ void __launch_bounds__(kBoxTile, DIMS == 2 ? DGAL_BOX_BWD2_MINB : DGAL_BOX_BWD3_MINB)
 box_bwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict__ b2, int64_t sk, int64_t sp,
@@ -454,21 +481,7 @@ box_bwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
     z_grads<DIMS>(co, z, gcz1, gd1, gcz2, gd2);
     store_box_grad<DIMS>(gb1, k, sk, sp, box_vjp(a.w, a.h, t.c1, t.s1, G1), gcz1, gd1);
     store_box_grad<DIMS>(gb2, k, sk, sp, box_vjp(b.w, b.h, t.c2, t.s2, G2), gcz2, gd2);
-    if (thin) {   // thin pair: intersection area in double from the corner tile, gradients again (rare)
-        // everything re-read (the first pass's values are dead: no register pressure on the common path)
-        const Box<DIMS> a2 = load_box<DIMS>(b1, k, sk, sp), b2_ = load_box<DIMS>(b2, k, sk, sp);
-        const ZOver z2 = z_overlap<DIMS>(a2, b2_);
-        Seq<4> s2;
-        s2.w[0] = __ldcs(reinterpret_cast<const unsigned long long *>(xflags) + k);
-        bwd_thin_redo<4, kBoxTile>(S.x1, S.y1, S.x2, S.y2, s2, nx[k], __ldcs(grad + k), S.scr, S.lut, G1, G2,
-                                   Extrude{z2.dz, a2.d, b2_.d}, &co);
-        Trig t2;
-        box_sincos(a2.th, t2.s1, t2.c1);
-        box_sincos(b2_.th, t2.s2, t2.c2);
-        z_grads<DIMS>(co, z2, gcz1, gd1, gcz2, gd2);
-        store_box_grad<DIMS>(gb1, k, sk, sp, box_vjp(a2.w, a2.h, t2.c1, t2.s1, G1), gcz1, gd1);
-        store_box_grad<DIMS>(gb2, k, sk, sp, box_vjp(b2_.w, b2_.h, t2.c2, t2.s2, G2), gcz2, gd2);
-    }
+    if (thin) box_bwd_thin_redo<DIMS>(b1, b2, sk, sp, grad, nx, xflags, gb1, gb2, k, S);
 }
 
 // ---------------------------------------------------------------------------
