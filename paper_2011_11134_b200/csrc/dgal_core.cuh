@@ -415,6 +415,64 @@ __device__ __forceinline__ void load_walk_lut4(WalkLut4 &dst, int tid, int nthre
     for (int q = tid; q < (int)(sizeof(WalkLut4) / 16); q += nthreads) d[q] = __ldg(s + q);
 }
 
+// Walk tables for K = 8 (the paired forward's flag walk).  The
+// K = 4 table keyed by the whole p2 inside mask would be 2^8 x 8 x 8 entries; the
+// K = 8 walk splits it in two small lookups instead:
+//   L[in2 << 3 | jo]: the length of the run of p2 vertices inside p1 after p2
+//     edge jo (trailing ones of in2 rotated right by jo + 1; 0..8);
+//   g[jo * 9 + L]: the bytes after byte 0 of a p1 edge's group when it exits
+//     across p2 line jo followed by that run — {bytes lo, bytes hi, -, count}:
+//       byte 1   the exit Cross(i, jo) = 0xC0 | i << 3 | jo   (without i << 3)
+//       byte 2.. FromP2(jo+1), ..., FromP2(jo+L)      (up to 8: bytes 8, 9 in hi)
+//     count = 2 + L; g[72] = {0, 0, 0, 1} (a valid edge without an exit: byte 0
+//     only), g[73] = all 0 (an invalid edge).
+// Byte 0 (FromP1(i) or the entry Cross(i, j_in)) and the i << 11 of byte 1 are
+// OR-ed in by the caller (static shared memory: the table must stay small).
+struct alignas(16) WalkLut8 {
+    uint32_t g[74][4];
+    uint8_t L[256 * 8];
+};
+
+constexpr WalkLut8 make_walk_lut8()
+{
+    WalkLut8 W{};
+    {
+        for (uint32_t jo = 0; jo < 8; ++jo) {
+            for (uint32_t L = 0; L <= 8; ++L) {
+                uint64_t lo = (uint64_t)(0xC0u | jo) << 8, hi = 0;
+                for (uint32_t r = 0; r < L; ++r) {
+                    const uint64_t b = 0x80u | ((jo + 1u + r) & 7u);
+                    const uint32_t at = 2u + r;
+                    if (at < 8u) lo |= b << (8u * at);
+                    else hi |= b << (8u * (at - 8u));
+                }
+                uint32_t *e = W.g[jo * 9 + L];
+                e[0] = (uint32_t)lo; e[1] = (uint32_t)(lo >> 32); e[2] = (uint32_t)hi; e[3] = 2u + L;
+            }
+        }
+        W.g[72][3] = 1u;
+    }
+    for (uint32_t in2 = 0; in2 < 256; ++in2) {
+        for (uint32_t jo = 0; jo < 8; ++jo) {
+            const uint32_t p0 = (jo + 1u) & 7u;
+            const uint32_t rot = ((in2 | (in2 << 8)) >> p0) & 0xFFu;
+            uint32_t L = 0;
+            while (L < 8u && ((rot >> L) & 1u)) ++L;
+            W.L[in2 << 3 | jo] = (uint8_t)L;
+        }
+    }
+    return W;
+}
+
+static __device__ const WalkLut8 kWalkLut8 = make_walk_lut8();
+
+__device__ __forceinline__ void load_walk_lut8(WalkLut8 &dst, int tid, int nthreads)
+{
+    const uint4 *s = reinterpret_cast<const uint4 *>(&kWalkLut8);
+    uint4 *d = reinterpret_cast<uint4 *>(&dst);
+    for (int q = tid; q < (int)(sizeof(WalkLut8) / 16); q += nthreads) d[q] = __ldg(s + q);
+}
+
 // The edge-interval clip shared by the paired forward, the pairwise path and the
 // fused loss kernel.
 //
@@ -858,7 +916,8 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
 template <int K, bool FLAGS, int MODE = (K == 4 ? kP2Pieces : kP2Regs), bool THIN = false>
 __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly<K> &Q,
                                                     QTable qt = QTable{nullptr, nullptr, 0},
-                                                    const WalkLut4 *wl = nullptr)
+                                                    const WalkLut4 *wl = nullptr,
+                                                    const WalkLut8 *wl8 = nullptr)
 {
     constexpr uint32_t KMASK = (1u << K) - 1u;
     Clip<K> c;
@@ -908,6 +967,27 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
                 w |= shl64((uint64_t)ghi[i] << 32 | glo[i], (off >> (8 * i)) & 0xFFu);
             s.w[0] = w;
             pos = (int)((cnt * 0x01010101u) >> 24);
+        } else if (K == 8 && wl8 != nullptr) {
+            // table walk (WalkLut8): run length, then the group's bytes 1.. and count
+            const uint8_t *Lrow = wl8->L + (in2 << 3);
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                const bool valid = (c.valid >> i) & 1u;
+                const bool has_in = (c.enter >> i) & 1u;
+                const bool has_out = (c.leave >> i) & 1u;
+                const uint32_t jo = (c.jout >> (4 * i)) & 7u;
+                const uint32_t L = Lrow[jo];
+                const uint32_t idx = has_out ? jo * 9u + L : (valid ? 72u : 73u);
+                const uint4 e = *reinterpret_cast<const uint4 *>(wl8->g[idx]);
+                const uint32_t b0 = has_in ? (0xC0u | (i << 3) | ((c.jin >> (4 * i)) & 7u))
+                                           : (valid ? (0x40u | i) : 0u);
+                const uint64_t glo = ((uint64_t)e.y << 32 | e.x) | b0 | (has_out ? (uint32_t)i << 11 : 0u);
+                const uint64_t ghi = e.z;
+                const uint32_t sh = 8u * (uint32_t)pos;
+                s.w[0] |= shl64(glo, sh);
+                s.w[Seq<K>::NW - 1] |= (sh >= 64u) ? shl64(glo, sh - 64u) : (shr64(glo, 64u - sh) | shl64(ghi, sh));
+                pos += (int)e.w;
+            }
         } else {
 #pragma unroll
         for (int i = 0; i < K; ++i) {

@@ -56,6 +56,9 @@ constexpr int kFwd4Threads = DGAL_FWD4_THREADS;
 #ifndef DGAL_FWD8_NT
 #define DGAL_FWD8_NT 4         // K = 8: 4 tiles per CTA with the cp.async prefetch (A/B: 0.373 -> 0.367 ms)
 #endif
+#ifndef DGAL_FWD8_WALKLUT
+#define DGAL_FWD8_WALKLUT 1   // K = 8: the flag walk from WalkLut8 (dgal_core.cuh)
+#endif
 #ifndef DGAL_FWD8_PREFETCH
 #define DGAL_FWD8_PREFETCH 1
 #endif
@@ -72,9 +75,11 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
 {
     constexpr int T = (K == 4) ? kFwd4Threads : kFwd8Threads;
     constexpr bool WL = (K == 4) && DGAL_FWD4_WALKLUT;
+    constexpr bool WL8 = (K == 8) && DGAL_FWD8_WALKLUT;
     constexpr int NT = (K == 4) ? DGAL_FWD4_NT : DGAL_FWD8_NT;
     __shared__ float sq[2 * K * T];   // per-thread p2 vertex table, [k][thread] (DGAL_FWD_P2MODE == kP2Smem)
     __shared__ WalkLut4 wlut[1];      // K = 4: the walk tables (DGAL_FWD4_WALKLUT; unused otherwise)
+    __shared__ WalkLut8 wlut8[1];     // K = 8: the walk tables (DGAL_FWD8_WALKLUT; unused otherwise)
     constexpr bool PF = (K == 4) ? DGAL_FWD4_PREFETCH : DGAL_FWD8_PREFETCH;
     // PF: 2-stage per-thread ring [stage][plane][thread][K] (each thread copies and
     // reads only its own 64 bytes: no CTA barrier, cp.async groups order it)
@@ -101,6 +106,10 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
     }
     if (WL) {
         load_walk_lut4(wlut[0], threadIdx.x, T);
+        __syncthreads();
+    }
+    if (WL8) {
+        load_walk_lut8(wlut8[0], threadIdx.x, T);
         __syncthreads();
     }
     QTable qt{sq + threadIdx.x, sq + K * T + threadIdx.x, T};
@@ -134,7 +143,8 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
 #pragma unroll
             for (int q = 0; q < K; ++q) { sq[q * T + threadIdx.x] = Q.x[q]; sq[(K + q) * T + threadIdx.x] = Q.y[q]; }
         }
-        const FwdOut<K, true> r = iou_fwd<K, true, DGAL_FWD_P2MODE, DGAL_THIN>(P, Q, qt, WL ? &wlut[0] : nullptr);
+        const FwdOut<K, true> r = iou_fwd<K, true, DGAL_FWD_P2MODE, DGAL_THIN>(P, Q, qt, WL ? &wlut[0] : nullptr,
+                                                                             WL8 ? &wlut8[0] : nullptr);
         thinmask |= (uint32_t)r.thin << t;   // thin pair: fixed after the loop
         __stcs(iou + k, r.iou);
         nx[k] = (uint8_t)r.nx;
