@@ -14,6 +14,16 @@ namespace {
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kGridMaxCells = 1 << 16;  // <= 256 x 256 cells
 constexpr int kThreads = 256;
+#ifndef DGAL_PW_FLAT
+#define DGAL_PW_FLAT 1   // candidate sweep over the flattened ranges (pw_candidates)
+#endif
+#ifndef DGAL_PW_U
+#define DGAL_PW_U 4      // circle loads in flight per lane in the flattened sweep (A/B cfg5: 1 / 2 / 4: 6.07 / 6.00 / 5.95 ms)
+#endif
+constexpr int kU = DGAL_PW_U;
+#ifndef DGAL_PW_CELL
+#define DGAL_PW_CELL 0.5f   // grid cell size in units of the largest column radius (A/B cfg5: 2 -> 0.5: -0.05 ms)
+#endif
 
 struct GridHeader {
     float xmin, ymin, xmax, ymax;  // extent of the column circle centres
@@ -145,13 +155,14 @@ __global__ void __launch_bounds__(kThreads) pw_circles(int64_t m, const float *_
     }
 }
 
-// grid geometry from the header: cells of size >= 2 rmax (>= the largest
-// possible centre distance of an intersecting row/column pair when the row
-// radius is <= rmax; larger rows scan more cells), at most 256 x 256 cells.
+// grid geometry from the header: cells of size DGAL_PW_CELL x rmax, at most
+// 256 x 256 cells.  Any size is exact: a row scans every cell within its reach
+// (its radius + rmax) of its centre; smaller cells scan fewer circles per row
+// in more (flattened) ranges.
 __device__ __forceinline__ void grid_dims(const GridHeader &h, float &cell, int &nx, int &ny)
 {
     const float ex = fmaxf(h.xmax - h.xmin, 0.f), ey = fmaxf(h.ymax - h.ymin, 0.f);
-    cell = fmaxf(fmaxf(2.f * h.rmax, fmaxf(ex, ey) * (1.f / 255.f)), 1e-20f);
+    cell = fmaxf(fmaxf(DGAL_PW_CELL * h.rmax, fmaxf(ex, ey) * (1.f / 255.f)), 1e-20f);
     nx = min(256, (int)(ex / cell) + 1);
     ny = min(256, (int)(ey / cell) + 1);
 }
@@ -265,7 +276,7 @@ pw_candidates(int64_t n_rows, const float *__restrict__ rx, const float *__restr
               float *__restrict__ iou, float thr, uint64_t *__restrict__ mask, int64_t mask_words,
               int32_t *__restrict__ nbr_count, int32_t *__restrict__ nbr_idx, int32_t cap, Workspace w)
 {
-    constexpr int kQ = 64;
+    constexpr int kQ = DGAL_PW_FLAT ? 32 * (kU + 1) : 64;
     __shared__ int64_t qrow[kThreads / 32][kQ];
     __shared__ int32_t qcol[kThreads / 32][kQ];
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
@@ -322,6 +333,67 @@ pw_candidates(int64_t n_rows, const float *__restrict__ rx, const float *__restr
         const int cx1 = cell_coord(rc.x + reach, h.xmin, h.cell, h.nx);
         const int cy0 = cell_coord(rc.y - reach, h.ymin, h.cell, h.ny);
         const int cy1 = cell_coord(rc.y + reach, h.ymin, h.cell, h.ny);
+#if DGAL_PW_FLAT
+        // the row's neighbourhood = one contiguous range of the cell-sorted circles per
+        // grid row gy (cells cx0..cx1); up to 32 ranges at a time, lane g holding range
+        // g, swept as ONE index space (no padding per range) with kU loads in flight
+        for (int gy0 = cy0; gy0 <= cy1; gy0 += 32) {
+            const int G = min(32, cy1 - gy0 + 1);
+            int rlo = 0, rlen = 0;
+            if (lane < G) {
+                const int gy = gy0 + lane;
+                const int id0 = gy * h.nx + cx0, id1 = gy * h.nx + cx1;
+                rlo = w.start[1 + id0];
+                rlen = ((id1 + 1 < ncells) ? w.start[2 + id1] : (int)m) - rlo;
+            }
+            int incl = rlen;   // inclusive prefix of the range lengths
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int v = __shfl_up_sync(kFull, incl, d);
+                if (lane >= d) incl += v;
+            }
+            const int total = __shfl_sync(kFull, incl, 31);
+            const int delta = rlo - (incl - rlen);   // pos = k + delta of the range holding k
+            for (int k0 = 0; k0 < total; k0 += 32 * kU) {           // warp-uniform
+                float4 q[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const int k = k0 + u * 32 + lane;
+                    int dl = __shfl_sync(kFull, delta, 0);     // (all lanes: shuffles)
+                    for (int g = 1; g < G; ++g) {
+                        const int e = __shfl_sync(kFull, incl, g - 1);
+                        const int dg = __shfl_sync(kFull, delta, g);
+                        dl = (k >= e) ? dg : dl;
+                    }
+                    q[u] = make_float4(0.f, 0.f, -1.f, 0.f);
+                    if (k < total) {
+                        DGAL_ASSERT(k + dl >= 0 && k + dl < m);
+                        q[u] = w.csorted[k + dl];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const float dx = q[u].x - rc.x, dy = q[u].y - rc.y, rs = q[u].z + rc.z;
+                    const bool hit = q[u].z >= 0.f && dx * dx + dy * dy < rs * rs;
+                    const int32_t c = __float_as_int(q[u].w);
+                    const unsigned bal = __ballot_sync(kFull, hit);
+                    if (hit) {
+                        const int at = qn + __popc(bal & ((1u << lane) - 1u));
+                        DGAL_ASSERT(at < kQ && c >= 0 && c < m);
+                        qrow[wp][at] = r;
+                        qcol[wp][at] = c;
+                    }
+                    qn += __popc(bal);
+                }
+                __syncwarp();
+                while (qn >= 32) {   // one call site: the evaluator's code once in the loop
+                    evaluate(qrow[wp][qn - 32 + lane], qcol[wp][qn - 32 + lane]);
+                    qn -= 32;
+                    __syncwarp();
+                }
+            }
+        }
+#else
         for (int gy = cy0; gy <= cy1; ++gy) {
             const int id0 = gy * h.nx + cx0, id1 = gy * h.nx + cx1;
             const int lo = w.start[1 + id0];
@@ -353,6 +425,7 @@ pw_candidates(int64_t n_rows, const float *__restrict__ rx, const float *__restr
                 }
             }
         }
+#endif
     }
     __syncwarp();
     if (lane < qn) evaluate(qrow[wp][lane], qcol[wp][lane]);
