@@ -202,6 +202,27 @@ def test_indexed_and_tiled_paths_agree():
     assert bool((u[0] == 1.0).all())
 
 
+@pytest.mark.parametrize("K", [4, 8])
+def test_indexed_and_tiled_agree_k4_k8(K):
+    """Indexed (persistent warps claiming rows) and tiled paths, K = 4 and K = 8:
+    matrix, mask, suppressor counts and sets bitwise equal."""
+    sc = synth.gen_cfg5_scene(n_objects=300, per_object=50, seed=23)
+    p = sc.polys
+    n = p.n
+    # K = 8: every box vertex repeated (a zero-length edge: the same polygon, include/dgal.h)
+    x = torch.from_numpy(np.repeat(p.x.reshape(n, 4), K // 4, axis=1).copy()).to(dev())
+    y = torch.from_numpy(np.repeat(p.y.reshape(n, 4), K // 4, axis=1).copy()).to(dev())
+    b = dgal.iou_pairwise(x, y, x, y, thr=sc.thr, nbr_cap=64, indexed=False)
+    a = dgal.iou_pairwise(x, y, x, y, thr=sc.thr, nbr_cap=64, indexed=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and torch.equal(a[2], b[2])
+    ia, ib = a[3].cpu().numpy(), b[3].cpu().numpy()
+    c = a[2].cpu().numpy()
+    for r in range(n):
+        k = min(c[r], 64)
+        assert sorted(ia[r, :k].tolist()) == sorted(ib[r, :k].tolist())
+
+
 def test_keep_grid_equals_single_cta_and_oracle():
     """The grid-wide rounds (cooperative launch) and the single-CTA rounds reach the same
     unique fixed point, which is the oracle's greedy scan of the same mask."""
