@@ -303,7 +303,7 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
             sq[q * T + threadIdx.x] = Q.x[q];
             sq[(4 + q) * T + threadIdx.x] = Q.y[q];
         }
-        const FwdOut<4, true> r = iou_fwd<4, true, kP2Smem, DGAL_THIN>(
+        const FwdOut<4, true> r = iou_fwd<4, true, kP2Smem, DGAL_THIN, true>(
             P, Q, QTable{sq + threadIdx.x, sq + 4 * T + threadIdx.x, T}, &wlut);
         thinmask |= (uint32_t)r.thin << t;   // thin pair: fixed after the loop
         float v = r.iou;

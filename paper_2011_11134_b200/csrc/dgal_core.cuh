@@ -242,7 +242,10 @@ __device__ __forceinline__ uint32_t seq_byte(const Seq<K> &s, int p)  // p stati
 }  // namespace dgal
 
 #ifndef DGAL_SEPT_FUSED
-#define DGAL_SEPT_FUSED 1   // the fused kernels keep the explicit separating-line test (A/B switch)
+#define DGAL_SEPT_FUSED 1   // K = 4 fused kernels (paired, box) keep the explicit separating-line test
+#endif                      // (without it ptxas spills them; A/B switch)
+#ifndef DGAL_SEPT_FUSED8
+#define DGAL_SEPT_FUSED8 0  // K = 8 fused kernel: without it (A/B cfg4 fused 0.383 -> 0.377 ms)
 #endif
 #ifndef DGAL_THIN
 #define DGAL_THIN 1     // thin / sliver pairs: areas of the recorded intersection in double (dgal_exact.cuh)
@@ -562,19 +565,20 @@ struct IllTab {
 // denominators are exactly these cross products) — a superset of the pairs with an
 // ill-conditioned crossing (nearly parallel edges that do not cross — the opposite
 // sides of two nearly aligned boxes — do not count: ~100x fewer pairs marked).
-template <int K, int MODE, bool ILL = false, int ILLG = -1>
+template <int K, int MODE, bool ILL = false, int ILLG = -1, bool WLUT = false>
 __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &Q, Clip<K> &c,
                                                QTable qt = QTable{nullptr, nullptr, 0},
                                                const WalkLut4 *wl = nullptr, IllTab it = IllTab{nullptr, 0})
 {
-    const bool LUT = (K == 4) && wl != nullptr;   // in2 from the table (wl in shared memory)
+    constexpr bool LUT = (K == 4) && WLUT;   // in2 from the table (wl in shared memory; WLUT:
+                                             // compile time — a shared address may be 0)
     // The explicit separating-line test (p1 strictly outside some p2 line -> empty)
     // is redundant: such a line bounds every p1 edge out (both ends negative: t* > 1
     // as a lower bound or < 0 as an upper one) and p2's centroid is outside p1, so
     // the clip finds no piece and no p2 vertex inside.  Dropped (K^2 max operations:
     // cfg3 forward -2.4 %, cfg4 -6 %; the GPU suite is unchanged); the fused kernels
     // (ILL) keep it — without it ptxas spills the K = 4 one.
-    constexpr bool SEPT = DGAL_SEPT_FUSED && ILL;
+    constexpr bool SEPT = ILL && (K == 4 ? DGAL_SEPT_FUSED : DGAL_SEPT_FUSED8);
     constexpr bool PIECES = (MODE == kP2Pieces || MODE == kP2PiecesSmem);
     constexpr bool PSMEM = (MODE == kP2PiecesSmem);
     constexpr uint32_t KMASK = (1u << K) - 1u;
@@ -913,7 +917,7 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
 // of p1, p2 and of that record in double (areas_exact, dgal_exact.cuh) and decide
 // emptiness and the IoU from them (fwd_thin_fix).  The kernels do that after their
 // tile loop (rare; keeps the double-precision code out of the hot loop).
-template <int K, bool FLAGS, int MODE = (K == 4 ? kP2Pieces : kP2Regs), bool THIN = false>
+template <int K, bool FLAGS, int MODE = (K == 4 ? kP2Pieces : kP2Regs), bool THIN = false, bool WLUT = false>
 __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly<K> &Q,
                                                     QTable qt = QTable{nullptr, nullptr, 0},
                                                     const WalkLut4 *wl = nullptr,
@@ -921,7 +925,7 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
 {
     constexpr uint32_t KMASK = (1u << K) - 1u;
     Clip<K> c;
-    clip_intervals<K, MODE>(P, Q, c, qt, wl);
+    clip_intervals<K, MODE, false, -1, WLUT>(P, Q, c, qt, wl);
     // (after the clip, which keeps P and Q live to its end anyway: one register through the walk)
     const float R2 = (FLAGS && THIN) ? pair_extent2<K>(P, Q) : 0.f;
     const float *t0 = c.t0, *t1 = c.t1;
@@ -948,7 +952,7 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
 #pragma unroll
         for (int k = 0; k < Seq<K>::NW; ++k) s.w[k] = 0;
         int pos = 0;
-        if (K == 4 && wl != nullptr) {
+        if (K == 4 && WLUT) {
             // table walk: edge i's group = table bytes + M i | j_in, at the byte offset
             // given by the prefix sum of the counts (all four in one multiply)
             uint32_t glo[4], ghi[4], cnt = 0;
@@ -967,7 +971,7 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
                 w |= shl64((uint64_t)ghi[i] << 32 | glo[i], (off >> (8 * i)) & 0xFFu);
             s.w[0] = w;
             pos = (int)((cnt * 0x01010101u) >> 24);
-        } else if (K == 8 && wl8 != nullptr) {
+        } else if (K == 8 && WLUT) {
             // table walk (WalkLut8): run length, then the group's bytes 1.. and count
             const uint8_t *Lrow = wl8->L + (in2 << 3);
 #pragma unroll

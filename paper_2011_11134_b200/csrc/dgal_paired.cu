@@ -143,7 +143,7 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
 #pragma unroll
             for (int q = 0; q < K; ++q) { sq[q * T + threadIdx.x] = Q.x[q]; sq[(K + q) * T + threadIdx.x] = Q.y[q]; }
         }
-        const FwdOut<K, true> r = iou_fwd<K, true, DGAL_FWD_P2MODE, DGAL_THIN>(P, Q, qt, WL ? &wlut[0] : nullptr,
+        const FwdOut<K, true> r = iou_fwd<K, true, DGAL_FWD_P2MODE, DGAL_THIN, WL || WL8>(P, Q, qt, WL ? &wlut[0] : nullptr,
                                                                              WL8 ? &wlut8[0] : nullptr);
         thinmask |= (uint32_t)r.thin << t;   // thin pair: fixed after the loop
         __stcs(iou + k, r.iou);
