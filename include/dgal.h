@@ -12,10 +12,12 @@
  *    fixed size point array ... in counter-clockwise order"): structure of arrays.
  *    Vertex k of polygon n is (x[n*K + k], y[n*K + k]).  Exactly K vertices per
  *    polygon, convex, counter-clockwise.  K is 4 or 8.
- *  - ALL pointers are DEVICE pointers owned by the caller; the library never
- *    allocates, never frees and never synchronises the host ("fix-size
+ *  - ALL pointers are DEVICE pointers owned by the caller (the one exception,
+ *    dgal_iou_paired_host, takes host buffers); the library never allocates
+ *    memory, never frees and never synchronises the host ("fix-size
  *    allocated memory"); its only state is a per-device cache of launch
- *    attributes (set once per kernel and device, thread-safe, idempotent).
+ *    attributes (set once per kernel and device, thread-safe, idempotent) and
+ *    the host-buffer call's three streams and four events.
  *    Work is enqueued on `stream`
  *    (a cudaStream_t; NULL = legacy default stream).
  *  - Inputs are trusted: no CCW/convexity check on the device.
@@ -100,6 +102,41 @@ dgal_status dgal_iou_paired_bwd(int K, int64_t n,
                                 const uint8_t *nx, const uint8_t *xflags,
                                 float *gx1, float *gy1, float *gx2, float *gy2,
                                 dgal_stream stream);
+
+/*
+ * Forward + backward on HOST buffers (the end-to-end path of the north_star
+ * metric: inputs arrive from and results return to host memory).  The same
+ * computation as dgal_iou_paired_fwd then dgal_iou_paired_bwd — bitwise the same
+ * iou and gradients — pipelined in chunks of `chunk` pairs over three library
+ * streams: chunk c's host->device copies, forward, backward and device->host
+ * copies run on stream c % 3, so PCIe traffic in both directions overlaps the
+ * kernels of the other chunks.  nx / xflags stay on the device (workspace).
+ *   x1, y1, x2, y2 [n * K], grad_iou [n]: HOST memory, read;
+ *   iou [n], gx1, gy1, gx2, gy2 [n * K]: HOST memory, written.
+ *   Page-locked (cudaHostAlloc / cudaHostRegister) host buffers give full PCIe
+ *   speed; pageable ones work but the driver stages every copy.
+ *   chunk     pairs per pipeline stage, > 0 and a multiple of 4 (2^21 is the
+ *             measured optimum on B200).
+ *   workspace >= dgal_paired_host_workspace_bytes(K, chunk) bytes of DEVICE
+ *             memory (three staging slots), 256-byte aligned; no initialisation.
+ * Ordering: the work starts after everything enqueued on `stream` before the
+ * call and everything enqueued on `stream` after the call waits for it (event
+ * fork / join).  Asynchronous like every call: the host buffers must stay valid
+ * (inputs unmodified, outputs unread) until `stream` is synchronised; one call
+ * at a time per workspace.  State: the first call on a device creates the three
+ * streams and four events (kept for the process's lifetime; calls from several
+ * host threads serialise on a lock while they enqueue).
+ */
+size_t dgal_paired_host_workspace_bytes(int K, int64_t chunk);
+
+dgal_status dgal_iou_paired_host(int K, int64_t n,
+                                 const float *x1, const float *y1,
+                                 const float *x2, const float *y2,
+                                 const float *grad_iou,
+                                 float *iou,
+                                 float *gx1, float *gy1, float *gx2, float *gy2,
+                                 int64_t chunk, void *workspace, size_t workspace_bytes,
+                                 dgal_stream stream);
 
 /*
  * Fused forward + backward for an IoU loss whose upstream gradient is known

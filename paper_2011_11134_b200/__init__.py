@@ -20,7 +20,7 @@ import torch
 from ._lib import DgalError, call, lib  # noqa: F401
 
 __all__ = ["iou_paired_fwd", "iou_paired_bwd", "iou_paired_fused", "iou_paired", "iou_paired_backward", "PolyIoULoss",
-           "box_iou_paired_fwd", "box_iou_paired_bwd", "box_iou_paired_fused", "BoxIoU", "BoxIoULoss", "iou_pairwise", "pairwise_workspace", "fused_workspace", "nms_round", "nms_keep",
+           "box_iou_paired_fwd", "box_iou_paired_bwd", "box_iou_paired_fused", "BoxIoU", "BoxIoULoss", "iou_pairwise", "pairwise_workspace", "fused_workspace", "iou_paired_host", "nms_round", "nms_keep",
            "nms", "PolyIoU", "DgalError", "build_info"]
 
 
@@ -127,6 +127,55 @@ def iou_paired_bwd(x1, y1, x2, y2, grad_iou, nx, xflags, K: int | None = None, o
     call("dgal_iou_paired_bwd", K, n, _ptr(x1), _ptr(y1), _ptr(x2), _ptr(y2), _ptr(grad_iou), _ptr(nx),
          _ptr(xflags), _ptr(gx1), _ptr(gy1), _ptr(gx2), _ptr(gy2), _stream(x1.device))
     return gx1, gy1, gx2, gy2
+
+
+def _host_plane(t, name, numel):
+    """A host buffer handed to dgal_iou_paired_host: contiguous CPU float32 of
+    `numel` elements (pinned memory gives full PCIe speed)."""
+    if not isinstance(t, torch.Tensor) or t.is_cuda:
+        raise TypeError(f"{name}: expected a CPU (host) tensor")
+    if t.dtype != torch.float32 or not t.is_contiguous() or t.numel() != numel:
+        raise ValueError(f"{name}: expected a contiguous float32 tensor of {numel} elements")
+    return t
+
+
+_HOST_WS = {}
+
+
+def iou_paired_host(x1, y1, x2, y2, grad_iou, K: int | None = None, out=None, chunk: int = 1 << 21,
+                    device=None, workspace: torch.Tensor | None = None):
+    """Forward + backward on HOST tensors (dgal_iou_paired_host): the chunked
+    three-stream pipeline of host->device copies, forward, backward and
+    device->host copies runs inside the library.  Inputs and `out` = (iou, gx1,
+    gy1, gx2, gy2) are CPU tensors (pin them for full PCIe speed).  Asynchronous
+    on the current stream of `device`: synchronise before reading the outputs."""
+    K, n = _K_n(x1, K)
+    for nm, t in (("x1", x1), ("y1", y1), ("x2", x2), ("y2", y2)):
+        _host_plane(t, nm, n * K)
+    _host_plane(grad_iou, "grad_iou", n)
+    if out is None:
+        pin = x1.is_pinned()
+        out = (torch.empty(n, dtype=torch.float32, pin_memory=pin),
+               *(torch.empty(tuple(x1.shape), dtype=torch.float32, pin_memory=pin) for _ in range(4)))
+    iou, gx1, gy1, gx2, gy2 = out
+    _host_plane(iou, "iou", n)
+    for nm, t in (("gx1", gx1), ("gy1", gy1), ("gx2", gx2), ("gy2", gy2)):
+        _host_plane(t, nm, n * K)
+    dev = torch.device(device or "cuda")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    need = int(lib().dgal_paired_host_workspace_bytes(K, int(chunk)))
+    if workspace is None:
+        workspace = _HOST_WS.get((dev, K, chunk))
+        if workspace is None:
+            workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+            _HOST_WS[(dev, K, chunk)] = workspace
+    _plane(workspace, "workspace", torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        call("dgal_iou_paired_host", K, n, _ptr(x1), _ptr(y1), _ptr(x2), _ptr(y2), _ptr(grad_iou), _ptr(iou),
+             _ptr(gx1), _ptr(gy1), _ptr(gx2), _ptr(gy2), int(chunk), _ptr(workspace), workspace.numel(),
+             _stream(dev))
+    return out
 
 
 def iou_paired_fused(x1, y1, x2, y2, grad=None, scale: float = 1.0, K: int | None = None, out=None,

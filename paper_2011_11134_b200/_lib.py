@@ -25,6 +25,9 @@ SIGNATURES = {
     "dgal_iou_paired_fused": (_INT, [_INT, _I64, _P, _P, _P, _P, _P, _F, _P, _P, _P, _P, _P, _P,
                                      ctypes.c_size_t, _P]),
     "dgal_fused_workspace_bytes": (ctypes.c_size_t, [_I64]),
+    "dgal_iou_paired_host": (_INT, [_INT, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P,
+                                    ctypes.c_size_t, _P]),
+    "dgal_paired_host_workspace_bytes": (ctypes.c_size_t, [_INT, _I64]),
     "dgal_box_iou_paired_fwd": (_INT, [_INT, _INT, _I64, _P, _P, _P, _P, _P, _P]),
     "dgal_box_iou_paired_bwd": (_INT, [_INT, _INT, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "dgal_box_iou_paired_fused": (_INT, [_INT, _INT, _I64, _P, _P, _P, _F, _P, _P, _P, _P, ctypes.c_size_t, _P]),

@@ -1,8 +1,10 @@
 // dgal_api.cu — the extern "C" boundary of libdgal.so (include/dgal.h): host-side
-// argument validation, K dispatch, launch on the caller's stream.  No
-// allocation, no global state, no host synchronisation.
+// argument validation, K dispatch, launch on the caller's stream.  No memory
+// allocation, no host synchronisation; the only global state is the host-buffer
+// call's per-device streams and events.
 #include <climits>
 #include <cstdint>
+#include <mutex>
 
 #include "../../include/dgal.h"
 #include "dgal_internal.h"
@@ -18,6 +20,45 @@ inline bool aligned(const void *p, uintptr_t a) { return (reinterpret_cast<uintp
 inline dgal_status from_cuda(cudaError_t e) { return e == cudaSuccess ? DGAL_OK : DGAL_ERR_CUDA; }
 
 inline cudaStream_t as_cuda(dgal_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// dgal_iou_paired_host: one staging slot per pipeline stream, carved from the
+// caller's device workspace (256-byte aligned pieces)
+constexpr int kHostStreams = 3;
+inline size_t a256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+struct HostSlot {
+    float *x1, *y1, *x2, *y2, *g, *iou, *gx1, *gy1, *gx2, *gy2;
+    uint8_t *nx, *xf;
+};
+
+inline size_t host_slot_bytes(int K, int64_t chunk)
+{
+    const size_t c = (size_t)chunk;
+    return 8 * a256(sizeof(float) * c * K) + 2 * a256(sizeof(float) * c) + a256(c) + a256(c * 2 * K);
+}
+
+inline HostSlot host_slot(void *ws, int K, int64_t chunk, int s)
+{
+    const size_t c = (size_t)chunk;
+    char *p = static_cast<char *>(ws) + (size_t)s * host_slot_bytes(K, chunk);
+    auto take = [&](size_t b) { char *q = p; p += a256(b); return q; };
+    HostSlot h;
+    float **planes[8] = {&h.x1, &h.y1, &h.x2, &h.y2, &h.gx1, &h.gy1, &h.gx2, &h.gy2};
+    for (float **q : planes) *q = reinterpret_cast<float *>(take(sizeof(float) * c * K));
+    h.g = reinterpret_cast<float *>(take(sizeof(float) * c));
+    h.iou = reinterpret_cast<float *>(take(sizeof(float) * c));
+    h.nx = reinterpret_cast<uint8_t *>(take(c));
+    h.xf = reinterpret_cast<uint8_t *>(take(c * 2 * K));
+    return h;
+}
+
+struct HostPipe {
+    std::mutex mu;
+    bool init = false;
+    cudaStream_t s[kHostStreams] = {};
+    cudaEvent_t fork = nullptr, join[kHostStreams] = {};
+};
+HostPipe g_host_pipe[64];
 
 }  // namespace
 
@@ -53,6 +94,79 @@ dgal_status dgal_iou_paired_bwd(int K, int64_t n, const float *x1, const float *
         return DGAL_ERR_MISALIGNED;
     return from_cuda(dgal::launch_paired_bwd(K, n, x1, y1, x2, y2, grad_iou, nx, xflags, gx1, gy1, gx2,
                                              gy2, as_cuda(stream)));
+}
+
+size_t dgal_paired_host_workspace_bytes(int K, int64_t chunk)
+{
+    if ((K != 4 && K != 8) || chunk <= 0) return 0;
+    return kHostStreams * host_slot_bytes(K, chunk);
+}
+
+dgal_status dgal_iou_paired_host(int K, int64_t n, const float *x1, const float *y1, const float *x2,
+                                 const float *y2, const float *grad_iou, float *iou, float *gx1, float *gy1,
+                                 float *gx2, float *gy2, int64_t chunk, void *workspace,
+                                 size_t workspace_bytes, dgal_stream stream)
+{
+    if (K != 4 && K != 8) return DGAL_ERR_UNSUPPORTED_K;
+    if (n < 0 || chunk <= 0 || (chunk & 3)) return DGAL_ERR_INVALID_ARG;
+    if (n == 0) return DGAL_OK;
+    if (!x1 || !y1 || !x2 || !y2 || !grad_iou || !iou || !gx1 || !gy1 || !gx2 || !gy2 || !workspace)
+        return DGAL_ERR_INVALID_ARG;
+    if (workspace_bytes < dgal_paired_host_workspace_bytes(K, chunk)) return DGAL_ERR_INVALID_ARG;
+    if (!aligned(workspace, 256)) return DGAL_ERR_MISALIGNED;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return DGAL_ERR_CUDA;
+    HostPipe &hp = g_host_pipe[dev];
+    std::lock_guard<std::mutex> lock(hp.mu);
+    if (!hp.init) {
+        for (int i = 0; i < kHostStreams; ++i) {
+            if (cudaStreamCreateWithFlags(&hp.s[i], cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreateWithFlags(&hp.join[i], cudaEventDisableTiming) != cudaSuccess)
+                return DGAL_ERR_CUDA;
+        }
+        if (cudaEventCreateWithFlags(&hp.fork, cudaEventDisableTiming) != cudaSuccess) return DGAL_ERR_CUDA;
+        hp.init = true;
+    }
+    const cudaStream_t cs = as_cuda(stream);
+    cudaError_t e = cudaEventRecord(hp.fork, cs);
+    for (int i = 0; i < kHostStreams && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(hp.s[i], hp.fork, 0);
+    dgal_status st = from_cuda(e);
+    const cudaMemcpyKind H2D = cudaMemcpyHostToDevice, D2H = cudaMemcpyDeviceToHost;
+    int64_t c = 0;
+    for (int64_t off = 0; off < n && st == DGAL_OK; off += chunk, ++c) {
+        const int64_t m = (n - off < chunk) ? n - off : chunk;
+        const int si = (int)(c % kHostStreams);
+        const cudaStream_t s = hp.s[si];
+        const HostSlot h = host_slot(workspace, K, chunk, si);
+        const size_t pb = sizeof(float) * (size_t)m * K, o = (size_t)off * K;
+        // (a stage reuses its slot after the stage kHostStreams chunks earlier: same stream)
+        e = cudaMemcpyAsync(h.x1, x1 + o, pb, H2D, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h.y1, y1 + o, pb, H2D, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h.x2, x2 + o, pb, H2D, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h.y2, y2 + o, pb, H2D, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h.g, grad_iou + off, sizeof(float) * (size_t)m, H2D, s);
+        st = from_cuda(e);
+        if (st == DGAL_OK)
+            st = from_cuda(dgal::launch_paired_fwd(K, m, h.x1, h.y1, h.x2, h.y2, h.iou, h.nx, h.xf, s));
+        if (st == DGAL_OK)
+            st = from_cuda(dgal::launch_paired_bwd(K, m, h.x1, h.y1, h.x2, h.y2, h.g, h.nx, h.xf, h.gx1, h.gy1,
+                                                   h.gx2, h.gy2, s));
+        if (st == DGAL_OK) {
+            e = cudaMemcpyAsync(iou + off, h.iou, sizeof(float) * (size_t)m, D2H, s);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(gx1 + o, h.gx1, pb, D2H, s);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(gy1 + o, h.gy1, pb, D2H, s);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(gx2 + o, h.gx2, pb, D2H, s);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(gy2 + o, h.gy2, pb, D2H, s);
+            st = from_cuda(e);
+        }
+    }
+    // join (also after an error: the caller's stream never runs ahead of enqueued work)
+    for (int i = 0; i < kHostStreams; ++i) {
+        const cudaError_t e1 = cudaEventRecord(hp.join[i], hp.s[i]);
+        const cudaError_t e2 = (e1 == cudaSuccess) ? cudaStreamWaitEvent(cs, hp.join[i], 0) : e1;
+        if (st == DGAL_OK && e2 != cudaSuccess) st = DGAL_ERR_CUDA;
+    }
+    return st;
 }
 
 size_t dgal_fused_workspace_bytes(int64_t n)

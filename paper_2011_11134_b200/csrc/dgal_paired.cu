@@ -48,10 +48,10 @@ constexpr int kFwd4Threads = DGAL_FWD4_THREADS;
 #define DGAL_FWD4_NT 8        // K = 4: consecutive tiles of T pairs per CTA (amortises the table fill)
 #endif
 #ifndef DGAL_FWD8_THREADS
-#define DGAL_FWD8_THREADS 128   // K = 8: 165 registers, 3 CTAs/SM (A/B: 256 x 1 CTA 0.50 ms, 128 x 3 0.38 ms)
+#define DGAL_FWD8_THREADS 128   // K = 8 (A/B: 256 x 1 CTA 0.50 ms, 128 x 3 0.38 ms)
 #endif
 #ifndef DGAL_FWD8_MINB
-#define DGAL_FWD8_MINB 3
+#define DGAL_FWD8_MINB 4   // 128 registers, no spill since the WalkLut8 walk (A/B: 3 CTAs/SM 0.305 ms, 4: 0.301)
 #endif
 #ifndef DGAL_FWD8_NT
 #define DGAL_FWD8_NT 4         // K = 8: 4 tiles per CTA with the cp.async prefetch (A/B: 0.373 -> 0.367 ms)

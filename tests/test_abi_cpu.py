@@ -26,7 +26,8 @@ def test_header_declares_the_boundary():
     names = _declared()
     assert names == sorted(["dgal_iou_paired_fwd", "dgal_iou_paired_bwd", "dgal_iou_paired_fused",
                             "dgal_box_iou_paired_fwd", "dgal_box_iou_paired_bwd", "dgal_box_iou_paired_fused",
-                            "dgal_iou_pairwise", "dgal_fused_workspace_bytes",
+                            "dgal_iou_pairwise", "dgal_fused_workspace_bytes", "dgal_iou_paired_host",
+                            "dgal_paired_host_workspace_bytes",
                             "dgal_pairwise_workspace_bytes", "dgal_nms_round", "dgal_nms_keep",
                             "dgal_status_string", "dgal_build_info"])
 
@@ -83,6 +84,22 @@ def test_host_side_validation_without_gpu():
                                    P(a), P(a), P(a), P(a), P(a), ws - 1, None) == 1
     assert L.dgal_iou_paired_fused(4, 8, P(a), P(a), P(a), P(a), None, F1, None,
                                    P(a), P(a), P(a), P(a), P(a + 4), ws, None) == 3
+    # host-buffer call: workspace size (3 slots), bad K / chunk, NULL, short or misaligned workspace
+    hw = L.dgal_paired_host_workspace_bytes(4, 1024)
+    assert hw == 3 * (8 * 16384 + 2 * 4096 + 1024 + 8192)
+    assert L.dgal_paired_host_workspace_bytes(8, 1024) == 3 * (8 * 32768 + 2 * 4096 + 1024 + 16384)
+    assert L.dgal_paired_host_workspace_bytes(5, 1024) == 0 and L.dgal_paired_host_workspace_bytes(4, 0) == 0
+    W = 1 << 20   # any 256-aligned address: validation rejects these before any CUDA call
+    h = [P(a)] * 10
+    assert L.dgal_iou_paired_host(6, 8, *h, 1024, P(W), hw, None) == 2
+    assert L.dgal_iou_paired_host(4, 8, *h, 1022, P(W), hw, None) == 1         # chunk % 4
+    assert L.dgal_iou_paired_host(4, 8, *h, 0, P(W), hw, None) == 1
+    assert L.dgal_iou_paired_host(4, -1, *h, 1024, P(W), hw, None) == 1
+    assert L.dgal_iou_paired_host(4, 8, *([P(a)] * 9), None, 1024, P(W), hw, None) == 1
+    assert L.dgal_iou_paired_host(4, 8, *h, 1024, None, hw, None) == 1
+    assert L.dgal_iou_paired_host(4, 8, *h, 1024, P(W), hw - 1, None) == 1
+    assert L.dgal_iou_paired_host(4, 8, *h, 1024, P(W + 128), hw, None) == 3
+    assert L.dgal_iou_paired_host(4, 0, *([None] * 10), 1024, None, 0, None) == 0
     # n == 0 is a no-op
     assert L.dgal_iou_paired_fwd(4, 0, None, None, None, None, None, None, None, None) == 0
     assert L.dgal_iou_paired_bwd(4, 0, *([None] * 11), None) == 0

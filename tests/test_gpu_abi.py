@@ -88,3 +88,31 @@ def test_binding_rejects_mismatched_sizes():
         dgal.iou_pairwise(x, x, x, x, out=(z(16, 15), None, None, None))
     with pytest.raises(ValueError):
         dgal.nms_keep(z(16, 2, dt=torch.int64))
+
+
+@pytest.mark.parametrize("K", [4, 8])
+@pytest.mark.parametrize("pinned", [True, False])
+@pytest.mark.parametrize("n,chunk", [(7 * 4096 + 17, 4096), (1000, 4096), (1, 4)])
+def test_host_buffer_call_equals_device_calls(K, pinned, n, chunk):
+    """dgal_iou_paired_host (host buffers in and out, chunked three-stream
+    pipeline inside the library): iou and the four gradient planes bitwise equal
+    to dgal_iou_paired_fwd + dgal_iou_paired_bwd on device copies of the same
+    inputs — ragged last chunk, slots reused across chunks, pinned and pageable."""
+    import paper_2011_11134_b200 as dgal
+    import synth
+    b = synth.gen_config(3 if K == 4 else 4, n)
+    dev = torch.device("cuda:0")
+    host = [torch.from_numpy(a.reshape(n, K).copy()) for a in (b.p1.x, b.p1.y, b.p2.x, b.p2.y)]
+    g = torch.from_numpy(np.random.default_rng(n).uniform(-1, 1, n).astype(np.float32))
+    if pinned:
+        host = [t.pin_memory() for t in host]
+        g = g.pin_memory()
+    out = dgal.iou_paired_host(*host, g, chunk=chunk, device=dev)
+    torch.cuda.synchronize()
+    d = [t.to(dev) for t in host]
+    iou, nx, xf = dgal.iou_paired_fwd(*d)
+    gr = dgal.iou_paired_bwd(*d, g.to(dev), nx, xf)
+    torch.cuda.synchronize()
+    assert torch.equal(out[0], iou.cpu())
+    for a, c in zip(out[1:], gr):
+        assert torch.equal(a, c.cpu())
