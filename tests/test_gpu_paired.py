@@ -393,10 +393,10 @@ def test_padded_polygons(m, K):
     n = 20000
     def convex():
         c = rng.uniform(-5, 5, (n, 2)); a = rng.uniform(1, 3, n); b = a * rng.uniform(0.5, 1, n)
-        # vertex angles at least 0.6 rad apart: no sliver polygons (a sliver intersection far
-        # from p1.v0 is conditioned by the origin distance)
-        gaps = rng.uniform(0.6, 1.0, (n, m))
-        gaps = gaps / gaps.sum(1, keepdims=True) * (2 * np.pi - 0.6 * m) + 0.6
+        # vertex angles uniform on the ellipse, no minimum gap: slivers and near-zero-length
+        # edges included (thin pairs are redone in double, DESIGN.md §4.1 Conditioning)
+        gaps = rng.uniform(0.0, 1.0, (n, m))
+        gaps = gaps / gaps.sum(1, keepdims=True) * (2 * np.pi)
         ang = rng.uniform(0, 2 * np.pi, (n, 1)) + np.cumsum(gaps, 1) - gaps[:, :1]
         phi = rng.uniform(-np.pi, np.pi, n)
         ex, ey = a[:, None] * np.cos(ang), b[:, None] * np.sin(ang)
