@@ -280,6 +280,11 @@ dgal_status dgal_iou_pairwise(int K, int64_t n_rows,
  *   its own rows in place, and atomically adds the number of its rows still
  *   undecided to *undecided (device int32; the caller zeroes it).  Uses nbr lists
  *   when nbr_count[r] <= nbr_cap, else scans the lower part of mask row r.
+ *   scratch (nullable, >= 2 int32, 4-byte aligned, device): with it the round
+ *   runs to the rank-local fixed point — passes over the rows, grid-wide barriers
+ *   between them (a cooperative launch), until a pass decides nothing new, so
+ *   only suppression chains that cross row blocks need further rounds; without
+ *   it, one pass.  Either way the rounds converge to the same keep vector.
  * dgal_nms_keep: all rounds for a single-GPU problem (rows = all n boxes,
  *   row_offset = 0) in one kernel (no host round trips); writes keep[i] in {0,1}.
  *   status [n] is caller-provided scratch.  scratch (nullable, >= 2 int32, 4-byte
@@ -291,7 +296,7 @@ dgal_status dgal_iou_pairwise(int K, int64_t n_rows,
 dgal_status dgal_nms_round(int64_t n_total, int64_t n_rows, int64_t row_offset,
                            const uint64_t *mask, int64_t mask_words,
                            const int32_t *nbr_count, const int32_t *nbr_idx, int32_t nbr_cap,
-                           uint8_t *status, int32_t *undecided,
+                           uint8_t *status, int32_t *undecided, int32_t *scratch,
                            dgal_stream stream);
 
 dgal_status dgal_nms_keep(int64_t n,

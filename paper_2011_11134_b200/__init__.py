@@ -403,8 +403,9 @@ def _nbr_check(nbr_count, nbr_idx, n_rows, dev) -> int:
     return nbr_idx.shape[1]
 
 
-def nms_round(n_total: int, row_offset: int, mask, nbr_count, nbr_idx, status, undecided):
-    """One parallel NMS round over this rank's rows (dgal_nms_round)."""
+def nms_round(n_total: int, row_offset: int, mask, nbr_count, nbr_idx, status, undecided, scratch=None):
+    """One parallel NMS round over this rank's rows (dgal_nms_round); with `scratch`
+    (int32 [>= 2], device) the round runs to the rank-local fixed point."""
     _plane(mask, "mask", torch.int64)
     dev = mask.device
     n_rows = mask.shape[0]
@@ -416,8 +417,12 @@ def nms_round(n_total: int, row_offset: int, mask, nbr_count, nbr_idx, status, u
         raise ValueError(f"status: {status.numel()} entries for n_total {n_total}, rows "
                          f"[{row_offset}, {row_offset + n_rows})")
     _plane(undecided, "undecided", torch.int32, 1, dev)
+    if scratch is not None:
+        _plane(scratch, "scratch", torch.int32, device=dev)
+        if scratch.numel() < 2:
+            raise ValueError("scratch: needs >= 2 int32")
     call("dgal_nms_round", int(n_total), n_rows, int(row_offset), _ptr(mask), mask.shape[1], _ptr(nbr_count),
-         _ptr(nbr_idx), cap, _ptr(status), _ptr(undecided), _stream(mask.device))
+         _ptr(nbr_idx), cap, _ptr(status), _ptr(undecided), _ptr(scratch), _stream(mask.device))
 
 
 def nms_keep(mask, nbr_count=None, nbr_idx=None, status=None, keep=None, grid: bool = True):

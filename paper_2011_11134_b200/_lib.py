@@ -34,7 +34,7 @@ SIGNATURES = {
     "dgal_iou_pairwise": (_INT, [_INT, _I64, _P, _P, _I64, _P, _P, _I64, _P, _F, _P, _I64, _P, _P,
                                  _I32, _P, ctypes.c_size_t, _P]),
     "dgal_pairwise_workspace_bytes": (ctypes.c_size_t, [_I64]),
-    "dgal_nms_round": (_INT, [_I64, _I64, _I64, _P, _I64, _P, _P, _I32, _P, _P, _P]),
+    "dgal_nms_round": (_INT, [_I64, _I64, _I64, _P, _I64, _P, _P, _I32, _P, _P, _P, _P]),
     "dgal_nms_keep": (_INT, [_I64, _P, _I64, _P, _P, _I32, _P, _P, _P, _P]),
     "dgal_status_string": (ctypes.c_char_p, [_INT]),
     "dgal_build_info": (ctypes.c_char_p, []),

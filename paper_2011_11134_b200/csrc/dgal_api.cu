@@ -291,16 +291,18 @@ size_t dgal_pairwise_workspace_bytes(int64_t m)
 
 dgal_status dgal_nms_round(int64_t n_total, int64_t n_rows, int64_t row_offset, const uint64_t *mask,
                            int64_t mask_words, const int32_t *nbr_count, const int32_t *nbr_idx,
-                           int32_t nbr_cap, uint8_t *status, int32_t *undecided, dgal_stream stream)
+                           int32_t nbr_cap, uint8_t *status, int32_t *undecided, int32_t *scratch,
+                           dgal_stream stream)
 {
     if (n_total < 0 || n_rows < 0 || row_offset < 0 || row_offset + n_rows > n_total)
         return DGAL_ERR_INVALID_ARG;
     if (n_rows == 0) return DGAL_OK;
     if (!mask || !status || !undecided || mask_words < (n_total + 63) / 64) return DGAL_ERR_INVALID_ARG;
     if ((nbr_count == nullptr) != (nbr_idx == nullptr) || nbr_cap < 0) return DGAL_ERR_INVALID_ARG;
-    if (!aligned(mask, 8) || !aligned(undecided, 4)) return DGAL_ERR_MISALIGNED;
+    if (!aligned(mask, 8) || !aligned(undecided, 4) || (scratch && !aligned(scratch, 4)))
+        return DGAL_ERR_MISALIGNED;
     return from_cuda(dgal::launch_nms_round(n_total, n_rows, row_offset, mask, mask_words, nbr_count,
-                                            nbr_idx, nbr_cap, status, undecided, as_cuda(stream)));
+                                            nbr_idx, nbr_cap, status, undecided, scratch, as_cuda(stream)));
 }
 
 dgal_status dgal_nms_keep(int64_t n, const uint64_t *mask, int64_t mask_words, const int32_t *nbr_count,

@@ -91,7 +91,7 @@ cudaError_t launch_pairwise_indexed(int K, int64_t n_rows, const float *rx, cons
 cudaError_t launch_nms_round(int64_t n_total, int64_t n_rows, int64_t row_offset,
                              const uint64_t *mask, int64_t mask_words, const int32_t *nbr_count,
                              const int32_t *nbr_idx, int32_t cap, uint8_t *status, int32_t *undecided,
-                             cudaStream_t st);
+                             int32_t *scratch, cudaStream_t st);
 cudaError_t launch_nms_keep(int64_t n, const uint64_t *mask, int64_t mask_words,
                             const int32_t *nbr_count, const int32_t *nbr_idx, int32_t cap,
                             uint8_t *status, uint8_t *keep, int32_t *scratch, cudaStream_t st);

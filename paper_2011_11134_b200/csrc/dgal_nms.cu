@@ -97,12 +97,74 @@ nms_keep_kernel(int64_t n, const uint64_t *__restrict__ mask, int64_t mask_words
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) keep[i] = (vs[i] == 1) ? 1 : 0;
 }
 
+// A round to the rank-local fixed point (dgal_nms_round with scratch): passes over
+// the rank's rows, grid barriers between them, until a pass decides nothing new
+// (the other ranks' entries of status are constant during the round).  Within
+// one rank every suppression chain resolves in this one round; only chains that
+// cross ranks need further rounds (exchanges).  Progress of pass p goes to
+// cnt[p & 1]; the last pass (no progress) counts the undecided rows.
+__global__ void __launch_bounds__(kNmsRoundThreads)
+nms_round_grid_kernel(int64_t n_rows, int64_t row_offset, const uint64_t *__restrict__ mask, int64_t mask_words,
+                      const int32_t *__restrict__ nbr_count, const int32_t *__restrict__ nbr_idx, int32_t cap,
+                      uint8_t *status, int32_t *undecided, int32_t *cnt)
+{
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    volatile uint8_t *vs = status;
+    if (t0 == 0) { cnt[0] = 0; cnt[1] = 0; }
+    grid.sync();
+    for (int p = 0;; ++p) {
+        volatile int32_t *c = cnt + (p & 1);
+        if (t0 == 0) cnt[(p + 1) & 1] = 0;
+        int prog = 0, still = 0;
+        for (int64_t r = t0; r < n_rows; r += stride) {
+            const int64_t i = row_offset + r;
+            if (vs[i] != 0) continue;
+            const int d = decide(r, i, mask, mask_words, nbr_count, nbr_idx, cap, vs);
+            if (d) { vs[i] = (uint8_t)d; ++prog; }
+            else ++still;
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            prog += __shfl_down_sync(0xFFFFFFFFu, prog, d);
+            still += __shfl_down_sync(0xFFFFFFFFu, still, d);
+        }
+        if ((threadIdx.x & 31) == 0 && prog) atomicAdd((int32_t *)c, prog);
+        grid.sync();
+        if (*c == 0) {           // the same value for every thread (read after the barrier)
+            if ((threadIdx.x & 31) == 0 && still) atomicAdd(undecided, still);
+            break;
+        }
+        grid.sync();             // everyone has read c before it is cleared again (pass p + 2)
+    }
+}
+
 cudaError_t launch_nms_round(int64_t n_total, int64_t n_rows, int64_t row_offset,
                              const uint64_t *mask, int64_t mask_words, const int32_t *nbr_count,
                              const int32_t *nbr_idx, int32_t cap, uint8_t *status, int32_t *undecided,
-                             cudaStream_t st)
+                             int32_t *scratch, cudaStream_t st)
 {
     (void)n_total;
+    if (scratch) {
+        static DeviceCache cache;   // co-resident grid size (-1: no cooperative launch)
+        const int limit = cache.get([&](int dev) {
+            int sms = 0, per = 0, coop = 0;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, nms_round_grid_kernel, kNmsRoundThreads, 0);
+            return coop ? sms * (per > 0 ? per : 1) : -1;
+        });
+        if (limit > 0) {
+            const int64_t need = (n_rows + kNmsRoundThreads - 1) / kNmsRoundThreads;
+            unsigned grid = (unsigned)(need < limit ? need : limit);
+            void *args[] = {&n_rows, &row_offset, (void *)&mask, &mask_words, (void *)&nbr_count,
+                            (void *)&nbr_idx, &cap, &status, &undecided, &scratch};
+            return cudaLaunchCooperativeKernel((const void *)nms_round_grid_kernel, dim3(grid),
+                                               dim3(kNmsRoundThreads), args, 0, st);
+        }
+    }
     const unsigned grid = (unsigned)((n_rows + kNmsRoundThreads - 1) / kNmsRoundThreads);
     nms_round_kernel<<<grid, kNmsRoundThreads, 0, st>>>(n_rows, row_offset, mask, mask_words, nbr_count,
                                                         nbr_idx, cap, status, undecided);

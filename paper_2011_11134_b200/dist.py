@@ -74,26 +74,28 @@ def nms_rounds(n: int, lo: int, hi: int, round_fn: Callable[[torch.Tensor], None
     round_fn(status): updates status[lo:hi] (this rank's boxes) in place from
             the whole vector (dgal_nms_round on the GPU).
     After every round the ranks all-gather their slices, so all copies agree.
-    The host checks for convergence only every `check_every` rounds (one device
-    -> host read of "any box undecided" per check, not per round: rounds after
-    convergence change nothing, so over-running is harmless).  Every rank reads
-    the same gathered vector, so all take the same decision.
-    Returns the number of rounds run (a multiple of check_every, or fewer at the limit).
+    The host checks for convergence after rounds 1, 2, 4, ... (doubling) and then
+    every `check_every` rounds (one device -> host read of "any box undecided" per
+    check, not per round: rounds after convergence change nothing, so over-running
+    is harmless; with rank-local fixed-point rounds a few rounds suffice).  Every
+    rank reads the same gathered vector, so all take the same decision.
+    Returns the number of rounds run (a check point, or fewer at the limit).
     """
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     B = status.numel() // world
     assert status.numel() == world * B and lo == min(n, rank * B)
     limit = max_rounds if max_rounds is not None else n + 1
-    r = 0
+    r, nxt = 0, 1
     while r < limit:
-        for _ in range(min(check_every, limit - r)):
+        while r < min(nxt, limit):
             round_fn(status)
             if world > 1:
                 gather_status(status, B, group)
             r += 1
         if not bool((status[:n] == 0).any()):
             return r
+        nxt = r + min(r, check_every)
     raise RuntimeError("NMS rounds did not converge")  # impossible: >= 1 box decides per round
 
 
@@ -113,10 +115,11 @@ def pairwise_nms_sharded(x, y, thr: float = 0.7, nbr_cap: int = 64, want_iou: bo
                                        want_mask=True, nbr_cap=nbr_cap, indexed=True)
     status = torch.zeros(world * B, dtype=torch.uint8, device=x.device)
     undecided = torch.zeros(1, dtype=torch.int32, device=x.device)
+    scratch = torch.zeros(2, dtype=torch.int32, device=x.device)   # rank-local fixed-point rounds
 
     def round_fn(st):
         if hi > lo:
-            nms_round(n, lo, mask, cnt, idx, st, undecided)
+            nms_round(n, lo, mask, cnt, idx, st, undecided, scratch)
 
     rounds = nms_rounds(n, lo, hi, round_fn, status, group=group)
     keep = (status[:n] == 1).to(torch.uint8)

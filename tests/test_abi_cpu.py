@@ -131,7 +131,8 @@ def test_host_side_validation_without_gpu():
     assert L.dgal_iou_pairwise(*[4, 8, None, None, 0, None, None, 0], None, 0.5, None, 0, P(a), None, 0, None, 0,
                                None) == 1
     # NMS: row block outside the problem
-    assert L.dgal_nms_round(10, 8, 4, P(a), 1, None, None, 0, P(a), P(a), None) == 1
+    assert L.dgal_nms_round(10, 8, 4, P(a), 1, None, None, 0, P(a), P(a), None, None) == 1
+    assert L.dgal_nms_round(10, 8, 0, P(a), 1, None, None, 0, P(a), P(a), P(a + 2), None) == 3
     assert L.dgal_nms_keep(0, None, 0, None, None, 0, None, None, None, None) == 0
     assert L.dgal_nms_keep(100, P(a), 1, None, None, 0, P(a), P(a), None, None) == 1
     assert L.dgal_nms_keep(10, P(a), 1, None, None, 0, P(a), P(a), P(a + 2), None) == 3
@@ -160,7 +161,7 @@ def test_sass_is_sm100a_register_resident():
     names = " ".join(stats)
     for k in ("paired_fwd_direct_kernelILi4", "paired_fwd_direct_kernelILi8", "paired_bwd_kernelILi4",
               "paired_fused_kernelILi4", "paired_fused_kernelILi8",
-              "paired_bwd_kernelILi8", "pairwise_kernelILi4", "nms_keep_kernel", "nms_round_kernel", "nms_keep_grid_kernel",
+              "paired_bwd_kernelILi8", "pairwise_kernelILi4", "nms_keep_kernel", "nms_round_kernel", "nms_keep_grid_kernel", "nms_round_grid_kernel",
               "box_fwd_kernelILi2", "box_fwd_kernelILi3", "box_bwd_kernelILi2", "box_bwd_kernelILi3",
               "box_fused_kernelILi2", "box_fused_kernelILi3"):
         assert k in names, k

@@ -148,6 +148,26 @@ def test_nms_rounds_equal_keep_and_overflow_fallback():
     assert np.array_equal(keep1.cpu().numpy(), k) and np.array_equal(keep0.cpu().numpy(), k)
     assert np.array_equal((status == 1).to(torch.uint8).cpu().numpy(), k)
     assert 0 < k.sum() < n
+    # rank-local fixed-point rounds (scratch): one block = everything in ONE round; two
+    # blocks: the same keep in at most as many rounds as single-pass rounds
+    scr = torch.zeros(2, dtype=torch.int32, device=dev())
+    st1 = torch.zeros(n, dtype=torch.uint8, device=dev())
+    und.zero_()
+    dgal.nms_round(n, 0, mask, cnt, idx, st1, und, scr)
+    assert int(und.item()) == 0
+    assert np.array_equal((st1 == 1).to(torch.uint8).cpu().numpy(), k)
+    rounds = {}
+    for use in (False, True):
+        st2 = torch.zeros(n, dtype=torch.uint8, device=dev())
+        for r in range(1, 10_000):
+            und.zero_()
+            dgal.nms_round(n, 0, mask[:h], cnt[:h], idx[:h], st2, und, scr if use else None)
+            dgal.nms_round(n, h, mask[h:], cnt[h:], idx[h:], st2, und, scr if use else None)
+            if int(und.item()) == 0:
+                break
+        rounds[use] = r
+        assert np.array_equal((st2 == 1).to(torch.uint8).cpu().numpy(), k)
+    assert rounds[True] <= rounds[False]
 
 
 def test_cfg5_full_size_sampled():
