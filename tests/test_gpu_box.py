@@ -255,3 +255,29 @@ def test_box_fused_near_coincident(dims, scale):
     assert same.mean() > 0.8
     assert_grad_close(g1.cpu().numpy().T[same], ref["gb1"][same])
     assert_grad_close(g2.cpu().numpy().T[same], ref["gb2"][same])
+
+
+@pytest.mark.parametrize("dims", [2, 3])
+def test_boxes_far_from_origin(dims):
+    """Box pairs with centres at scene coordinates up to +-5 km (float32 centres,
+    rounded once there): the kernels build both boxes' corners relative to box 1's
+    centre, so IoU (every pair), flags and parameter gradients (margin pairs) match
+    the oracle on the same float parameters."""
+    n = 20000
+    b = synth.gen_box_pairs(n, dims)
+    rng = np.random.default_rng(dims + 77)
+    off = rng.uniform(-5e3, 5e3, (2, n))
+    b1, b2 = b.b1.copy(), b.b2.copy()
+    for p in range(2):   # cx, cy planes
+        b1[p] = (b1[p].astype(np.float64) + off[p]).astype(np.float32)
+        b2[p] = (b2[p].astype(np.float64) + off[p]).astype(np.float32)
+    s = synth.BoxPairBatch(np.ascontiguousarray(b1), np.ascontiguousarray(b2), b.grad)
+    iou, nx, xf, g1, g2 = gpu_box(s)
+    r1, r2 = s.rows64()
+    ref = oracle.box_iou_paired(r1, r2, s.grad.astype(np.float64))
+    assert_iou_close(iou, ref["iou"])
+    ok = box_margin_ok(r1, r2)
+    assert ok.mean() > 0.8
+    assert_flags_exact(nx[ok], xf[ok], {"nx": ref["nx"][ok], "xflags": ref["xflags"][ok]})
+    assert_grad_close(g1.T[ok], ref["gb1"][ok])
+    assert_grad_close(g2.T[ok], ref["gb2"][ok])

@@ -306,3 +306,27 @@ def test_pairwise_nms_sharded_single_rank():
     assert np.array_equal(k, keep1.cpu().numpy())
     assert np.array_equal(k, oracle.nms_scan_mask(mask.cpu().numpy().view(np.uint64)))
     assert 0 < k.sum() < p.n
+
+
+def test_pairwise_far_from_origin():
+    """A nuScenes-like scene shifted to (+4.5 km, -3.2 km) (float32 vertices rounded
+    there): the indexed and tiled matrices are bitwise equal and match the oracle on
+    the same float polygons (IoU <= 1e-5, mask bits outside the R14 band)."""
+    sc = synth.gen_cfg5_scene(n_objects=80, per_object=50, seed=41)
+    p = sc.polys
+    n = p.n
+    xs = (p.x.astype(np.float64) + 4500.0).astype(np.float32)
+    ys = (p.y.astype(np.float64) - 3200.0).astype(np.float32)
+    q = synth.Polys(xs, ys, 4)
+    x, y = to_dev(q)
+    a = dgal.iou_pairwise(x, y, x, y, thr=sc.thr, nbr_cap=64, indexed=True)
+    b = dgal.iou_pairwise(x, y, x, y, thr=sc.thr, nbr_cap=64, indexed=False)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and torch.equal(a[2], b[2])
+    rows = np.sort(np.random.default_rng(3).choice(n, 256, replace=False))
+    ref = oracle.iou_pairwise(q.take(rows), q)
+    got = a[0][torch.from_numpy(rows).to(dev())].cpu().numpy()
+    assert np.abs(got - ref).max() <= IOU_ATOL
+    bits = _bits(a[1][torch.from_numpy(rows).to(dev())].cpu().numpy(), n)
+    want = (ref > sc.thr) & (np.arange(n)[None, :] != rows[:, None])
+    assert not ((bits != want) & (np.abs(ref - sc.thr) > BAND)).any()
