@@ -545,7 +545,9 @@ enum P2Mode { kP2Pieces = 0, kP2Regs = 1, kP2Smem = 2, kP2PiecesSmem = 3 };
 //              instead of per-(edge, line) selects, then read back.
 
 // Per-thread table of p2's (recentred) vertices in shared memory: vertex j at
-// x[j * stride], y[j * stride].  Written and read by the same thread only.
+// x[j * stride], y[j * stride], j < K, and (0, 0) at row K (the vertex of an absent
+// event: its Green term vanishes without a select).  Written and read by the same
+// thread only.
 struct QTable {
     const float *x, *y;
     int stride;
@@ -691,7 +693,7 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     //     sum_{j on boundary} C2_j + sum_exits X_out x w_jout + sum_entries w_jin+1 x X_in
     // (a piece with both events on one edge adds the product of two vectors along
     // that edge, which vanishes).  One vertex select per event, no per-edge state.
-    float p2e = 0.f;
+    uint64_t sxw = 0ull, syw = 0ull;   // per-event modes: paired sums (exit, entry) of x*w.y, y*w.x
     float Aix2 = 0.f;   // twice the area of p1 ∩ p2 (Green over the closed boundary)
     uint32_t ev_out = 0, ev_in = 0;
     float *ax = c.ax, *ay = c.ay, *bx = c.bx, *by = c.by;
@@ -823,18 +825,29 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
                 by[j] = (ji == j) ? xiy : by[j];
             }
         } else {
+            // event vertices W_out = w_jout, W_in = w_jin+1, or (0, 0) without the event
+            // (kP2Smem: row K of the table is zero), so the terms need no select:
+            //   sxw += (X_out x-part, X_in x-part) * (W_out.y, W_in.y)
+            //   syw += (X_out y-part, X_in y-part) * (W_out.x, W_in.x)
+            // one paired FMA each; p2e = (X_out x W_out) - (X_in x W_in) at the end
             float wox, woy, wix, wiy;
-            const uint32_t jn = (ljin + 1u) & (K - 1u);
+            const uint32_t jo = has_out ? ljout : (uint32_t)K;
+            const uint32_t jn = has_in ? ((ljin + 1u) & (K - 1u)) : (uint32_t)K;
             if (MODE == kP2Smem) {
-                wox = qt.x[ljout * qt.stride]; woy = qt.y[ljout * qt.stride];
+                wox = qt.x[jo * qt.stride]; woy = qt.y[jo * qt.stride];
                 wix = qt.x[jn * qt.stride]; wiy = qt.y[jn * qt.stride];
             } else {
                 pick_xy<K>(Q.x, Q.y, ljout, wox, woy);
-                pick_xy<K>(Q.x, Q.y, jn, wix, wiy);
+                pick_xy<K>(Q.x, Q.y, (ljin + 1u) & (K - 1u), wix, wiy);
+                wox = has_out ? wox : 0.f; woy = has_out ? woy : 0.f;
+                wix = has_in ? wix : 0.f; wiy = has_in ? wiy : 0.f;
             }
-            // (area terms, not decisions: contracted, one rounding fewer)
-            p2e += has_out ? fmaf(xox, woy, -(xoy * wox)) : 0.f;
-            p2e += has_in ? fmaf(wix, xiy, -(wiy * xix)) : 0.f;
+            // (area terms, not decisions: contracted)
+            const uint64_t A2 = f2pack(a1, a0);
+            const uint64_t X2 = f2fma(A2, f2pack(gx[i], gx[i]), f2pack(P.x[i], P.x[i]));
+            const uint64_t Y2 = f2fma(A2, f2pack(gy[i], gy[i]), f2pack(P.y[i], P.y[i]));
+            sxw = f2fma(X2, f2pack(woy, wiy), sxw);
+            syw = f2fma(Y2, f2pack(wox, wix), syw);
         }
 #pragma unroll
         for (int j = 0; j < K; ++j) dc[j] = dn[j];
@@ -864,15 +877,37 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     const uint32_t ev = ev_out | ev_in;
     uint32_t in2;
     if (ev == 0u) {
-        float mx = 0.f, my = 0.f;
+        // centroid m of p2 against p1's edge lines, g_i x (m - v_i), two edges per paired
+        // op.  Without events and without a p1 piece the centroid is strictly inside p1
+        // or strictly outside it (a p2 of positive area that touches p1 from outside
+        // keeps its centroid away from p1's lines), so the test is >= 0: a zero-length
+        // edge of a padded p1 (g = 0: the contraction-free cross product is exactly 0)
+        // is no constraint.
+        // (The K = 4 piece modes keep the direct form cross(g_i, m - v_i) > 0: fewer
+        // instructions in their register allocation, static count 924 vs 936 fused.)
+        float sx = 0.f, sy = 0.f;
 #pragma unroll
-        for (int j = 0; j < K; ++j) { mx += Q.x[j]; my += Q.y[j]; }
-        mx *= (1.f / K);
-        my *= (1.f / K);
+        for (int j = 0; j < K; ++j) { sx += Q.x[j]; sy += Q.y[j]; }
         bool cin = true;
+        if (!PIECES || K != 4) {
+            const float mx = sx * (1.f / K), my = sy * (1.f / K);
+            const uint64_t mx2 = f2pack(mx, mx), my2 = f2pack(my, my);
 #pragma unroll
-        for (int i = 0; i < K; ++i)   // (a zero-length edge of a padded p1 is no constraint)
-            cin &= (cross_rn(gx[i], gy[i], mx - P.x[i], my - P.y[i]) > 0.f) | (fabsf(gx[i]) + fabsf(gy[i]) == 0.f);
+            for (int q = 0; q < K / 2; ++q) {
+                const uint64_t gx2 = f2pack(gx[2 * q], gx[2 * q + 1]), gy2 = f2pack(gy[2 * q], gy[2 * q + 1]);
+                const uint64_t dx2 = f2sub(mx2, f2pack(P.x[2 * q], P.x[2 * q + 1]));
+                const uint64_t dy2 = f2sub(my2, f2pack(P.y[2 * q], P.y[2 * q + 1]));
+                const uint64_t v = f2sub(f2mul_nc(gx2, dy2), f2mul_nc(gy2, dx2));
+                float v0, v1;
+                f2unpack(v, v0, v1);
+                cin &= (v0 >= 0.f) & (v1 >= 0.f);
+            }
+        } else {
+            const float mx = sx * (1.f / K), my = sy * (1.f / K);
+#pragma unroll
+            for (int i = 0; i < K; ++i)
+                cin &= (cross_rn(gx[i], gy[i], mx - P.x[i], my - P.y[i]) > 0.f) | (fabsf(gx[i]) + fabsf(gy[i]) == 0.f);
+        }
         in2 = (valid == 0u && cin) ? KMASK : 0u;
     } else if (LUT) {
         in2 = wl->in2[ev_in | (ev_out << 4)];
@@ -896,7 +931,12 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
         const float c2 = PIECES ? cross_rn(ax[k], ay[k], bx[k], by[k]) : C2[k];
         Aix2 = __fadd_rn(Aix2, ((on2 >> k) & 1u) ? c2 : 0.f);
     }
-    if (!PIECES) Aix2 = __fadd_rn(Aix2, p2e);
+    if (!PIECES) {
+        float xo, xi, yo, yi;
+        f2unpack(sxw, xo, xi);
+        f2unpack(syw, yo, yi);
+        Aix2 = __fadd_rn(Aix2, __fsub_rn(__fsub_rn(xo, yo), __fsub_rn(xi, yi)));
+    }
     Aix2 = fminf(Aix2, fminf(A1x2, A2x2));
     c.A1x2 = A1x2;
     c.A2x2 = A2x2;

@@ -77,7 +77,9 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
     constexpr bool WL = (K == 4) && DGAL_FWD4_WALKLUT;
     constexpr bool WL8 = (K == 8) && DGAL_FWD8_WALKLUT;
     constexpr int NT = (K == 4) ? DGAL_FWD4_NT : DGAL_FWD8_NT;
-    __shared__ float sq[2 * K * T];   // per-thread p2 vertex table, [k][thread] (DGAL_FWD_P2MODE == kP2Smem)
+    // per-thread p2 vertex table (DGAL_FWD_P2MODE == kP2Smem): x rows 0..K, y rows K+1..2K+1,
+    // [row][thread]; rows K and 2K+1 stay zero (the "no event" vertex of clip_intervals)
+    __shared__ float sq[2 * (K + 1) * T];
     __shared__ WalkLut4 wlut[1];      // K = 4: the walk tables (DGAL_FWD4_WALKLUT; unused otherwise)
     __shared__ WalkLut8 wlut8[1];     // K = 8: the walk tables (DGAL_FWD8_WALKLUT; unused otherwise)
     constexpr bool PF = (K == 4) ? DGAL_FWD4_PREFETCH : DGAL_FWD8_PREFETCH;
@@ -112,7 +114,9 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
         load_walk_lut8(wlut8[0], threadIdx.x, T);
         __syncthreads();
     }
-    QTable qt{sq + threadIdx.x, sq + K * T + threadIdx.x, T};
+    QTable qt{sq + threadIdx.x, sq + (K + 1) * T + threadIdx.x, T};
+    sq[K * T + threadIdx.x] = 0.f;
+    sq[(2 * K + 1) * T + threadIdx.x] = 0.f;
     uint32_t thinmask = 0;   // tiles whose pair is thin (R^2 > kThinRatio A_u)
 #pragma unroll 1
     for (int t = 0; t < NT; ++t) {
@@ -141,7 +145,7 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
         recentre<K>(P, Q);
         if (DGAL_FWD_P2MODE == kP2Smem) {
 #pragma unroll
-            for (int q = 0; q < K; ++q) { sq[q * T + threadIdx.x] = Q.x[q]; sq[(K + q) * T + threadIdx.x] = Q.y[q]; }
+            for (int q = 0; q < K; ++q) { sq[q * T + threadIdx.x] = Q.x[q]; sq[(K + 1 + q) * T + threadIdx.x] = Q.y[q]; }
         }
         const FwdOut<K, true> r = iou_fwd<K, true, DGAL_FWD_P2MODE, DGAL_THIN, WL || WL8>(P, Q, qt, WL ? &wlut[0] : nullptr,
                                                                              WL8 ? &wlut8[0] : nullptr);
@@ -709,7 +713,7 @@ struct RefineSmem {
     float x1[kRefT * K], y1[kRefT * K], x2[kRefT * K], y2[kRefT * K];   // raw tile, [pair][k]
     float scr[4 * K * kRefT];                               // interval end points, [slot][pair]
     uint16_t queue[kRefT / 32][32 * 2 * K];                 // per-warp crossing queue
-    float sq[2 * K * kRefT];                                // per-thread p2 vertex table (kP2Smem), [k][thread]
+    float sq[2 * (K + 1) * kRefT];                          // per-thread p2 vertex table (kP2Smem), [row][thread]
     FlagLut lut;
 };
 
@@ -750,8 +754,10 @@ paired_fused_refine_kernel(int64_t n, const float *__restrict__ x1, const float 
         }
         recentre<K>(P, Q);
 #pragma unroll
-        for (int q = 0; q < K; ++q) { S.sq[q * kRefT + tid] = Q.x[q]; S.sq[(K + q) * kRefT + tid] = Q.y[q]; }
-        FwdOut<K, true> r = iou_fwd<K, true, kP2Smem, true>(P, Q, QTable{S.sq + tid, S.sq + K * kRefT + tid, kRefT});
+        for (int q = 0; q < K; ++q) { S.sq[q * kRefT + tid] = Q.x[q]; S.sq[(K + 1 + q) * kRefT + tid] = Q.y[q]; }
+        S.sq[K * kRefT + tid] = 0.f;
+        S.sq[(2 * K + 1) * kRefT + tid] = 0.f;
+        FwdOut<K, true> r = iou_fwd<K, true, kP2Smem, true>(P, Q, QTable{S.sq + tid, S.sq + (K + 1) * kRefT + tid, kRefT});
         if (r.thin)
             fwd_thin_fix<K>(RawPolyVerts{S.x1 + tid * K, S.y1 + tid * K, S.x2 + tid * K, S.y2 + tid * K}, r.seq,
                             r.nx, r.iou);
