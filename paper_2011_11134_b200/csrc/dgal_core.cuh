@@ -804,8 +804,8 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
         const uint32_t ljin = (uint32_t)dec_idx(lo), ljout = (uint32_t)dec_idx(hi);
         jin |= ljin << (4 * i);
         jout |= ljout << (4 * i);
-        ev_in |= has_in ? (1u << ljin) : 0u;
-        ev_out |= has_out ? (1u << ljout) : 0u;
+        if (has_in) ev_in |= 1u << ljin;
+        if (has_out) ev_out |= 1u << ljout;
         c.key[i] = (ok ? 0x40u : 0u) | (has_in ? 0x80u : 0u) | (has_out ? 0x100u : 0u) | (ljout << 4) |
                    ((has_in ? ljin : 0u) << 16);
         const float xox = fmaf(a1, gx[i], P.x[i]), xoy = fmaf(a1, gy[i], P.y[i]);
@@ -876,7 +876,7 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     // (strictly: a p2 touching p1 from outside is not inside).
     const uint32_t ev = ev_out | ev_in;
     uint32_t in2;
-    if (ev == 0u) {
+    if ((ev | valid) == 0u) {
         // centroid m of p2 against p1's edge lines, g_i x (m - v_i), two edges per paired
         // op.  Without events and without a p1 piece the centroid is strictly inside p1
         // or strictly outside it (a p2 of positive area that touches p1 from outside
@@ -908,7 +908,9 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
             for (int i = 0; i < K; ++i)
                 cin &= (cross_rn(gx[i], gy[i], mx - P.x[i], my - P.y[i]) > 0.f) | (fabsf(gx[i]) + fabsf(gy[i]) == 0.f);
         }
-        in2 = (valid == 0u && cin) ? KMASK : 0u;
+        in2 = cin ? KMASK : 0u;
+    } else if (ev == 0u) {
+        in2 = 0u;   // p1's boundary inside p2 without a crossing: p1 within p2
     } else if (LUT) {
         in2 = wl->in2[ev_in | (ev_out << 4)];
     } else {

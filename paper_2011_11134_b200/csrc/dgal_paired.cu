@@ -13,10 +13,19 @@ __device__ __forceinline__ void recentre(Poly<K> &P, Poly<K> &Q)
     // local origin o = p1.v0 (R11): IoU is translation invariant, and float
     // coordinates near 0 keep the decision predicates accurate.
     const float ox = P.x[0], oy = P.y[0];
+    // (paired: vertices 2q, 2q+1 per sub.rn.f32x2, bitwise the scalar result)
+    const uint64_t o2x = f2pack(ox, ox), o2y = f2pack(oy, oy);
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        P.x[k] = __fsub_rn(P.x[k], ox); P.y[k] = __fsub_rn(P.y[k], oy);
-        Q.x[k] = __fsub_rn(Q.x[k], ox); Q.y[k] = __fsub_rn(Q.y[k], oy);
+    for (int q = 0; q < K / 2; ++q) {
+        f2unpack(f2sub(f2pack(Q.x[2 * q], Q.x[2 * q + 1]), o2x), Q.x[2 * q], Q.x[2 * q + 1]);
+        f2unpack(f2sub(f2pack(Q.y[2 * q], Q.y[2 * q + 1]), o2y), Q.y[2 * q], Q.y[2 * q + 1]);
+        if (q > 0) {
+            f2unpack(f2sub(f2pack(P.x[2 * q], P.x[2 * q + 1]), o2x), P.x[2 * q], P.x[2 * q + 1]);
+            f2unpack(f2sub(f2pack(P.y[2 * q], P.y[2 * q + 1]), o2y), P.y[2 * q], P.y[2 * q + 1]);
+        } else {
+            P.x[1] = __fsub_rn(P.x[1], ox);
+            P.y[1] = __fsub_rn(P.y[1], oy);
+        }
     }
     // x - x == 0 for every finite x: stated as a constant so the compiler folds
     // the products with p1.v0 (fewer instructions and registers)
@@ -77,9 +86,12 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
     constexpr bool WL = (K == 4) && DGAL_FWD4_WALKLUT;
     constexpr bool WL8 = (K == 8) && DGAL_FWD8_WALKLUT;
     constexpr int NT = (K == 4) ? DGAL_FWD4_NT : DGAL_FWD8_NT;
-    // per-thread p2 vertex table (DGAL_FWD_P2MODE == kP2Smem): x rows 0..K, y rows K+1..2K+1,
-    // [row][thread]; rows K and 2K+1 stay zero (the "no event" vertex of clip_intervals)
-    __shared__ float sq[2 * (K + 1) * T];
+    // per-thread p2 vertex table (DGAL_FWD_P2MODE == kP2Smem), [thread][slot]: x at slots
+    // 0..K, y at K+1..2K+1, slots K and 2K+1 stay zero (the "no event" vertex of
+    // clip_intervals); an odd per-thread stride kQS keeps the warp's accesses
+    // conflict-free and an event's address one LEA
+    constexpr int kQS = 2 * K + 3;
+    __shared__ float sq[kQS * T];
     __shared__ WalkLut4 wlut[1];      // K = 4: the walk tables (DGAL_FWD4_WALKLUT; unused otherwise)
     __shared__ WalkLut8 wlut8[1];     // K = 8: the walk tables (DGAL_FWD8_WALKLUT; unused otherwise)
     constexpr bool PF = (K == 4) ? DGAL_FWD4_PREFETCH : DGAL_FWD8_PREFETCH;
@@ -114,9 +126,10 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
         load_walk_lut8(wlut8[0], threadIdx.x, T);
         __syncthreads();
     }
-    QTable qt{sq + threadIdx.x, sq + (K + 1) * T + threadIdx.x, T};
-    sq[K * T + threadIdx.x] = 0.f;
-    sq[(2 * K + 1) * T + threadIdx.x] = 0.f;
+    float *const sqt = sq + threadIdx.x * kQS;
+    const QTable qt{sqt, sqt + K + 1, 1};
+    sqt[K] = 0.f;
+    sqt[2 * K + 1] = 0.f;
     uint32_t thinmask = 0;   // tiles whose pair is thin (R^2 > kThinRatio A_u)
 #pragma unroll 1
     for (int t = 0; t < NT; ++t) {
@@ -145,7 +158,7 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
         recentre<K>(P, Q);
         if (DGAL_FWD_P2MODE == kP2Smem) {
 #pragma unroll
-            for (int q = 0; q < K; ++q) { sq[q * T + threadIdx.x] = Q.x[q]; sq[(K + 1 + q) * T + threadIdx.x] = Q.y[q]; }
+            for (int q = 0; q < K; ++q) { sqt[q] = Q.x[q]; sqt[K + 1 + q] = Q.y[q]; }
         }
         const FwdOut<K, true> r = iou_fwd<K, true, DGAL_FWD_P2MODE, DGAL_THIN, WL || WL8>(P, Q, qt, WL ? &wlut[0] : nullptr,
                                                                              WL8 ? &wlut8[0] : nullptr);
