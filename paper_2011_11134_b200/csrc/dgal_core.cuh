@@ -73,13 +73,14 @@ __device__ __forceinline__ float rcp_approx(float x)
     return r;
 }
 
-// IoU = a / u (u > 0) by div.full (<= 2 ulp, no slow-path branch of the IEEE
-// division: a smaller loop body), clamped to 1; a == u (identical polygons) gives 1
-// exactly.  The one IoU division of every kernel (paired, fused, pairwise agree).
+// IoU = a / u (0 < a <= u) as a * rcp.approx(u) (<= 1 ulp reciprocal: the quotient
+// within ~2 ulp, as div.full, without its range-scaling checks: u is a normal float
+// here — twice an area of polygons whose Green sums do not overflow), clamped to 1;
+// a == u (identical polygons) gives 1 exactly.  The one IoU division of every kernel
+// (paired, fused, pairwise agree bitwise).
 __device__ __forceinline__ float iou_div(float a, float u)
 {
-    float q;
-    asm("div.full.f32 %0, %1, %2;" : "=f"(q) : "f"(a), "f"(u));
+    const float q = a * rcp_approx(u);
     return (a == u) ? 1.f : fminf(q, 1.f);
 }
 
@@ -1182,11 +1183,7 @@ __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, f
             AL[i] = f2sub(L, BE[i]);
         }
         const float Vi = 0.5f * Vix2, Vu = 0.5f * Vux2;
-        #ifdef DGAL_FASTRCP
-    const float inv = rcp_refined(Vu);
-#else
-    const float inv = 1.f / Vu;
-#endif
+    const float inv = rcp_refined(Vu);   // 1 / V_u to ~1 ulp (V_u normal, > 0)
         const float q = Vi * inv;
         const float cvi = g * ((1.f + q) * inv);
         const float cvu = g * (-q * inv);
@@ -1228,11 +1225,7 @@ __device__ __forceinline__ float iou_fused(const Poly<K> &P, const Poly<K> &Q, f
     }
     // dIoU/dV_i = (V_u + V_i)/V_u^2, dIoU/dV_1,2 = -V_i/V_u^2; dV/dA = d
     const float Vi = 0.5f * Vix2, Vu = 0.5f * Vux2;
-    #ifdef DGAL_FASTRCP
-    const float inv = rcp_refined(Vu);
-#else
-    const float inv = 1.f / Vu;
-#endif
+    const float inv = rcp_refined(Vu);   // 1 / V_u to ~1 ulp (V_u normal, > 0)
     const float q = Vi * inv;
     const float cvi = g * ((1.f + q) * inv);
     const float cvu = g * (-q * inv);
@@ -1487,11 +1480,7 @@ __device__ __forceinline__ bool bwd_epilogue(const float *sPx, const float *sPy,
     const float Vi = Ai * ex.dz;
     const float Vu = 0.5f * ((A1x2 * ex.d1 + A2x2 * ex.d2) - Aix2 * ex.dz);
     if (!(Vu > 0.f) || !(Vi > 0.f)) return thin;  // R10 guard
-    #ifdef DGAL_FASTRCP
-    const float inv = rcp_refined(Vu);
-#else
-    const float inv = 1.f / Vu;
-#endif
+    const float inv = rcp_refined(Vu);   // 1 / V_u to ~1 ulp (V_u normal, > 0)
     const float q = Vi * inv;
     const float cvi = g * ((1.f + q) * inv);
     const float cvu = g * (-q * inv);
@@ -1574,11 +1563,7 @@ __device__ __forceinline__ bool bwd_epilogue(const float *sPx, const float *sPy,
     const float Vi = Ai * ex.dz;
     const float Vu = 0.5f * ((A1x2 * ex.d1 + A2x2 * ex.d2) - Aix2 * ex.dz);
     if (!(Vu > 0.f) || !(Vi > 0.f)) return thin;  // R10 guard
-    #ifdef DGAL_FASTRCP
-    const float inv = rcp_refined(Vu);
-#else
-    const float inv = 1.f / Vu;
-#endif
+    const float inv = rcp_refined(Vu);   // 1 / V_u to ~1 ulp (V_u normal, > 0)
     const float q = Vi * inv;
     const float cvi = g * ((1.f + q) * inv);
     const float cvu = g * (-q * inv);

@@ -58,6 +58,9 @@ def main(argv=None):
                 tgt = int(m.group(1), 16)
                 if tgt < off and (best is None or off - tgt > best[1] - best[0]):
                     best = (tgt, off)
+    if best is None:
+        print(f"{a.kernel}: total {len(ins)}, no backward branch")
+        return
     lo, hi = best
     body = [op for off, op, _ in ins if lo <= off <= hi]
     print(f"{a.kernel}: total {len(ins)}, loop [{lo:#x}, {hi:#x}] {len(body)} instructions")
