@@ -265,9 +265,13 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
 {
     constexpr int T = kBoxFwdT;
     constexpr bool PF = DGAL_BOX_PF;
-    // per-thread p2 vertex table (kP2Smem): x rows 0..4, y rows 5..9, [row][thread]; rows 4
-    // and 9 stay zero (the "no event" vertex of clip_intervals; the thin pass reuses rows 0..7)
-    __shared__ float sq[10 * T];
+    // per-thread p2 vertex table (kP2Smem, QTable rows), [thread][slot] with an odd stride
+    // (conflict-free): x at slots 0..5, y at 6..11, the zero slots 5 and 11 written once
+    // (the "no event" vertex of clip_intervals); the thin pass reuses the array as 8 rows
+    // [row][thread]
+    constexpr int kQS = 13;
+    __shared__ float sq[kQS * T];
+    float *const sqt = sq + threadIdx.x * kQS;
     __shared__ float sp1[DGAL_THIN ? 8 * T : 1];   // p1 corners of a thin pair (dgal_exact.cuh), [k][thread]
     __shared__ WalkLut4 wlut;     // flag-walk tables
     __shared__ __align__(16) BoxRing<DIMS, PF ? T : 1> ring;   // tile t+1 in flight while tile t computes
@@ -282,8 +286,8 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
         b = load_box<DIMS>(b2, k0, sk, sp);
     }
     load_walk_lut4(wlut, tid, T);
-    sq[4 * T + tid] = 0.f;
-    sq[9 * T + tid] = 0.f;
+    sqt[5] = 0.f;
+    sqt[11] = 0.f;
     __syncthreads();
     uint32_t thinmask = 0;   // tiles whose pair is thin (R^2 > kThinRatio A_u)
 #pragma unroll 1
@@ -304,11 +308,12 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
         box_pair_polys<DIMS>(a, b, P, Q);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            sq[q * T + threadIdx.x] = Q.x[q];
-            sq[(5 + q) * T + threadIdx.x] = Q.y[q];
+            sqt[q] = Q.x[q];
+            sqt[6 + q] = Q.y[q];
         }
-        const FwdOut<4, true> r = iou_fwd<4, true, kP2Smem, DGAL_THIN, true>(
-            P, Q, QTable{sq + threadIdx.x, sq + 5 * T + threadIdx.x, T}, &wlut);
+        sqt[4] = Q.x[0];
+        sqt[10] = Q.y[0];
+        const FwdOut<4, true> r = iou_fwd<4, true, kP2Smem, DGAL_THIN, true>(P, Q, QTable{sqt, sqt + 6, 1}, &wlut);
         thinmask |= (uint32_t)r.thin << t;   // thin pair: fixed after the loop
         float v = r.iou;
         int m = r.nx;

@@ -545,10 +545,11 @@ enum P2Mode { kP2Pieces = 0, kP2Regs = 1, kP2Smem = 2, kP2PiecesSmem = 3 };
 //              per-thread shared-memory table (QTable x/y = a, stride; b at +2K)
 //              instead of per-(edge, line) selects, then read back.
 
-// Per-thread table of p2's (recentred) vertices in shared memory: vertex j at
-// x[j * stride], y[j * stride], j < K, and (0, 0) at row K (the vertex of an absent
-// event: its Green term vanishes without a select).  Written and read by the same
-// thread only.
+// Per-thread table of p2's (recentred) vertices in shared memory (kP2Smem): vertex j
+// at x[j * stride], y[j * stride] for rows j < K, w_0 again at row K (the vertex after
+// an entry line j is row j + 1, no wrap) and (0, 0) at row K + 1 (the vertex of an
+// absent event: its Green term vanishes without a select).  Written and read by the
+// same thread only.
 struct QTable {
     const float *x, *y;
     int stride;
@@ -832,11 +833,13 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
             //   syw += (X_out y-part, X_in y-part) * (W_out.x, W_in.x)
             // one paired FMA each; p2e = (X_out x W_out) - (X_in x W_in) at the end
             float wox, woy, wix, wiy;
-            const uint32_t jo = has_out ? ljout : (uint32_t)K;
-            const uint32_t jn = has_in ? ((ljin + 1u) & (K - 1u)) : (uint32_t)K;
             if (MODE == kP2Smem) {
+                // rows: w_0 .. w_K-1, w_0 again (row K: w_jin+1 is row jin + 1, no wrap),
+                // zero (row K + 1)
+                const uint32_t jo = has_out ? ljout : (uint32_t)(K + 1);
+                const uint32_t jn = has_in ? ljin : (uint32_t)K;   // read at row jn + 1
                 wox = qt.x[jo * qt.stride]; woy = qt.y[jo * qt.stride];
-                wix = qt.x[jn * qt.stride]; wiy = qt.y[jn * qt.stride];
+                wix = qt.x[jn * qt.stride + qt.stride]; wiy = qt.y[jn * qt.stride + qt.stride];
             } else {
                 pick_xy<K>(Q.x, Q.y, ljout, wox, woy);
                 pick_xy<K>(Q.x, Q.y, (ljin + 1u) & (K - 1u), wix, wiy);

@@ -86,11 +86,11 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
     constexpr bool WL = (K == 4) && DGAL_FWD4_WALKLUT;
     constexpr bool WL8 = (K == 8) && DGAL_FWD8_WALKLUT;
     constexpr int NT = (K == 4) ? DGAL_FWD4_NT : DGAL_FWD8_NT;
-    // per-thread p2 vertex table (DGAL_FWD_P2MODE == kP2Smem), [thread][slot]: x at slots
-    // 0..K, y at K+1..2K+1, slots K and 2K+1 stay zero (the "no event" vertex of
-    // clip_intervals); an odd per-thread stride kQS keeps the warp's accesses
-    // conflict-free and an event's address one LEA
-    constexpr int kQS = 2 * K + 3;
+    // per-thread p2 vertex table (DGAL_FWD_P2MODE == kP2Smem, rows as QTable), [thread][slot]:
+    // x at slots 0..K+1, y at K+2..2K+3; the zero slots K+1 and 2K+3 are written once.  An
+    // odd per-thread stride kQS keeps the warp's accesses conflict-free and an event's
+    // address one LEA
+    constexpr int kQS = 2 * K + 5;
     __shared__ float sq[kQS * T];
     __shared__ WalkLut4 wlut[1];      // K = 4: the walk tables (DGAL_FWD4_WALKLUT; unused otherwise)
     __shared__ WalkLut8 wlut8[1];     // K = 8: the walk tables (DGAL_FWD8_WALKLUT; unused otherwise)
@@ -127,9 +127,9 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
         __syncthreads();
     }
     float *const sqt = sq + threadIdx.x * kQS;
-    const QTable qt{sqt, sqt + K + 1, 1};
-    sqt[K] = 0.f;
-    sqt[2 * K + 1] = 0.f;
+    const QTable qt{sqt, sqt + K + 2, 1};
+    sqt[K + 1] = 0.f;
+    sqt[2 * K + 3] = 0.f;
     uint32_t thinmask = 0;   // tiles whose pair is thin (R^2 > kThinRatio A_u)
 #pragma unroll 1
     for (int t = 0; t < NT; ++t) {
@@ -158,7 +158,9 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
         recentre<K>(P, Q);
         if (DGAL_FWD_P2MODE == kP2Smem) {
 #pragma unroll
-            for (int q = 0; q < K; ++q) { sqt[q] = Q.x[q]; sqt[K + 1 + q] = Q.y[q]; }
+            for (int q = 0; q < K; ++q) { sqt[q] = Q.x[q]; sqt[K + 2 + q] = Q.y[q]; }
+            sqt[K] = Q.x[0];
+            sqt[2 * K + 2] = Q.y[0];
         }
         const FwdOut<K, true> r = iou_fwd<K, true, DGAL_FWD_P2MODE, DGAL_THIN, WL || WL8>(P, Q, qt, WL ? &wlut[0] : nullptr,
                                                                              WL8 ? &wlut8[0] : nullptr);
@@ -726,7 +728,7 @@ struct RefineSmem {
     float x1[kRefT * K], y1[kRefT * K], x2[kRefT * K], y2[kRefT * K];   // raw tile, [pair][k]
     float scr[4 * K * kRefT];                               // interval end points, [slot][pair]
     uint16_t queue[kRefT / 32][32 * 2 * K];                 // per-warp crossing queue
-    float sq[2 * (K + 1) * kRefT];                          // per-thread p2 vertex table (kP2Smem), [row][thread]
+    float sq[2 * (K + 2) * kRefT];                          // per-thread p2 vertex table (kP2Smem, QTable rows), [row][thread]
     FlagLut lut;
 };
 
@@ -767,10 +769,13 @@ paired_fused_refine_kernel(int64_t n, const float *__restrict__ x1, const float 
         }
         recentre<K>(P, Q);
 #pragma unroll
-        for (int q = 0; q < K; ++q) { S.sq[q * kRefT + tid] = Q.x[q]; S.sq[(K + 1 + q) * kRefT + tid] = Q.y[q]; }
-        S.sq[K * kRefT + tid] = 0.f;
-        S.sq[(2 * K + 1) * kRefT + tid] = 0.f;
-        FwdOut<K, true> r = iou_fwd<K, true, kP2Smem, true>(P, Q, QTable{S.sq + tid, S.sq + (K + 1) * kRefT + tid, kRefT});
+        for (int q = 0; q <= K; ++q) {
+            S.sq[q * kRefT + tid] = Q.x[q % K];
+            S.sq[(K + 2 + q) * kRefT + tid] = Q.y[q % K];
+        }
+        S.sq[(K + 1) * kRefT + tid] = 0.f;
+        S.sq[(2 * K + 3) * kRefT + tid] = 0.f;
+        FwdOut<K, true> r = iou_fwd<K, true, kP2Smem, true>(P, Q, QTable{S.sq + tid, S.sq + (K + 2) * kRefT + tid, kRefT});
         if (r.thin)
             fwd_thin_fix<K>(RawPolyVerts{S.x1 + tid * K, S.y1 + tid * K, S.x2 + tid * K, S.y2 + tid * K}, r.seq,
                             r.nx, r.iou);
