@@ -313,10 +313,11 @@ def time_paired(ctx, K, planes, g, steps, warmup, sampler=None, extra=False):
     The timed steps alternate between two copies of the input planes (step s reads
     set s % 2), so no step finds the previous step's inputs in L2 (the backward walks
     its tiles in descending order to reuse the forward's L2 lines WITHIN a step; across
-    steps a training loop would not get that reuse).  Per-kernel averages come from a
-    separate pass with events around each launch.  extra=True also measures the same
-    steps on ONE buffer set, with the 126 MB L2 flushed (a 256 MB memset outside each
-    step's events) before every step, and a sustained run of max(200, steps) steps.
+    steps a training loop would not get that reuse).  Per-kernel averages come from
+    the events around each launch inside the timed region.  extra=True also measures
+    the same steps on ONE buffer set, with the 126 MB L2 flushed (a 256 MB memset
+    outside each step's events) before every step, and a sustained run of
+    max(200, steps) steps.
     Returns (ms_total, fwd_ms, bwd_ms, t0, t1, (iou, grads), extras)."""
     import paper_2011_11134_b200 as dgal
     torch = ctx.torch
@@ -336,25 +337,15 @@ def time_paired(ctx, K, planes, g, steps, warmup, sampler=None, extra=False):
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream(ctx.dev)
     E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    start, end = E(), E()
-    # (1) the timed steps: fwd + bwd back to back, events only around the region
-    #     (an event between two kernels drains the first before the second starts)
+    # the timed steps: fwd + bwd back to back on the launching stream, an event before,
+    # between and after the two launches of every step (events cost no GPU time; the
+    # per-kernel split comes from the same timed region as the total, so fwd + bwd
+    # sums to the step — a separate pass later in the run measured a hotter GPU)
+    ev = [tuple(E() for _ in range(3)) for _ in range(steps)]
     ctx.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    start.record(stream)
     for s in range(steps):
-        step(sets[s % 2])
-    end.record(stream)
-    torch.cuda.synchronize()
-    t1 = time.perf_counter()
-    ctx.barrier()
-    ms = start.elapsed_time(end)
-    # (2) per-kernel split for the roofline: the same steps with an event around
-    #     each launch (a separate pass, not part of the timed value)
-    ns = min(steps, 50)
-    ev = [tuple(E() for _ in range(3)) for _ in range(ns)]
-    for s in range(ns):
         e0, e1, e2 = ev[s]
         pl = sets[s % 2]
         e0.record(stream)
@@ -363,8 +354,11 @@ def time_paired(ctx, K, planes, g, steps, warmup, sampler=None, extra=False):
         dgal.iou_paired_bwd(*pl, g, nx, xf, out=grads)
         e2.record(stream)
     torch.cuda.synchronize()
-    fwd_ms = sum(a.elapsed_time(b) for a, b, _ in ev) / ns
-    bwd_ms = sum(b.elapsed_time(c) for _, b, c in ev) / ns
+    t1 = time.perf_counter()
+    ctx.barrier()
+    ms = ev[0][0].elapsed_time(ev[-1][2])
+    fwd_ms = sum(a.elapsed_time(b) for a, b, _ in ev) / steps
+    bwd_ms = sum(b.elapsed_time(c) for _, b, c in ev) / steps
     extras = {}
     if extra:
         # same buffers every step (L2 carry-over between steps allowed)
