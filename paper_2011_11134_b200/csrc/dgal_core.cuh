@@ -1677,14 +1677,17 @@ __device__ __forceinline__ bool bwd_tile_pair(const float *tx1, const float *ty1
 #pragma unroll
     for (int p = 0; p < 2 * K; ++p) V |= lut.v[seq_byte<K>(w, p)];
 
-    int incl = cnt;                                  // warp prefix sum of the counts
+    // warp prefix sum of the counts (0 .. 2K) bit by bit: one ballot per bit, the bits
+    // independent (a shuffle scan is a chain of five dependent shuffles: ncu put 8 % of
+    // the backward's stall samples on it)
+    const unsigned below = (1u << lane) - 1u;
+    int at = 0, total = 0;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-        if (lane >= d) incl += v;
+    for (int bit = 0; (1 << bit) <= 2 * K; ++bit) {
+        const unsigned bb = __ballot_sync(0xFFFFFFFFu, (cnt >> bit) & 1);
+        at += __popc(bb & below) << bit;
+        total += __popc(bb) << bit;
     }
-    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-    int at = incl - cnt;
 #pragma unroll
     for (int p = 0; p < 2 * K; ++p) {
         const uint32_t b = seq_byte<K>(w, p);
