@@ -267,12 +267,12 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
     constexpr bool PF = DGAL_BOX_PF;
     // per-thread p2 vertex table (kP2Smem, QTable rows), [thread][slot] with an odd stride
     // (conflict-free): x at slots 0..5, y at 6..11, the zero slots 5 and 11 written once
-    // (the "no event" vertex of clip_intervals); the thin pass reuses the array as 8 rows
-    // [row][thread]
+    // (the "no event" vertex of clip_intervals); the thin pass reuses the thread's own
+    // slots for p2's corners
     constexpr int kQS = 13;
     __shared__ float sq[kQS * T];
     float *const sqt = sq + threadIdx.x * kQS;
-    __shared__ float sp1[DGAL_THIN ? 8 * T : 1];   // p1 corners of a thin pair (dgal_exact.cuh), [k][thread]
+    __shared__ float sp1[DGAL_THIN ? 8 * T : 1];   // p1 corners of a thin pair (dgal_exact.cuh), [thread][k]
     __shared__ WalkLut4 wlut;     // flag-walk tables
     __shared__ __align__(16) BoxRing<DIMS, PF ? T : 1> ring;   // tile t+1 in flight while tile t computes
     const int tid = threadIdx.x;
@@ -342,17 +342,19 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
         const Box<DIMS> a = load_box<DIMS>(b1, k, sk, sp), b = load_box<DIMS>(b2, k, sk, sp);
         Poly<4> P, Q;
         box_pair_polys<DIMS>(a, b, P, Q);
+        // (each thread only in its own words: other warps may still be in the tile loop)
+        float *const p1t = sp1 + tid * 8;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            sp1[q * T + tid] = P.x[q]; sp1[(4 + q) * T + tid] = P.y[q];
-            sq[q * T + tid] = Q.x[q]; sq[(4 + q) * T + tid] = Q.y[q];
+            p1t[q] = P.x[q]; p1t[4 + q] = P.y[q];
+            sqt[q] = Q.x[q]; sqt[6 + q] = Q.y[q];
         }
         Seq<4> s2;
         s2.w[0] = reinterpret_cast<const unsigned long long *>(xflags)[k];
         int m = nx[k];
         float v;
         AreasX2 e;
-        fwd_thin_fix<4>(StridedVerts{sp1 + tid, sp1 + 4 * T + tid, sq + tid, sq + 4 * T + tid, T}, s2, m, v, &e);
+        fwd_thin_fix<4>(StridedVerts{p1t, p1t + 4, sqt, sqt + 6, 1}, s2, m, v, &e);
         if (DIMS == 3 && m > 0) {
             const ZOver z = z_overlap<DIMS>(a, b);
             const double Vi = e.ai * z.dz, Vu = (e.a1 * a.d + e.a2 * b.d) - Vi;
