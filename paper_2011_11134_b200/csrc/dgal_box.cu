@@ -157,6 +157,35 @@ struct Trig {
     float c1, s1, c2, s2;
 };
 
+// Corner k of a box in double from its float parameters, as the oracle builds it
+// (S:347): centre (dcx, dcy) relative to the frame, cos / sin of theta by sincospi.
+__device__ __forceinline__ void box_corner_d(double dcx, double dcy, double w, double h, double s, double c, int k,
+                                             double &x, double &y)
+{
+    const double lx = ((k == 1 || k == 2) ? 0.5 : -0.5) * w, ly = ((k >= 2) ? 0.5 : -0.5) * h;
+    x = dcx + (c * lx - s * ly);
+    y = dcy + (s * lx + c * ly);
+}
+
+// The corners of a box pair in double (frame: box 1's centre; box 2's offset is exact
+// in double), the vertex source of the thin-pair areas (dgal_exact.cuh): the float
+// corners of a long thin box carry ~eps L of rounding against a width L / aspect
+// (aspect 300, L = 60 m at 300 m: up to 1.4e-5 of IoU from the corners alone), the
+// oracle's are built from the same float parameters in double.
+struct BoxCornersD {
+    double dcx, dcy, s1, c1, s2, c2;
+    float w1, h1, w2, h2;
+    template <int DIMS>
+    __device__ __forceinline__ BoxCornersD(const Box<DIMS> &a, const Box<DIMS> &b)
+        : dcx((double)b.cx - (double)a.cx), dcy((double)b.cy - (double)a.cy), w1(a.w), h1(a.h), w2(b.w), h2(b.h)
+    {
+        sincospi((double)a.th * 0.318309886183790671537767526745, &s1, &c1);
+        sincospi((double)b.th * 0.318309886183790671537767526745, &s2, &c2);
+    }
+    __device__ __forceinline__ void p(int k, double &x, double &y) const { box_corner_d(0.0, 0.0, w1, h1, s1, c1, k, x, y); }
+    __device__ __forceinline__ void q(int k, double &x, double &y) const { box_corner_d(dcx, dcy, w2, h2, s2, c2, k, x, y); }
+};
+
 template <int DIMS>
 __device__ __forceinline__ Trig box_pair_polys(const Box<DIMS> &a, const Box<DIMS> &b, Poly<4> &P, Poly<4> &Q)
 {
@@ -267,12 +296,10 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
     constexpr bool PF = DGAL_BOX_PF;
     // per-thread p2 vertex table (kP2Smem, QTable rows), [thread][slot] with an odd stride
     // (conflict-free): x at slots 0..5, y at 6..11, the zero slots 5 and 11 written once
-    // (the "no event" vertex of clip_intervals); the thin pass reuses the thread's own
-    // slots for p2's corners
+    // (the "no event" vertex of clip_intervals)
     constexpr int kQS = 13;
     __shared__ float sq[kQS * T];
     float *const sqt = sq + threadIdx.x * kQS;
-    __shared__ float sp1[DGAL_THIN ? 8 * T : 1];   // p1 corners of a thin pair (dgal_exact.cuh), [thread][k]
     __shared__ WalkLut4 wlut;     // flag-walk tables
     __shared__ __align__(16) BoxRing<DIMS, PF ? T : 1> ring;   // tile t+1 in flight while tile t computes
     const int tid = threadIdx.x;
@@ -333,7 +360,7 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
         __stcs(reinterpret_cast<unsigned long long *>(xflags) + k, (unsigned long long)seq);
     }
     // thin pairs (rare; dgal_exact.cuh): the areas of the stored record in double from
-    // the float corners (rebuilt from the parameters: bitwise the same), IoU / volumes
+    // the corners rebuilt in double from the parameters (BoxCornersD), IoU / volumes
 #pragma unroll 1
     while (thinmask) {
         const int t = __ffs(thinmask) - 1;
@@ -341,20 +368,12 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
         const int64_t k = k0 + (int64_t)t * T;
         const Box<DIMS> a = load_box<DIMS>(b1, k, sk, sp), b = load_box<DIMS>(b2, k, sk, sp);
         Poly<4> P, Q;
-        box_pair_polys<DIMS>(a, b, P, Q);
-        // (each thread only in its own words: other warps may still be in the tile loop)
-        float *const p1t = sp1 + tid * 8;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            p1t[q] = P.x[q]; p1t[4 + q] = P.y[q];
-            sqt[q] = Q.x[q]; sqt[6 + q] = Q.y[q];
-        }
         Seq<4> s2;
         s2.w[0] = reinterpret_cast<const unsigned long long *>(xflags)[k];
         int m = nx[k];
         float v;
         AreasX2 e;
-        fwd_thin_fix<4>(StridedVerts{p1t, p1t + 4, sqt, sqt + 6, 1}, s2, m, v, &e);
+        fwd_thin_fix<4>(BoxCornersD(a, b), s2, m, v, &e);
         if (DIMS == 3 && m > 0) {
             const ZOver z = z_overlap<DIMS>(a, b);
             const double Vi = e.ai * z.dz, Vu = (e.a1 * a.d + e.a2 * b.d) - Vi;
@@ -386,9 +405,7 @@ struct BoxGeometry {
     {
         double s, c;
         sincospi(th * 0.318309886183790671537767526745, &s, &c);
-        const double lx = ((k == 1 || k == 2) ? 0.5 : -0.5) * w, ly = ((k >= 2) ? 0.5 : -0.5) * h;
-        x = dcx + (c * lx - s * ly);
-        y = dcy + (s * lx + c * ly);
+        box_corner_d(dcx, dcy, w, h, s, c, k, x, y);
     }
     __device__ __forceinline__ void get(int pt, int i, int i1, int j, int j1, double &vx, double &vy, double &v1x,
                                         double &v1y, double &wx, double &wy, double &w1x, double &w1y) const
@@ -608,8 +625,7 @@ box_fused_refine_kernel(int64_t n, const float *__restrict__ b1, const float *__
             float A1x2 = r.A1x2, A2x2 = r.A2x2, Aix2 = r.Aix2;
             if (r.thin) {
                 AreasX2 e;
-                fwd_thin_fix<4>(RawPolyVerts{S.x1 + tid * 4, S.y1 + tid * 4, S.x2 + tid * 4, S.y2 + tid * 4}, r.seq,
-                                r.nx, r.iou, &e);
+                fwd_thin_fix<4>(BoxCornersD(a, b), r.seq, r.nx, r.iou, &e);
                 A1x2 = (float)e.a1; A2x2 = (float)e.a2; Aix2 = (float)e.ai;
             }
             int m = r.nx;
