@@ -131,11 +131,20 @@ struct BoxRing {
     }
 };
 
-// cos / sin of theta: exact reduction of theta / pi (no Payne-Hanek slow path, no
-// local memory); theta is accepted unbounded.
+// cos / sin of theta by sincospif(theta / pi) (exact argument reduction inside, no
+// Payne-Hanek slow path, no local memory); theta is accepted unbounded.  The
+// float product theta * (1/pi) loses |theta / pi| * 6e-8 of a half turn — 1e-6 of IoU
+// at |theta| = 16, but 1e-5 at ~100 rad and 9e-5 at 1000 (tools/probes/theta_range.py)
+// — so beyond |theta| = 16 theta / pi is formed in double and reduced modulo 2 (a full
+// turn) there first (a branch no warp of a normalised-angle batch takes).
 __device__ __forceinline__ void box_sincos(float th, float &s, float &c)
 {
-    sincospif(th * 0.318309886183790672f, &s, &c);
+    float a = th * 0.318309886183790672f;
+    if (!(fabsf(th) <= 16.f)) {
+        const double t = (double)th * 0.318309886183790671537767526745;
+        a = (float)(t - 2.0 * rint(0.5 * t));
+    }
+    sincospif(a, &s, &c);
 }
 
 // box_to_polygon relative to the origin o: (cx - ox, cy - oy) = (dcx, dcy).

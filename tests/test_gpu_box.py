@@ -365,3 +365,25 @@ def test_box_thin_crossing_gradients(dims):
     assert_iou_close(iou_f.cpu().numpy(), ref["iou"])
     assert_grad_close(f1.cpu().numpy().T[ok], ref["gb1"][ok])
     assert_grad_close(f2.cpu().numpy().T[ok], ref["gb2"][ok])
+
+
+@pytest.mark.parametrize("dims", [2, 3])
+def test_box_unbounded_theta(dims):
+    """theta is accepted unbounded: KITTI pairs with both angles shifted by a
+    common U(-1000, 1000) rad — IoU of every pair at 1e-5 against the oracle (cos / sin
+    of the float theta in double), flags bit-exact on the margin pairs.  (A float
+    theta * (1/pi) alone put 9e-5 on the IoU at |theta| ~ 1000.)"""
+    b = synth.gen_box_pairs(1 << 15, dims, seed=99)
+    rng = np.random.default_rng(5)
+    sh = rng.uniform(-1000.0, 1000.0, b.n).astype(np.float32)
+    ti = 4 if dims == 2 else 6
+    b.b1[ti] += sh
+    b.b2[ti] += sh
+    iou, nx, xf, g1, g2 = gpu_box(b)
+    r1, r2 = b.rows64()
+    ref = oracle.box_iou_paired(r1, r2, b.grad.astype(np.float64))
+    assert_iou_close(iou, ref["iou"])
+    ok = box_margin_ok(r1, r2)
+    assert_flags_exact(nx[ok], xf[ok], {"nx": ref["nx"][ok], "xflags": ref["xflags"][ok]})
+    assert_grad_close(g1.T[ok], ref["gb1"][ok])
+    assert_grad_close(g2.T[ok], ref["gb2"][ok])
