@@ -6,6 +6,7 @@ TAG=${1:-r02}
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/${TAG}_gpu_suite.log
 DGAL_CHECKED=1 python -m pytest tests -m gpu -q 2>&1 | tail -5 > gpurun_out/${TAG}_checked_build_gpu_suite.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_bench.csv \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-secondary --no-cpu-baseline > /dev/null 2>&1
