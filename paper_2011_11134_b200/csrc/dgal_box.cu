@@ -131,20 +131,25 @@ struct BoxRing {
     }
 };
 
-// cos / sin of theta by sincospif(theta / pi) (exact argument reduction inside, no
-// Payne-Hanek slow path, no local memory); theta is accepted unbounded.  The
-// float product theta * (1/pi) loses |theta / pi| * 6e-8 of a half turn — 1e-6 of IoU
-// at |theta| = 16, but 1e-5 at ~100 rad and 9e-5 at 1000 (tools/probes/theta_range.py)
-// — so beyond |theta| = 16 theta / pi is formed in double and reduced modulo 2 (a full
-// turn) there first (a branch no warp of a normalised-angle batch takes).
+// cos / sin of theta; theta is accepted unbounded.  sincospif(p) of the float
+// p = theta * (1/pi) is exact for that p (exact argument reduction inside, no
+// Payne-Hanek slow path, no local memory), but p misses theta / pi by up to
+// |theta / pi| * 6e-8 of a half turn — 1e-6 of IoU at |theta| = 16, 1e-5 at ~100 rad,
+// 9e-5 at 1000 (tools/probes/theta_range.py).  The missing part d = theta/pi - p is
+// formed exactly by FMA (the rounding error of the product, plus theta times the low
+// part of 1/pi) and applied to first order: sin(pi (p + d)) = sin(pi p) + pi d cos(pi p)
+// (the second-order term is < 1e-7 up to |theta| ~ 1e4).  Five FMA-pipe operations,
+// no branch.
 __device__ __forceinline__ void box_sincos(float th, float &s, float &c)
 {
-    float a = th * 0.318309886183790672f;
-    if (!(fabsf(th) <= 16.f)) {
-        const double t = (double)th * 0.318309886183790671537767526745;
-        a = (float)(t - 2.0 * rint(0.5 * t));
-    }
-    sincospif(a, &s, &c);
+    constexpr float kInvPiHi = 0.318309886183790672f;       // float(1/pi)
+    constexpr float kInvPiLo = 1.2841276e-08f;              // 1/pi - float(1/pi)
+    const float p = th * kInvPiHi;
+    const float pd = fmaf(th, kInvPiLo, fmaf(th, kInvPiHi, -p)) * 3.14159265358979324f;   // pi d
+    float s0, c0;
+    sincospif(p, &s0, &c0);
+    s = fmaf(pd, c0, s0);
+    c = fmaf(-pd, s0, c0);
 }
 
 // box_to_polygon relative to the origin o: (cx - ox, cy - oy) = (dcx, dcy).
