@@ -122,12 +122,14 @@ static void intersect_by_definition(int K, const vec2 *P, const vec2 *Q, isect_t
     uint8_t cflag[OR_MAXC];
     int nc = 0;
 
-    /* dedupe tolerance: 1e-9 x the coordinate scale of the pair */
-    double scale = 1.0;
+    /* dedupe tolerance: 1e-9 x the coordinate scale of the pair (its extent: the
+     * callers put the pair in its local frame, to_local) */
+    double scale = 0.0;
     for (int k = 0; k < K; ++k) {
         scale = fmax(scale, fmax(fabs(P[k].x), fabs(P[k].y)));
         scale = fmax(scale, fmax(fabs(Q[k].x), fabs(Q[k].y)));
     }
+    if (!(scale > 0.0)) scale = 1.0;
     const double tol = 1e-9 * scale;
     /* on-boundary tolerance: absorbs the double rounding of coordinates (~1e-16
      * scale), far below any float32 input resolution (~1e-7 scale) */
@@ -213,6 +215,20 @@ static void load_poly(int K, const double *x, const double *y, vec2 *p)
     for (int k = 0; k < K; ++k) p[k] = v2(x[k], y[k]);
 }
 
+/* Local frame of a pair: both polygons translated by -o (o = p1's vertex 0, returned).
+ * IoU, flags and vertex gradients are translation invariant ("rigid
+ * invariance"); computing them about a point of the pair keeps every coordinate,
+ * shoelace product and dedupe tolerance at the size of the pair instead of its
+ * distance from the origin (a 0.2 m box 10 km away: the absolute-coordinate shoelace
+ * and a 1e-9 x |coordinate| dedupe tolerance put 1e-4 on the IoU).  The differences
+ * of float-valued inputs are exact in double. */
+static vec2 to_local(int K, vec2 *P, vec2 *Q)
+{
+    vec2 o = P[0];
+    for (int k = 0; k < K; ++k) { P[k] = vsub(P[k], o); Q[k] = vsub(Q[k], o); }
+    return o;
+}
+
 /* IoU of one pair.  Returns IoU; fills nx/xflags (2K bytes). */
 static double iou_pair(int K, const vec2 *P, const vec2 *Q, isect_t *I,
                        double *A1o, double *A2o)
@@ -261,6 +277,7 @@ int oracle_iou_paired_fwd(int K, int64_t n,
         isect_t I;
         load_poly(K, x1 + k * K, y1 + k * K, P);
         load_poly(K, x2 + k * K, y2 + k * K, Q);
+        to_local(K, P, Q);
         double v = iou_pair(K, P, Q, &I, NULL, NULL);
         int cap = 2 * K, nv = I.n < cap ? I.n : cap;
         iou[k] = v;
@@ -285,9 +302,10 @@ int oracle_intersect_one(int K, const double *x1, const double *y1,
     isect_t I;
     load_poly(K, x1, y1, P);
     load_poly(K, x2, y2, Q);
+    const vec2 o = to_local(K, P, Q);
     double A1, A2;
     (void)iou_pair(K, P, Q, &I, &A1, &A2);
-    for (int c = 0; c < I.n; ++c) { vx[c] = I.v[c].x; vy[c] = I.v[c].y; flags[c] = I.flag[c]; }
+    for (int c = 0; c < I.n; ++c) { vx[c] = I.v[c].x + o.x; vy[c] = I.v[c].y + o.y; flags[c] = I.flag[c]; }
     *nv = I.n;
     if (areas) { areas[0] = A1; areas[1] = A2; areas[2] = I.area; }
     return 0;
@@ -300,6 +318,7 @@ int oracle_area(int K, int64_t n, const double *x, const double *y, double *out)
     for (int64_t k = 0; k < n; ++k) {
         vec2 P[64];
         load_poly(K, x + k * K, y + k * K, P);
+        for (int v = K - 1; v >= 0; --v) P[v] = vsub(P[v], P[0]);   /* about vertex 0 */
         out[k] = shoelace(P, K);
     }
     return 0;
@@ -423,6 +442,7 @@ int oracle_iou_paired_bwd(int K, int64_t n,
         vec2 P[OR_MAXK], Q[OR_MAXK], g1[OR_MAXK], g2[OR_MAXK];
         load_poly(K, x1 + k * K, y1 + k * K, P);
         load_poly(K, x2 + k * K, y2 + k * K, Q);
+        to_local(K, P, Q);
         iou_grad_pair(K, P, Q, grad_iou[k], g1, g2);
         for (int v = 0; v < K; ++v) {
             gx1[k * K + v] = g1[v].x; gy1[k * K + v] = g1[v].y;
@@ -446,9 +466,12 @@ int oracle_iou_pairwise(int K, int64_t nr, const double *rx, const double *ry,
     for (int64_t r = 0; r < nr; ++r) {
         vec2 P[OR_MAXK], Q[OR_MAXK];
         isect_t I;
-        load_poly(K, rx + r * K, ry + r * K, P);
+        vec2 P0[OR_MAXK];
+        load_poly(K, rx + r * K, ry + r * K, P0);
         for (int64_t c = 0; c < m; ++c) {
+            for (int v = 0; v < K; ++v) P[v] = P0[v];
             load_poly(K, cx + c * K, cy + c * K, Q);
+            to_local(K, P, Q);
             out[r * m + c] = iou_pair(K, P, Q, &I, NULL, NULL);
         }
     }
@@ -469,6 +492,7 @@ int oracle_iou_pairs_indexed(int K, int64_t npairs, const int64_t *ri, const int
         isect_t I;
         load_poly(K, rx + ri[k] * K, ry + ri[k] * K, P);
         load_poly(K, cx + ci[k] * K, cy + ci[k] * K, Q);
+        to_local(K, P, Q);
         out[k] = iou_pair(K, P, Q, &I, NULL, NULL);
     }
     return 0;
@@ -535,6 +559,7 @@ int oracle_sh_intersect(int K, int64_t n,
         vec2 P[OR_MAXK], Q[OR_MAXK];
         load_poly(K, x1 + k * K, y1 + k * K, P);
         load_poly(K, x2 + k * K, y2 + k * K, Q);
+        to_local(K, P, Q);
         vec2 cur[4 * OR_MAXK], nxt[4 * OR_MAXK];
         uint8_t cf[4 * OR_MAXK], nf[4 * OR_MAXK];
         int ce[4 * OR_MAXK], ne[4 * OR_MAXK];   /* id of edge cur[c] -> cur[c+1] */
@@ -629,6 +654,7 @@ int oracle_margin(int K, int64_t n, const double *x1, const double *y1,
         isect_t I;
         load_poly(K, x1 + k * K, y1 + k * K, P);
         load_poly(K, x2 + k * K, y2 + k * K, Q);
+        to_local(K, P, Q);
         double A1, A2;
         (void)iou_pair(K, P, Q, &I, &A1, &A2);
         double dmin = INFINITY, smin = 1.0;
@@ -718,6 +744,7 @@ static double box_pair(int dims, const double *b1, const double *b2, isect_t *I,
     vec2 P[4], Q[4];
     box_corners(b1[0], b1[1], w1, h1, th1, P);
     box_corners(b2[0], b2[1], w2, h2, th2, Q);
+    to_local(4, P, Q);
     double A1, A2;
     (void)iou_pair(4, P, Q, I, &A1, &A2);
     int top1 = 1, bot1 = 1;

@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import oracle
+import synth
 from helpers import box_margin_batch, footprint
 
 PI = math.pi
@@ -242,3 +243,23 @@ def test_monte_carlo_volume(dims):                                # S:391 cross-
         # ratio estimator sd ~ sqrt(p_i (1 - p_i / p_u) / N) / p_u
         sd = math.sqrt(max(p_i * (1 - est), 1e-12) / Nmc) / max(p_u, 1e-12)
         assert abs(est - ref[k]) <= 5 * sd + 1e-4, (k, est, ref[k], sd)
+
+
+def test_translation_invariance_far_from_origin():
+    """S:397 rigid invariance at 10 km: KITTI box pairs shrunk to 5 % (~20 x 8 cm) and
+    translated by (1e4, -1e4) exactly give the same 2D / 3D IoU within 1e-9."""
+    for dims in (2, 3):
+        b = synth.gen_box_pairs(4000, dims, seed=11)
+        r1, r2 = b.rows64()
+        sz = [2, 3] if dims == 2 else [2, 3, 4, 5]
+        for r in (r1, r2):
+            r[:, 0] *= 0.05
+            r[:, 1] *= 0.05
+            r[:, sz] *= 0.05
+        i0 = oracle.box_iou_paired(r1, r2)["iou"]
+        f1, f2 = r1.copy(), r2.copy()
+        for r in (f1, f2):
+            r[:, 0] += 1e4
+            r[:, 1] -= 1e4
+        assert (i0 > 0).mean() > 0.8
+        assert np.max(np.abs(oracle.box_iou_paired(f1, f2)["iou"] - i0)) < 1e-9

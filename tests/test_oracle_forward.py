@@ -420,3 +420,25 @@ def test_integer_grid_rectangles_closed_form():
     ai = ox * oy
     want = ai / (a * b + c * d - ai)
     assert np.max(np.abs(r["iou"] - want)) < 1e-12
+
+
+def test_translation_invariance_far_from_origin():
+    """S:397 rigid invariance, at 10 km: small polygons (~5-50 cm) translated by
+    (1e4, -1e4) exactly (double inputs) give the same IoU within 1e-9 and the same flags
+    and vertex gradients.  (An oracle computing in absolute coordinates fails this by
+    ~1e-4: the shoelace products and a dedupe tolerance proportional to |coordinate|.)"""
+    b = synth.gen_config(1, 2000)
+    sc = 0.01
+    p1 = (b.p1.x.reshape(-1, 4).astype(np.float64) * sc, b.p1.y.reshape(-1, 4).astype(np.float64) * sc)
+    p2 = (b.p2.x.reshape(-1, 4).astype(np.float64) * sc, b.p2.y.reshape(-1, 4).astype(np.float64) * sc)
+    far = lambda p: (p[0] + 1e4, p[1] - 1e4)  # noqa: E731  (exact in double)
+    r0 = oracle.iou_paired_fwd(p1, p2)
+    r1 = oracle.iou_paired_fwd(far(p1), far(p2))
+    assert (r0["iou"] > 0).mean() > 0.8
+    assert np.max(np.abs(r0["iou"] - r1["iou"])) < 1e-9
+    assert np.array_equal(r0["nx"], r1["nx"]) and np.array_equal(r0["xflags"], r1["xflags"])
+    g = np.random.default_rng(3).uniform(-1, 1, b.n)
+    g0 = oracle.iou_paired_bwd(p1, p2, g)
+    g1 = oracle.iou_paired_bwd(far(p1), far(p2), g)
+    for a, c in zip(g0, g1):
+        assert np.max(np.abs(a - c)) <= 1e-9 * max(1.0, np.max(np.abs(a)))
