@@ -387,3 +387,26 @@ def test_box_unbounded_theta(dims):
     assert_flags_exact(nx[ok], xf[ok], {"nx": ref["nx"][ok], "xflags": ref["xflags"][ok]})
     assert_grad_close(g1.T[ok], ref["gb1"][ok])
     assert_grad_close(g2.T[ok], ref["gb2"][ok])
+
+
+@pytest.mark.parametrize("dims", [2, 3])
+def test_box_small_far_from_origin(dims):
+    """KITTI pairs shrunk to 5 % (~20 x 8 cm boxes, centres within 3.5 m) and moved 10 km
+    from the origin (float parameters): IoU of every pair at 1e-5 and flags on the margin
+    pairs against the oracle (both work about the pair, not the origin)."""
+    b = synth.gen_box_pairs(1 << 15, dims, seed=7)
+    sz = (2, 3) if dims == 2 else (2, 3, 4, 5)
+    for bb in (b.b1, b.b2):
+        bb[0] = bb[0] * np.float32(0.05) + np.float32(1e4)
+        bb[1] = bb[1] * np.float32(0.05) - np.float32(1e4)
+        for r in sz:
+            bb[r] *= np.float32(0.05)
+    iou, nx, xf, g1, g2 = gpu_box(b)
+    r1, r2 = b.rows64()
+    ref = oracle.box_iou_paired(r1, r2, b.grad.astype(np.float64))
+    assert (ref["iou"] > 0).mean() > 0.8
+    assert_iou_close(iou, ref["iou"])
+    ok = box_margin_ok(r1, r2)
+    assert_flags_exact(nx[ok], xf[ok], {"nx": ref["nx"][ok], "xflags": ref["xflags"][ok]})
+    assert_grad_close(g1.T[ok], ref["gb1"][ok])
+    assert_grad_close(g2.T[ok], ref["gb2"][ok])
