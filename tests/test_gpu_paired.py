@@ -488,13 +488,14 @@ def test_fused_workspace_stays_zero_and_reusable():
         assert torch.equal(a_, b_)
 
 
-@pytest.mark.parametrize("K,offset", [(4, 1e3), (4, 5e3), (8, 5e3)])
+@pytest.mark.parametrize("K,offset", [(4, 1e3), (4, 5e3), (8, 5e3), (4, 2e4), (8, 2e4)])
 def test_far_from_origin_scene_coordinates(K, offset):
     """Pairs placed at scene coordinates up to +-offset metres (float32 inputs rounded
     once there: the ulp of the coordinates grows to ~5e-4 m): every result is that of
     the rounded float polygons, so the oracle runs on exactly the device's inputs.
     The kernels re-centre on p1's vertex 0 (exact subtraction) before any arithmetic:
-    IoU <= 1e-5 on every pair, flags and gradients on the margin pairs."""
+    IoU <= 1e-5 on every pair, flags and gradients on the margin pairs; the same for the
+    fused loss kernel."""
     cfg = 3 if K == 4 else 4
     n = 20000
     b = synth.gen_config(cfg, n)
@@ -517,4 +518,9 @@ def test_far_from_origin_scene_coordinates(K, offset):
                        {"nx": ref["nx"][ok], "xflags": ref["xflags"][ok]})
     rg = oracle.iou_paired_bwd(p1, p2, b.grad)
     for got, want in zip(gr, rg):
+        assert_grad_close(got.cpu().numpy().astype(np.float64)[ok], want[ok])
+    # the fused loss kernel (and its refine pass) on the same far-away pairs
+    iou_f, *gf = dgal.iou_paired_fused(*X, grad=g)
+    assert_iou_close(iou_f.cpu().numpy(), ref["iou"])
+    for got, want in zip(gf, rg):
         assert_grad_close(got.cpu().numpy().astype(np.float64)[ok], want[ok])
