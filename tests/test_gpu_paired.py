@@ -524,3 +524,22 @@ def test_far_from_origin_scene_coordinates(K, offset):
     assert_iou_close(iou_f.cpu().numpy(), ref["iou"])
     for got, want in zip(gf, rg):
         assert_grad_close(got.cpu().numpy().astype(np.float64)[ok], want[ok])
+
+
+@pytest.mark.parametrize("K,scale", [(4, 1e-6), (4, 1e6), (8, 1e-6), (8, 1e6)])
+def test_scale_extremes(K, scale):
+    """cfg3 / cfg4 pairs scaled by 1e-6 and 1e6 (float inputs rounded after scaling): the
+    decisions, areas and thin test are relative, so IoU of every pair (split and fused)
+    stays within 1e-5 of the oracle, flags bit-exact on the margin pairs."""
+    b = synth.gen_config(3 if K == 4 else 4, 8192)
+    a = [(v.reshape(-1, K).astype(np.float64) * scale).astype(np.float32) for v in (b.p1.x, b.p1.y, b.p2.x, b.p2.y)]
+    X = [torch.from_numpy(np.ascontiguousarray(v)).to(dev()) for v in a]
+    iou, nx, xf = dgal.iou_paired_fwd(*X)
+    iou_f = dgal.iou_paired_fused(*X, scale=1.0)[0]
+    p1 = (a[0].astype(np.float64), a[1].astype(np.float64))
+    p2 = (a[2].astype(np.float64), a[3].astype(np.float64))
+    ref = oracle.iou_paired_fwd(p1, p2)
+    assert_iou_close(iou.cpu().numpy(), ref["iou"])
+    assert_iou_close(iou_f.cpu().numpy(), ref["iou"])
+    ok = oracle.margin_ok(p1, p2)
+    assert_flags_exact(nx.cpu().numpy()[ok], xf.cpu().numpy()[ok], {"nx": ref["nx"][ok], "xflags": ref["xflags"][ok]})
