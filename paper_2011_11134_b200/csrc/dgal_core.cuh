@@ -828,7 +828,8 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
             }
         } else {
             // event vertices W_out = w_jout, W_in = w_jin+1, or (0, 0) without the event
-            // (kP2Smem: row K of the table is zero), so the terms need no select:
+            // (kP2Smem: row K + 1 of the table is zero; kP2Regs: selected), so the terms
+            // need no select:
             //   sxw += (X_out x-part, X_in x-part) * (W_out.y, W_in.y)
             //   syw += (X_out y-part, X_in y-part) * (W_out.x, W_in.x)
             // one paired FMA each; p2e = (X_out x W_out) - (X_in x W_in) at the end
