@@ -190,7 +190,9 @@ dgal_status dgal_iou_paired_fused(int K, int64_t n,
  *   dims 3: yaw-only Box3 (cx, cy, cz, w, h, d, theta)  P = 7 parameters;
  *           IoU = V_i / (V_1 + V_2 - V_i), V_i = A_i dz, dz = overlap of the
  *           z extents [cz - d/2, cz + d/2]; dz == 0 -> IoU 0, nx 0.
- * theta is in radians, unbounded; w, h, d > 0 (inputs are trusted).
+ * theta is in radians, unbounded (cos / sin to ~1e-7 rad at any |theta| up to ~1e4:
+ * float(theta/pi) plus a first-order correction by the part it misses); w, h, d > 0 (inputs
+ * are trusted).
  * layout DGAL_BOX_PLANES: parameter p of box k at b[p * n + k] (a [P, n] tensor,
  *        coalesced: the fast layout); DGAL_BOX_ROWS: at b[k * P + p] ([n, P]).
  * Gradients use the layout of the inputs and are OVERWRITTEN; they are the
