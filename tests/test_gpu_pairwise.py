@@ -330,3 +330,21 @@ def test_pairwise_far_from_origin():
     bits = _bits(a[1][torch.from_numpy(rows).to(dev())].cpu().numpy(), n)
     want = (ref > sc.thr) & (np.arange(n)[None, :] != rows[:, None])
     assert not ((bits != want) & (np.abs(ref - sc.thr) > BAND)).any()
+
+
+@pytest.mark.parametrize("s,o", [(1e-6, 0.0), (1e6, 0.0), (1.0, 2e4), (0.05, 1e4)])
+@pytest.mark.parametrize("indexed", [True, False])
+def test_pairwise_scale_and_offset_extremes(s, o, indexed):
+    """A cfg2-like scene scaled by 1e-6 / 1e6, moved 20 km, or shrunk to 5 % 10 km away
+    (float vertices rounded after the transform): the full matrix against the oracle at
+    1e-5 on both paths (circle prepass, grid cells and evaluator are all relative)."""
+    sc = synth.gen_cfg2_scene(n_objects=20, per_object=25)
+    n = sc.polys.n
+    x = (sc.polys.x.reshape(n, 4).astype(np.float64) * s + o).astype(np.float32)
+    y = (sc.polys.y.reshape(n, 4).astype(np.float64) * s - o).astype(np.float32)
+    P = synth.Polys(np.ascontiguousarray(x.reshape(-1)), np.ascontiguousarray(y.reshape(-1)), 4)
+    ref = oracle.iou_pairwise(P, P)
+    X, Y = torch.from_numpy(x).to(dev()), torch.from_numpy(y).to(dev())
+    got = dgal.iou_pairwise(X, Y, X, Y, want_mask=False, indexed=indexed)[0].cpu().numpy()
+    assert (ref > 0).sum() > 10 * n
+    assert np.abs(got - ref).max() <= 1e-5
