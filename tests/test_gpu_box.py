@@ -410,3 +410,26 @@ def test_box_small_far_from_origin(dims):
     assert_flags_exact(nx[ok], xf[ok], {"nx": ref["nx"][ok], "xflags": ref["xflags"][ok]})
     assert_grad_close(g1.T[ok], ref["gb1"][ok])
     assert_grad_close(g2.T[ok], ref["gb2"][ok])
+
+
+@pytest.mark.parametrize("cz", [1e3, 1e4])
+def test_box3d_high_centres(cz):
+    """3D KITTI pairs lifted by a common cz (global-frame heights): V_i / V_u is invariant
+    under a vertical shift, and the z overlap is taken relative to box 1's centre — IoU of
+    every pair (split and fused) at 1e-5, flags and gradients on the margin pairs."""
+    b = synth.gen_box_pairs(1 << 14, 3, seed=21)
+    b.b1[2] += np.float32(cz)
+    b.b2[2] += np.float32(cz)
+    iou, nx, xf, g1, g2 = gpu_box(b)
+    r1, r2 = b.rows64()
+    ref = oracle.box_iou_paired(r1, r2, b.grad.astype(np.float64))
+    assert_iou_close(iou, ref["iou"])
+    ok = box_margin_ok(r1, r2)
+    assert_flags_exact(nx[ok], xf[ok], {"nx": ref["nx"][ok], "xflags": ref["xflags"][ok]})
+    assert_grad_close(g1.T[ok], ref["gb1"][ok])
+    assert_grad_close(g2.T[ok], ref["gb2"][ok])
+    B1, B2 = torch.from_numpy(b.b1).to(dev()), torch.from_numpy(b.b2).to(dev())
+    iou_f, f1, f2 = dgal.box_iou_paired_fused(B1, B2, grad=torch.from_numpy(b.grad).to(dev()))
+    assert_iou_close(iou_f.cpu().numpy(), ref["iou"])
+    assert_grad_close(f1.cpu().numpy().T[ok], ref["gb1"][ok])
+    assert_grad_close(f2.cpu().numpy().T[ok], ref["gb2"][ok])
