@@ -391,7 +391,7 @@ box_fwd_kernel(int64_t n, const float *__restrict__ b1, const float *__restrict_
         int m = nx[k];
         float v;
         AreasX2 e;
-        fwd_thin_fix<4>(BoxCornersD(a, b), s2, m, v, &e);
+        fwd_thin_redo<4>(BoxCornersD(a, b), s2, m, v, &e);
         if (DIMS == 3 && m > 0) {
             const ZOver z = z_overlap<DIMS>(a, b);
             const double Vi = e.ai * z.dz, Vu = (e.a1 * a.d + e.a2 * b.d) - Vi;
@@ -643,7 +643,7 @@ box_fused_refine_kernel(int64_t n, const float *__restrict__ b1, const float *__
             float A1x2 = r.A1x2, A2x2 = r.A2x2, Aix2 = r.Aix2;
             if (r.thin) {
                 AreasX2 e;
-                fwd_thin_fix<4>(BoxCornersD(a, b), r.seq, r.nx, r.iou, &e);
+                fwd_thin_redo<4>(BoxCornersD(a, b), r.seq, r.nx, r.iou, &e);
                 A1x2 = (float)e.a1; A2x2 = (float)e.a2; Aix2 = (float)e.ai;
             }
             int m = r.nx;

@@ -955,6 +955,184 @@ __device__ __forceinline__ void clip_intervals(const Poly<K> &P, const Poly<K> &
     c.ill = ILL && (illacc >> 31) != 0u;
 }
 
+// The flag walk of R3 from the per-edge clip results (bit form; the K = 4 / K = 8
+// kernels use table forms of the same rules): walking p1's edges in order, a piece
+// emits FromP1(i) or its entry Cross(i, j_in), then its exit Cross(i, j_out) and the
+// run of p2 vertices inside p1 after p2 edge j_out.  Masks: bit i of valid / enter /
+// leave, 4 bits per edge of jin / jout; in2: p2 vertices inside p1.  Returns the
+// byte count (s must be zero on entry).
+template <int K>
+__device__ __forceinline__ int walk_bits(uint32_t valid_m, uint32_t enter_m, uint32_t leave_m, uint32_t jin_m,
+                                         uint32_t jout_m, uint32_t in2, Seq<K> &s)
+{
+    constexpr uint32_t KMASK = (1u << K) - 1u;
+    const uint32_t in2dup = in2 | (in2 << K);
+    int pos = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        const bool valid = (valid_m >> i) & 1u;
+        const bool has_in = (enter_m >> i) & 1u;
+        const bool has_out = (leave_m >> i) & 1u;
+        const uint32_t b0 = has_in ? (0xC0u | (i << 3) | ((jin_m >> (4 * i)) & 7u)) : (0x40u | i);
+        const uint32_t jo = (jout_m >> (4 * i)) & 7u;
+        const uint32_t b1 = 0xC0u | (i << 3) | jo;
+        // run of p2 vertices inside p1 after p2 edge j_out: trailing ones of in2 rotated
+        const uint32_t p0 = (jo + 1u) & (K - 1u);
+        const uint32_t rot = (in2dup >> p0) & KMASK;
+        const uint32_t L = __ffs(~rot) - 1;               // <= K
+        uint64_t run;
+        if (K == 4) {
+            const uint32_t pat = __funnelshift_r(0x83828180u, 0x83828180u, 8u * p0);
+            run = (uint64_t)(pat & (uint32_t)(shl64(1ull, 8u * L) - 1ull));
+        } else {
+            const uint64_t pat = 0x8786858483828180ull;
+            const uint64_t r8 = shr64(pat, 8u * p0) | shl64(pat, 64u - 8u * p0);
+            run = r8 & (shl64(1ull, 8u * L) - 1ull);
+        }
+        if (K == 4) {
+            uint64_t seg = b0;
+            seg |= has_out ? (((uint64_t)b1 << 8) | (run << 16)) : 0ull;
+            const int c = valid ? (has_out ? 2 + (int)L : 1) : 0;
+            s.w[0] |= valid ? shl64(seg, 8u * (uint32_t)pos) : 0ull;
+            pos += c;
+        } else {
+            // group = b0 | b1 << 8 | run << 16 (up to 9 bytes: lo word + byte 8),
+            // OR-ed in at byte pos of the 16-byte sequence, branch-free
+            const uint64_t glo = has_out ? ((uint64_t)b0 | ((uint64_t)b1 << 8) | (run << 16)) : (uint64_t)b0;
+            const uint64_t ghi = has_out ? (run >> 48) : 0ull;
+            const uint32_t sh = 8u * (uint32_t)pos;
+            const uint64_t olo = shl64(glo, sh);
+            const uint64_t ohi = (sh >= 64u) ? shl64(glo, sh - 64u) : (shr64(glo, 64u - sh) | shl64(ghi, sh));
+            s.w[0] |= valid ? olo : 0ull;
+            s.w[Seq<K>::NW - 1] |= valid ? ohi : 0ull;
+            pos += valid ? (has_out ? 2 + (int)L : 1) : 0;
+        }
+    }
+    return pos;
+}
+
+// The record (nx, xflags) of a thin pair recomputed in double (the thin-pair paths,
+// after their tile loops; rare).  A thin pair's float decisions can be wrong where the
+// shapes are a few ulps of their coordinates wide (aspect 1e4 at 354 m: a missed
+// crossing turns the event order into a run of far-away p2 vertices "inside" p1,
+// tools/probes/thin_dbg.py), and fwd_thin_fix only recomputes the areas OF the record.
+// Same rules as clip_intervals + walk_bits, scalar and in double from the vertex source
+// (dgal_exact.cuh: float inputs, their differences exact in double): closed inside
+// test d >= 0, per edge the Cyrus-Beck interval over the lines it crosses (an edge
+// outside a line at both ends has no piece), events, p2 vertices inside p1 from the
+// event order, the walk.  m = 0 when fewer than 3 or more than 2K vertices.
+template <int K, class VERTS>
+__device__ __forceinline__ void record_exact(const VERTS &V, Seq<K> &s, int &m)
+{
+    constexpr int KM = K - 1;
+    constexpr uint32_t KMASK = (1u << K) - 1u;
+    // decision value of p1 vertex i against p2 line j (p2 edge j, CCW: inside >= 0)
+    auto dec = [&](int i, int j) -> double {
+        double vx, vy, wx, wy, w1x, w1y;
+        V.p(i, vx, vy);
+        V.q(j, wx, wy);
+        V.q((j + 1) & KM, w1x, w1y);
+        return (w1x - wx) * (vy - wy) - (w1y - wy) * (vx - wx);
+    };
+    uint32_t in1 = 0;
+#pragma unroll 1
+    for (int i = 0; i < K; ++i) {
+        bool in = true;
+#pragma unroll 1
+        for (int j = 0; j < K; ++j) in = in && dec(i, j) >= 0.0;
+        in1 |= (uint32_t)in << i;
+    }
+    uint32_t valid = 0, enter = 0, leave = 0, jin = 0, jout = 0, ev_in = 0, ev_out = 0;
+#pragma unroll 1
+    for (int i = 0; i < K; ++i) {
+        const int i1 = (i + 1) & KM;
+        double lo = 0.0, hi = 1.0;
+        int jl = 0, jh = 0;
+        bool kill = false;
+#pragma unroll 1
+        for (int j = 0; j < K; ++j) {
+            const double a = dec(i, j), b = dec(i1, j);
+            if (a >= 0.0 && b >= 0.0) continue;          // no constraint
+            if (a < 0.0 && b < 0.0) { kill = true; continue; }   // edge outside line j
+            const double t = a / (a - b);                 // opposite signs: a - b != 0
+            if (b > a) {                                  // enters through line j
+                if (t > lo || (t == lo && j > jl)) { lo = t; jl = j; }
+            } else if (t < hi || (t == hi && j < jh)) {   // exits through line j
+                hi = t; jh = j;
+            }
+        }
+        const bool in_s = (in1 >> i) & 1u, in_e = (in1 >> i1) & 1u;
+        const double a0 = in_s ? 0.0 : fmin(lo, 1.0), a1 = in_e ? 1.0 : fmax(fmin(hi, 1.0), 0.0);
+        const bool ok = in_s || in_e || (!kill && a0 < a1);
+        const bool has_in = ok && !in_s, has_out = ok && !in_e;
+        valid |= (uint32_t)ok << i;
+        enter |= (uint32_t)has_in << i;
+        leave |= (uint32_t)has_out << i;
+        jin |= (has_in ? (uint32_t)jl : 0u) << (4 * i);
+        jout |= (has_out ? (uint32_t)jh : 0u) << (4 * i);
+        if (has_in) ev_in |= 1u << jl;
+        if (has_out) ev_out |= 1u << jh;
+    }
+    const uint32_t ev = ev_in | ev_out;
+    uint32_t in2;
+    if ((ev | valid) == 0u) {
+        // no piece, no event: p2 within p1 iff its vertex centroid is (strictly or on
+        // an edge line: p2 of positive area keeps its centroid off p1's lines otherwise)
+        double mx = 0.0, my = 0.0;
+#pragma unroll 1
+        for (int j = 0; j < K; ++j) {
+            double x, y;
+            V.q(j, x, y);
+            mx += x;
+            my += y;
+        }
+        mx /= K;
+        my /= K;
+        bool cin = true;
+#pragma unroll 1
+        for (int i = 0; i < K; ++i) {
+            double vx, vy, v1x, v1y;
+            V.p(i, vx, vy);
+            V.p((i + 1) & KM, v1x, v1y);
+            cin = cin && (v1x - vx) * (my - vy) - (v1y - vy) * (mx - vx) >= 0.0;
+        }
+        in2 = cin ? KMASK : 0u;
+    } else if (ev == 0u) {
+        in2 = 0u;
+    } else {   // the last event before p2 vertex j along p2 is an exit (clip_intervals)
+        uint32_t evd = ev | (ev << K);
+        uint32_t st = (ev_out & ~ev_in) | ((ev_out & ~ev_in) << K);
+#pragma unroll
+        for (int sh = 1; sh < 2 * K; sh <<= 1) {
+            st = (st & evd) | ((st << sh) & ~evd);
+            evd |= evd << sh;
+        }
+        in2 = (st >> (K - 1)) & KMASK;
+    }
+#pragma unroll
+    for (int q = 0; q < Seq<K>::NW; ++q) s.w[q] = 0ull;
+    int pos = walk_bits<K>(valid, enter, leave, jin, jout, in2, s);
+    if (pos == 0 && in2 == KMASK) {   // p2 inside p1: all FromP2, in order
+        if (K == 4) s.w[0] = 0x83828180ull;
+        else { s.w[0] = 0x8786858483828180ull; s.w[Seq<K>::NW - 1] = 0ull; }
+        pos = K;
+    }
+    m = (pos >= 3 && pos <= 2 * K) ? pos : 0;
+    if (m == 0) {
+#pragma unroll
+        for (int q = 0; q < Seq<K>::NW; ++q) s.w[q] = 0ull;
+    }
+}
+
+// A thin pair's forward outputs: its record recomputed in double (record_exact), then
+// the areas of that record in double (fwd_thin_fix).
+template <int K, class VERTS>
+__device__ __forceinline__ void fwd_thin_redo(const VERTS &V, Seq<K> &s, int &m, float &iou, AreasX2 *out = nullptr)
+{
+    record_exact<K>(V, s, m);
+    fwd_thin_fix<K>(V, s, m, iou, out);
+}
+
 // p1, p2 must already be recentred on o = p1.v0 (p1.x[0] == p1.y[0] == 0).
 // THIN (FLAGS only): detect thin pairs, R^2 > kThinRatio A_u (pair_is_thin).  A thin
 // pair's float area sum — including the sign test that decides an empty
@@ -1040,46 +1218,7 @@ __device__ __forceinline__ FwdOut<K, FLAGS> iou_fwd(const Poly<K> &P, const Poly
                 pos += (int)e.w;
             }
         } else {
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            const bool valid = (c.valid >> i) & 1u;
-            const bool has_in = (c.enter >> i) & 1u;
-            const bool has_out = (c.leave >> i) & 1u;
-            const uint32_t b0 = has_in ? (0xC0u | (i << 3) | ((c.jin >> (4 * i)) & 7u)) : (0x40u | i);
-            const uint32_t jo = (c.jout >> (4 * i)) & 7u;
-            const uint32_t b1 = 0xC0u | (i << 3) | jo;
-            // run of p2 vertices inside p1 after p2 edge j_out: trailing ones of in2 rotated
-            const uint32_t p0 = (jo + 1u) & (K - 1u);
-            const uint32_t rot = (in2dup >> p0) & KMASK;
-            const uint32_t L = __ffs(~rot) - 1;               // <= K
-            uint64_t run;
-            if (K == 4) {
-                const uint32_t pat = __funnelshift_r(0x83828180u, 0x83828180u, 8u * p0);
-                run = (uint64_t)(pat & (uint32_t)(shl64(1ull, 8u * L) - 1ull));
-            } else {
-                const uint64_t pat = 0x8786858483828180ull;
-                const uint64_t r8 = shr64(pat, 8u * p0) | shl64(pat, 64u - 8u * p0);
-                run = r8 & (shl64(1ull, 8u * L) - 1ull);
-            }
-            if (K == 4) {
-                uint64_t seg = b0;
-                seg |= has_out ? (((uint64_t)b1 << 8) | (run << 16)) : 0ull;
-                const int c = valid ? (has_out ? 2 + (int)L : 1) : 0;
-                s.w[0] |= valid ? shl64(seg, 8u * (uint32_t)pos) : 0ull;
-                pos += c;
-            } else {
-                // group = b0 | b1 << 8 | run << 16 (up to 9 bytes: lo word + byte 8),
-                // OR-ed in at byte pos of the 16-byte sequence, branch-free
-                const uint64_t glo = has_out ? ((uint64_t)b0 | ((uint64_t)b1 << 8) | (run << 16)) : (uint64_t)b0;
-                const uint64_t ghi = has_out ? (run >> 48) : 0ull;
-                const uint32_t sh = 8u * (uint32_t)pos;
-                const uint64_t olo = shl64(glo, sh);
-                const uint64_t ohi = (sh >= 64u) ? shl64(glo, sh - 64u) : (shr64(glo, 64u - sh) | shl64(ghi, sh));
-                s.w[0] |= valid ? olo : 0ull;
-                s.w[Seq<K>::NW - 1] |= valid ? ohi : 0ull;
-                pos += valid ? (has_out ? 2 + (int)L : 1) : 0;
-            }
-        }
+            pos = walk_bits<K>(c.valid, c.enter, c.leave, c.jin, c.jout, in2, s);
         }
         if (pos == 0 && in2 == KMASK) {  // p2 inside p1: all FromP2, in order
             if (K == 4) s.w[0] = 0x83828180ull;
@@ -1122,7 +1261,7 @@ __device__ __noinline__ float pair_iou_exact(const float *px, const float *py, c
     P.x[0] = 0.f;
     P.y[0] = 0.f;
     FwdOut<K, true> r = iou_fwd<K, true, kP2Regs, true>(P, Q);
-    if (r.thin || r.nx > 0) fwd_thin_fix<K>(RawPolyVerts{px, py, qx, qy}, r.seq, r.nx, r.iou);
+    if (r.thin || r.nx > 0) fwd_thin_redo<K>(RawPolyVerts{px, py, qx, qy}, r.seq, r.nx, r.iou);
     return r.iou;
 }
 

@@ -195,13 +195,11 @@ paired_fwd_direct_kernel(int64_t n, const float *__restrict__ x1, const float *_
             sq2.w[0] = v.x; sq2.w[Seq<K>::NW - 1] = v.y;
         }
         float v;
-        fwd_thin_fix<K>(RawPolyVerts{x1 + k * K, y1 + k * K, x2 + k * K, y2 + k * K}, sq2, m, v);
+        fwd_thin_redo<K>(RawPolyVerts{x1 + k * K, y1 + k * K, x2 + k * K, y2 + k * K}, sq2, m, v);
         iou[k] = v;
-        if (m == 0) {
-            nx[k] = 0;
-            if (K == 4) reinterpret_cast<unsigned long long *>(xflags)[k] = 0ull;
-            else reinterpret_cast<ulonglong2 *>(xflags)[k] = make_ulonglong2(0ull, 0ull);
-        }
+        nx[k] = (uint8_t)m;
+        if (K == 4) reinterpret_cast<unsigned long long *>(xflags)[k] = sq2.w[0];
+        else reinterpret_cast<ulonglong2 *>(xflags)[k] = make_ulonglong2(sq2.w[0], sq2.w[Seq<K>::NW - 1]);
     }
 }
 
@@ -777,7 +775,7 @@ paired_fused_refine_kernel(int64_t n, const float *__restrict__ x1, const float 
         S.sq[(2 * K + 3) * kRefT + tid] = 0.f;
         FwdOut<K, true> r = iou_fwd<K, true, kP2Smem, true>(P, Q, QTable{S.sq + tid, S.sq + (K + 2) * kRefT + tid, kRefT});
         if (r.thin)
-            fwd_thin_fix<K>(RawPolyVerts{S.x1 + tid * K, S.y1 + tid * K, S.x2 + tid * K, S.y2 + tid * K}, r.seq,
+            fwd_thin_redo<K>(RawPolyVerts{S.x1 + tid * K, S.y1 + tid * K, S.x2 + tid * K, S.y2 + tid * K}, r.seq,
                             r.nx, r.iou);
         if (live && iou) iou[k] = r.iou;
         const float g = live ? (grad ? grad[k] : scale) : 0.f;

@@ -1,10 +1,10 @@
 """GPU parity on thin / sliver polygons (§V: "improve the numerical stability
 ... arbitrary shape input"; north_star tolerances): synth.gen_thin_pairs, aspect
-30-300, scene coordinates up to +-354 m, padded triangles / quads for K=4 and
+30-1000, scene coordinates up to +-354 m, padded triangles / quads for K=4 and
 octagon / pentagon slivers for K=8.  The float area sum of such pairs is
 ill-conditioned (~eps R^2 against an area ~R^2 / aspect); the kernels detect them
-(R^2 > kThinRatio A_u) and redo the area of the recorded intersection in double
-(csrc/dgal_exact.cuh).  IoU is compared on EVERY pair (R18), flags and vertex
+(R^2 > kThinRatio A_u) and redo the record and its area in double (record_exact,
+csrc/dgal_core.cuh; areas_exact, csrc/dgal_exact.cuh).  IoU is compared on EVERY pair (R18), flags and vertex
 gradients on the margin pairs (R13); padded vertices' gradients are folded onto
 the last real vertex (include/dgal.h)."""
 import numpy as np
@@ -18,7 +18,7 @@ from gpu_util import assert_flags_exact, assert_grad_close, assert_iou_close, de
 
 pytestmark = pytest.mark.gpu
 
-CASES = [(K, v, a) for K, v in ((4, 3), (4, 4), (8, 8), (8, 5)) for a in (30.0, 100.0, 300.0)]
+CASES = [(K, v, a) for K, v in ((4, 3), (4, 4), (8, 8), (8, 5)) for a in (30.0, 100.0, 300.0, 1000.0)]
 N = 20000
 
 
@@ -47,7 +47,7 @@ def test_thin_split_path(K, verts, aspect):
     assert (ref["iou"] > 0).mean() > 0.85             # the workload does overlap
     assert_iou_close(iou.cpu().numpy(), ref["iou"])
     ok = oracle.margin_ok(p1, p2)
-    assert ok.mean() > 0.5
+    assert ok.mean() > (0.5 if aspect < 1000 else 0.3)   # enough margin pairs to compare flags / gradients
     # flags of the padded polygons: indices of the real vertices / edges are the same
     # (the repeated vertex's zero-length edge never carries a crossing)
     nxk = nx.cpu().numpy()

@@ -48,6 +48,8 @@ def main(argv=None):
     ap.add_argument("--cubin", default="dgal_paired")
     ap.add_argument("--kernel", required=True)
     ap.add_argument("--mix", action="store_true")
+    ap.add_argument("--contains", default="LDGSTS",
+                    help="only loops whose body holds this opcode (the tile loop's prefetch); '' for any")
     a = ap.parse_args(argv)
     ins = kernel_sass(a.so, a.cubin, a.kernel)
     best = None
@@ -56,7 +58,9 @@ def main(argv=None):
             m = re.search(r"0x([0-9a-f]+)", rest)
             if m:
                 tgt = int(m.group(1), 16)
-                if tgt < off and (best is None or off - tgt > best[1] - best[0]):
+                has = not a.contains or any(o2 == a.contains or o2.startswith(a.contains + ".")
+                                            for o3, o2, _ in ins if tgt <= o3 <= off)
+                if tgt < off and has and (best is None or off - tgt > best[1] - best[0]):
                     best = (tgt, off)
     if best is None:
         print(f"{a.kernel}: total {len(ins)}, no backward branch")
