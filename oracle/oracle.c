@@ -237,6 +237,11 @@ static double iou_pair(int K, const vec2 *P, const vec2 *Q, isect_t *I,
     double A1 = shoelace(P, K), A2 = shoelace(Q, K);
     if (A1o) *A1o = A1;
     if (A2o) *A2o = A2;
+    /* |P1 n P2| <= min(|P1|, |P2|) (set inclusion): a polygon of zero area (all
+     * vertices equal: its zero-length edges constrain nothing, so the other polygon's
+     * vertices all test "inside" it) has an empty intersection, IoU 0 (0 <= IoU
+     * <= 1 always; without this a point p2 inside p1 gave IoU = A1 / rounding) */
+    if (!(A1 > 0.0) || !(A2 > 0.0)) { I->n = 0; I->area = 0.0; return 0.0; }
     double Au = A1 + A2 - I->area;
     if (I->n == 0 || !(Au > 0.0)) return 0.0;           /* R10 guard */
     return I->area / Au;

@@ -543,3 +543,22 @@ def test_scale_extremes(K, scale):
     assert_iou_close(iou_f.cpu().numpy(), ref["iou"])
     ok = oracle.margin_ok(p1, p2)
     assert_flags_exact(nx.cpu().numpy()[ok], xf.cpu().numpy()[ok], {"nx": ref["nx"][ok], "xflags": ref["xflags"][ok]})
+
+
+@pytest.mark.parametrize("K", [4, 8])
+def test_zero_area_polygons(K):
+    """Degenerate inputs of zero area (S:396 range, set inclusion): a point polygon inside
+    the other, in both roles, and a segment along an edge — IoU within 1e-5 of the
+    oracle's 0 (split and fused); identical polygons with a rotated vertex order give 1."""
+    b = synth.gen_config(3 if K == 4 else 4, 4096)
+    x, y = b.p1.x.reshape(-1, K), b.p1.y.reshape(-1, K)
+    cx, cy = np.repeat(x.mean(1, keepdims=True), K, 1), np.repeat(y.mean(1, keepdims=True), K, 1)
+    sx = np.concatenate([np.repeat(x[:, :1], K // 2, 1), np.repeat(x[:, 1:2], K // 2, 1)], 1)
+    sy = np.concatenate([np.repeat(y[:, :1], K // 2, 1), np.repeat(y[:, 1:2], K // 2, 1)], 1)
+    cases = [(x, y, cx, cy), (cx, cy, x, y), (x, y, sx, sy), (x, y, np.roll(x, 1, 1), np.roll(y, 1, 1))]
+    for a in cases:
+        X = [torch.from_numpy(np.ascontiguousarray(v.astype(np.float32))).to(dev()) for v in a]
+        ref = oracle.iou_paired_fwd(*[(X[i].cpu().numpy().astype(np.float64), X[i + 1].cpu().numpy().astype(np.float64))
+                                      for i in (0, 2)])
+        assert_iou_close(dgal.iou_paired_fwd(*X)[0].cpu().numpy(), ref["iou"])
+        assert_iou_close(dgal.iou_paired_fused(*X, scale=1.0)[0].cpu().numpy(), ref["iou"])

@@ -442,3 +442,16 @@ def test_translation_invariance_far_from_origin():
     g1 = oracle.iou_paired_bwd(far(p1), far(p2), g)
     for a, c in zip(g0, g1):
         assert np.max(np.abs(a - c)) <= 1e-9 * max(1.0, np.max(np.abs(a)))
+
+
+def test_zero_area_polygons_give_zero():
+    """S:396 (0 <= IoU <= 1 always) and set inclusion (|P1 n P2| <= min(|P1|, |P2|)): a
+    polygon of zero area — all vertices at one point inside the other, or on a segment
+    along its edge — intersects in nothing: IoU 0, nx 0, both argument orders."""
+    P = SQ * 2.0
+    pt = np.full((4, 2), 0.7)
+    seg = np.array([[0.0, 0.0], [0.0, 0.0], [2.0, 0.0], [2.0, 0.0]])
+    for Z in (pt, seg):
+        for a, b in ((P, Z), (Z, P)):
+            iou, nx, fl, ai = fwd1(a, b)
+            assert iou == 0.0 and nx == 0 and ai == 0.0
