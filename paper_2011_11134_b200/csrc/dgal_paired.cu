@@ -38,7 +38,9 @@ __device__ __forceinline__ void recentre(Poly<K> &P, Poly<K> &Q)
 // bulk-copy pipeline (tried: DESIGN.md §4.1) costs more in registers than the
 // latency it hides; for K = 8 it also spills.
 #ifndef DGAL_FWD4_MINB
-#define DGAL_FWD4_MINB 6     // CTAs per SM the K=4 forward is register-budgeted for
+#define DGAL_FWD4_MINB 7     // CTAs per SM the K=4 forward is register-budgeted for (72 registers,
+                             // 31.5 KB shared: 7 fit; A/B after the events-without-selects diet:
+                             // 0.3480 vs 0.3502 ms at 6, outputs bitwise equal)
 #endif
 #ifndef DGAL_FWD4_THREADS
 #define DGAL_FWD4_THREADS 128
