@@ -45,6 +45,10 @@
  * Example (offset unit squares p1 = [0,1]^2, p2 = p1 + (0.5, 0.5)):
  * C8 42 D3 80 = Cross(1,0) FromP1(2) Cross(2,3) FromP2(0) — NOT sorted by byte
  * value.  nx == 0 <=> empty intersection (IoU 0).
+ * Thin pairs (R^2 > 8 A_u, R the pair's extent about p1's vertex 0, A_u the union
+ * area: the float decisions and area sum are conditioned by R^2 / A_u) get their
+ * nx / xflags recomputed in double (the same rules) and their areas from that
+ * record in double, in every entry point below.
  */
 #ifndef DGAL_H_
 #define DGAL_H_
@@ -156,7 +160,7 @@ dgal_status dgal_iou_paired_host(int K, int64_t n,
  * conditioned by R^2 / A_u).  The first kernel queues them in `workspace` and a
  * second kernel, enqueued right after it, recomputes exactly those pairs with
  * the split path's arithmetic (dgal_iou_paired_fwd + _bwd: crossings refined in
- * double, thin areas in double), overwriting their iou and gradients.  Unqueued
+ * double, thin records and areas in double), overwriting their iou and gradients.  Unqueued
  * pairs: IoU bit-identical to dgal_iou_pairwise, gradients equal to the split
  * path's up to rounding.
  *   workspace        >= dgal_fused_workspace_bytes(n) bytes of device memory
