@@ -16,8 +16,10 @@
  *    dgal_iou_paired_host, takes host buffers); the library never allocates
  *    memory, never frees and never synchronises the host ("fix-size
  *    allocated memory"); its only state is a per-device cache of launch
- *    attributes (set once per kernel and device, thread-safe, idempotent) and
- *    the host-buffer call's three streams and four events.
+ *    attributes (set once per kernel and device, thread-safe, idempotent),
+ *    the host-buffer call's three streams and four events, and the indexed
+ *    pairwise call's side stream and two events (its grid build overlaps the
+ *    zero fill; fork / join with `stream`, capturable).
  *    Work is enqueued on `stream`
  *    (a cudaStream_t; NULL = legacy default stream).
  *  - Inputs are trusted: no CCW/convexity check on the device.

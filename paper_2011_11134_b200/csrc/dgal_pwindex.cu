@@ -4,6 +4,8 @@
 // found through a uniform grid over the column circles (counting sort built on
 // the device in a caller-provided workspace).  Exactness: disjoint bounding
 // circles => disjoint polygons => IoU 0, which the zero-fill already wrote.
+#include <mutex>
+
 #include "dgal_core.cuh"
 #include "dgal_internal.h"
 
@@ -448,6 +450,20 @@ pw_candidates(PwArgs a, Workspace w)
 
 }  // namespace
 
+namespace {
+// The grid build (two memsets and five small kernels, ~0.05 ms of launches and latency)
+// runs on a per-device, high-priority side stream, overlapping the output zero fill of the
+// caller's stream: fork / join events, so it stays ordered with the caller's stream and
+// capturable into a CUDA graph; the lock keeps one call's fork / join pairs together.
+struct SideStream {
+    std::mutex mu;
+    bool init = false;
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream g_side[kMaxDevices];
+}  // namespace
+
 size_t pairwise_workspace_bytes(int64_t m)
 {
     return align256(sizeof(GridHeader)) + align256(sizeof(PwState)) + 2 * align256(sizeof(float4) * (size_t)m) +
@@ -463,23 +479,40 @@ cudaError_t launch_pairwise_indexed(int K, int64_t n_rows, const float *rx, cons
     const Workspace w = carve(workspace, m);
     const PwArgs a{n_rows, rx, ry, m, cx, cy, row_offset, iou, thr, mask, mask_words, nbr_count, nbr_idx, cap};
     cudaError_t e;
-    // (1) zero-fill the outputs at streaming-write speed (nbr_count: zeroed as each
-    // row is claimed, claim_row)
-    if (iou) launch_zero(iou, sizeof(float) * (size_t)n_rows * m, st);
-    if (mask) launch_zero(mask, sizeof(uint64_t) * (size_t)n_rows * mask_words, st);
-    // (2) grid index of the column circles
-    if ((e = cudaMemsetAsync(w.start, 0, sizeof(int32_t) * (kGridMaxCells + 1), st))) return e;
-    if ((e = cudaMemsetAsync(w.fill, 0, sizeof(int32_t) * kGridMaxCells, st))) return e;
-    pw_init<<<1, 1, 0, st>>>(w);
-    const unsigned mg = (unsigned)((m + kThreads - 1) / kThreads);
-    if (K == 4) pw_circles<4><<<mg, kThreads, 0, st>>>(m, cx, cy, w);
-    else pw_circles<8><<<mg, kThreads, 0, st>>>(m, cx, cy, w);
-    pw_count<<<mg, kThreads, 0, st>>>(m, w);
-    pw_scan<<<1, 1024, 0, st>>>(w);
-    pw_scatter<<<mg, kThreads, 0, st>>>(m, w);
-    // (3) candidates: a persistent grid, warps claiming rows in order
     int dev = 0, sms = 0;
     if ((e = cudaGetDevice(&dev))) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    SideStream &ss = g_side[dev];
+    std::lock_guard<std::mutex> lock(ss.mu);
+    if (!ss.init) {
+        int lo = 0, hi = 0;
+        if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi))) return e;
+        if ((e = cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, hi))) return e;
+        if ((e = cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming))) return e;
+        if ((e = cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming))) return e;
+        ss.init = true;
+    }
+    // (2, side stream) grid index of the column circles, after everything before the call
+    if ((e = cudaEventRecord(ss.fork, st))) return e;
+    if ((e = cudaStreamWaitEvent(ss.s, ss.fork, 0))) return e;
+    const cudaStream_t gs = ss.s;
+    if ((e = cudaMemsetAsync(w.start, 0, sizeof(int32_t) * (kGridMaxCells + 1), gs))) return e;
+    if ((e = cudaMemsetAsync(w.fill, 0, sizeof(int32_t) * kGridMaxCells, gs))) return e;
+    pw_init<<<1, 1, 0, gs>>>(w);
+    const unsigned mg = (unsigned)((m + kThreads - 1) / kThreads);
+    if (K == 4) pw_circles<4><<<mg, kThreads, 0, gs>>>(m, cx, cy, w);
+    else pw_circles<8><<<mg, kThreads, 0, gs>>>(m, cx, cy, w);
+    pw_count<<<mg, kThreads, 0, gs>>>(m, w);
+    pw_scan<<<1, 1024, 0, gs>>>(w);
+    pw_scatter<<<mg, kThreads, 0, gs>>>(m, w);
+    if ((e = cudaGetLastError())) return e;
+    if ((e = cudaEventRecord(ss.join, gs))) return e;
+    // (1) meanwhile, zero-fill the outputs at streaming-write speed (nbr_count: zeroed as
+    // each row is claimed, claim_row)
+    if (iou) launch_zero(iou, sizeof(float) * (size_t)n_rows * m, st);
+    if (mask) launch_zero(mask, sizeof(uint64_t) * (size_t)n_rows * mask_words, st);
+    if ((e = cudaStreamWaitEvent(st, ss.join, 0))) return e;
+    // (3) candidates: a persistent grid, warps claiming rows in order
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (K == 4) pw_candidates<4><<<(unsigned)sms * 2, kThreads, 0, st>>>(a, w);
     else pw_candidates<8><<<(unsigned)sms, kThreads, 0, st>>>(a, w);
