@@ -613,6 +613,9 @@ cudaError_t launch_paired_bwd(int K, int64_t n, const float *x1, const float *y1
 #endif
 constexpr int kFused4Threads = DGAL_FUSED4_THREADS, kFused8Threads = DGAL_FUSED8_THREADS;
 
+#ifndef DGAL_FUSED_PT_TS
+#define DGAL_FUSED_PT_TS 1    // piece table [thread][slot] (1) or [slot][thread] (0)
+#endif
 #ifndef DGAL_FUSED_NEED
 #define DGAL_FUSED_NEED 1     // mark nearly parallel crossings / thin pairs for the refine pass (A/B switch)
 #endif
@@ -656,7 +659,10 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
     float *ring = fsm;
     float *gring = ring + (PF ? 2 * 4 * T * K : 0);
     float *pt = gring + (PF ? 2 * T : 0);
-    uint64_t *illt = reinterpret_cast<uint64_t *>(pt + 4 * K * T);   // K = 8: ILL factors, [q][thread]
+    // piece table: [thread][slot] with an odd per-thread stride kPtS (conflict-free; an
+    // event's address is one LEA) — x of a_j at j, of b_j at K + j, y at 2K + ...
+    constexpr int kPtS = DGAL_FUSED_PT_TS ? 4 * K + 1 : 1;
+    uint64_t *illt = reinterpret_cast<uint64_t *>(pt + (DGAL_FUSED_PT_TS ? kPtS * T : 4 * K * T));   // K = 8: ILL factors, [q][thread]
     const int tid = threadIdx.x;
     const int64_t k0 = (int64_t)blockIdx.x * (NT * T) + tid;
     auto prefetch = [&](int stage, int64_t k) {
@@ -705,7 +711,9 @@ paired_fused_kernel(int64_t n, const float *__restrict__ x1, const float *__rest
         recentre<K>(P, Q);
         bool need = false;
         const float v = iou_fused<K, DGAL_FUSED_P2MODE, K == 4 && DGAL_FUSED_PK>(
-            P, Q, g, G1, G2, flat(), nullptr, QTable{pt + tid, pt + 2 * K * T + tid, T},
+            P, Q, g, G1, G2, flat(), nullptr,
+            DGAL_FUSED_PT_TS ? QTable{pt + tid * kPtS, pt + tid * kPtS + 2 * K, 1}
+                             : QTable{pt + tid, pt + 2 * K * T + tid, T},
             DGAL_FUSED_NEED ? &need : nullptr, IllTab{illt + tid, T});
         refine_mark(refine, k, need);   // redone exactly by paired_fused_refine_kernel
         if (iou) __stcs(iou + k, v);
@@ -820,7 +828,8 @@ constexpr size_t fused_smem_bytes()
 {
     constexpr int T = (K == 4) ? kFused4Threads : kFused8Threads;
     constexpr bool PF = (K == 4) ? DGAL_FUSED_PF : DGAL_FUSED8_PF;
-    return sizeof(float) * ((PF ? 2 * 4 * T * K + 2 * T : 0) + 4 * K * T) + (K == 8 ? 8 * (K / 2) * T : 0);
+    return sizeof(float) * ((PF ? 2 * 4 * T * K + 2 * T : 0) + (DGAL_FUSED_PT_TS ? 4 * K + 1 : 4 * K) * T) +
+           (K == 8 ? 8 * (K / 2) * T : 0);
 }
 template <int K>
 cudaError_t launch_fused_k(int64_t n, const float *x1, const float *y1, const float *x2, const float *y2,

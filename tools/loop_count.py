@@ -54,7 +54,7 @@ def main(argv=None):
     ins = kernel_sass(a.so, a.cubin, a.kernel)
     best = None
     for off, op, rest in ins:
-        if op == "BRA":
+        if op == "BRA" or op.startswith("BRA."):
             m = re.search(r"0x([0-9a-f]+)", rest)
             if m:
                 tgt = int(m.group(1), 16)
